@@ -1,0 +1,148 @@
+/*
+ * mttkrp_b200.h — C ABI of the B200-native all-mode spMTTKRP library
+ * (libmttkrp_b200.so, built from paper_2503_18198_b200/csrc for sm_100a).
+ *
+ * The reference (arxiv 2503.18198 CPU model, /root/reference/proj/core) exposes no FFI:
+ * its boundary is the header-only C++ template API in namespace `mttkrp`.  Every entry
+ * point below replaces one call of that API; the reference file:line is cited on each.
+ * The C++ drop-in layer include/mttkrp_b200/mttkrp.hpp re-exposes the reference's names
+ * and exception messages on top of these functions.
+ *
+ * Conventions: plain pointers and sizes only; host buffers are caller-owned; every
+ * function returns an mk_status and on failure stores a message retrievable with
+ * mk_last_error() (thread-local).  A context is driven by one host thread at a time.
+ * Index type is uint32 (types.hpp:14), values fp32.
+ */
+#ifndef MTTKRP_B200_H
+#define MTTKRP_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  MK_OK = 0,
+  MK_EINVAL = 1,     /* argument / shape / plan validation (reference: throw mttkrp::error) */
+  MK_ENOMEM = 2,     /* device or host allocation failed */
+  MK_ECUDA = 3,      /* CUDA runtime / launch failure */
+  MK_ENONFINITE = 4, /* non-finite partial product (kernel.hpp:109-114) */
+  MK_ESTATE = 5,     /* call-order error (e.g. no tensor uploaded) */
+  MK_ENCCL = 6       /* multi-GPU collective failure */
+} mk_status;
+
+/* Scheme / Strategy / SchemePolicy enums (layout.hpp:17-24). */
+enum { MK_SCHEME1 = 1, MK_SCHEME2 = 2 };
+enum { MK_CYCLIC = 0, MK_LEAST_LOADED = 1 };
+enum { MK_ADAPTIVE = 0, MK_SCHEME1_ONLY = 1, MK_SCHEME2_ONLY = 2 };
+
+/* Execution flags for the MTTKRP entry points. */
+enum {
+  MK_EXEC_FAST = 0,          /* tile-parallel, atomics only on tile-split rows (1e-5 class) */
+  MK_EXEC_DETERMINISTIC = 1, /* one owner per output row, element order, no FMA:
+                                bitwise equal to ExecConfig{deterministic=true}
+                                (kernel.hpp:26-28) and to oracle_mttkrp (oracle.hpp:20-43) */
+};
+
+typedef struct mk_context mk_context;
+
+typedef struct {
+  int scheme;              /* MK_SCHEME1 / MK_SCHEME2 (ModePlan::scheme, layout.hpp:49) */
+  uint64_t kappa;          /* ModePlan::kappa */
+  uint64_t nnz;            /* ModePlan::nnz() */
+  uint64_t owned_total;    /* Σ owned_indices[z].size() (Scheme 1), 0 for Scheme 2 */
+  uint64_t distinct_rows;  /* DegreeProfile::distinct() (layout.hpp:38-42) */
+  uint64_t split_rows;     /* rows the fast kernel updates atomically (tile boundaries) */
+  uint64_t device_bytes;   /* bytes of the materialised mode copy on the device */
+} mk_plan_info;
+
+/* ---- library / context ------------------------------------------------------------ */
+const char* mk_last_error(void);
+const char* mk_version(void);
+int mk_device_count(int* count);
+int mk_create(int device, mk_context** out);
+int mk_destroy(mk_context* ctx);
+/* Run all work on an external CUDA stream (cudaStream_t passed as void*); NULL restores
+ * the context's own stream. */
+int mk_set_stream(mk_context* ctx, void* cuda_stream);
+int mk_synchronize(mk_context* ctx);
+
+/* ---- tensor: SparseTensorCOO<float>::from_parts (tensor.hpp:45-55) ---------------
+ * coords_aos is nnz × n_modes (element-major, tensor.hpp:80-82).  Validated on device
+ * with the reference's messages ("tensor: coordinate C out of range for mode H",
+ * "tensor: non-finite element value"). */
+int mk_tensor_upload(mk_context* ctx, uint32_t n_modes, const uint32_t* dims, uint64_t nnz,
+                     const uint32_t* coords_aos, const float* values);
+/* Σ val² of the uploaded tensor (||X||_F², for the CPD fit). */
+int mk_tensor_norm2(mk_context* ctx, double* norm2);
+
+/* ---- format build + partition: build_mode_plans (layout.hpp:131-149) ---------------
+ * Builds all N mode-specific copies on the device (GPU histogram + stable radix sorts,
+ * layout.cpp:76-183) and materialises each as SoA (N uint32 index arrays + fp32 values)
+ * in that mode's order. */
+int mk_build_plans(mk_context* ctx, uint64_t kappa, int strategy, int policy);
+int mk_get_plan_info(mk_context* ctx, uint32_t mode, mk_plan_info* info);
+/* ModePlan export (layout.hpp:47-64): order[nnz], partition_offsets[kappa+1],
+ * owned_flat[owned_total] (concatenated owned_indices), owned_offsets[kappa+1].
+ * Any output pointer may be NULL to skip it. */
+int mk_plan_export(mk_context* ctx, uint32_t mode, uint64_t* order, uint64_t* partition_offsets,
+                   uint32_t* owned_flat, uint64_t* owned_offsets);
+/* mode_degrees (layout.hpp:106-111): degrees[extent]. */
+int mk_mode_degrees(mk_context* ctx, uint32_t mode, uint64_t* degrees);
+/* The materialised mode copy (parity/inspection): idx is n_modes × nnz, mode-major. */
+int mk_copy_export(mk_context* ctx, uint32_t mode, uint32_t* idx, float* values);
+
+/* ---- factors: FactorMatrix<float> (factor.hpp:16-48), row-major I_d × R --------------- */
+int mk_factors_upload(mk_context* ctx, uint32_t rank, const float* const* factors);
+int mk_factor_upload(mk_context* ctx, uint32_t mode, const float* factor);
+int mk_factor_download(mk_context* ctx, uint32_t mode, float* factor);
+
+/* ---- spMTTKRP -------------------------------------------------------------------
+ * mttkrp_mode (kernel.hpp:161-169): one mode from the current factors into out[I_d × R]. */
+int mk_mttkrp_mode(mk_context* ctx, uint32_t mode, int exec, float* out);
+/* mttkrp_all_modes (kernel.hpp:177-197); chain != 0 feeds each output to later modes. */
+int mk_mttkrp_all_modes(mk_context* ctx, int chain, int exec, float* const* outs);
+/* Device-resident sweep (Algorithm 1): enqueue only, outputs stay in
+ * the context.  mk_synchronize() surfaces errors (non-finite detection). */
+int mk_sweep_async(mk_context* ctx, int chain, int exec);
+/* One mode of the sweep, enqueue only (reads the context's input factors). */
+int mk_mttkrp_mode_async(mk_context* ctx, uint32_t mode, int exec);
+int mk_output_download(mk_context* ctx, uint32_t mode, float* out);
+/* End-to-end step as a caller sees it: H2D of all factors from host memory, the sweep,
+ * D2H of all outputs, synchronise. */
+int mk_sweep_host(mk_context* ctx, const float* const* factors, float* const* outs, int chain,
+                  int exec);
+/* run_timed analogue (kernel.hpp:239-287) timed with CUDA events on the context stream.
+ * mode_ms[iters × N] and total_ms[iters]; flush_l2 writes a 2×L2 buffer between
+ * iterations (outside the timed events). */
+int mk_run_timed(mk_context* ctx, uint64_t iters, int exec, int flush_l2, double* mode_ms,
+                 double* total_ms);
+/* L2 flush as used by mk_run_timed (enqueued on the context stream). */
+int mk_flush_l2(mk_context* ctx);
+
+/* ---- CPD-ALS (absent in the reference; hook kernel.hpp:171-176) ----------
+ * One ALS iteration over all modes on the current factors: per mode d,
+ * M = MTTKRP(d); V = ⊛_{w≠d} Y_wᵀY_w; Y_d = M V⁻¹; column 2-norms -> lambda; then the
+ * fit 1 - ||X - X̂|| / ||X||.  lambda[R] may be NULL. */
+int mk_cpd_als_iter(mk_context* ctx, double* fit, float* lambda);
+/* Full driver: up to max_iters iterations, stops when |Δfit| < tol. */
+int mk_cpd_als(mk_context* ctx, uint64_t max_iters, double tol, double* fit,
+               uint64_t* iters_done, float* lambda);
+
+/* ---- host-side tensor ingest (synthetic.hpp:58-158, factor.hpp:71-84) ---------------
+ * Bit-identical to the reference generator (same draw sequence), multi-threaded dedup.
+ * dist: 0 uniform, 1 mode_skewed. */
+int mk_generate_synthetic(uint32_t n_modes, const uint32_t* dims, uint64_t nnz, int dist,
+                          uint64_t skew_mode, uint64_t skew_distinct, uint64_t seed,
+                          uint32_t* coords_aos, float* values);
+/* DESIGN.md §5 power-law (Zipf) generator for the nips-shaped config. */
+int mk_generate_powerlaw(uint32_t n_modes, const uint32_t* dims, uint64_t nnz, double exponent,
+                         uint64_t seed, uint32_t* coords_aos, float* values);
+int mk_random_factors(uint32_t n_modes, const uint32_t* dims, uint64_t rank, uint64_t seed,
+                      float* const* factors);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MTTKRP_B200_H */

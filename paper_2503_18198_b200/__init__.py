@@ -1,0 +1,666 @@
+"""B200-native all-mode spMTTKRP (arxiv 2503.18198) — Python host layer.
+
+This package mirrors the reference library's ``mttkrp`` namespace
+(/root/reference/proj/core/include/mttkrp) on top of the C ABI in
+``include/mttkrp_b200.h``, implemented by ``libmttkrp_b200.so`` (CUDA, sm_100a):
+
+=====================================  ===============================================
+reference (C++)                        here
+=====================================  ===============================================
+SparseTensorCOO<T>::from_parts         SparseTensorCOO.from_parts (tensor.hpp:45-55)
+generate_synthetic                     generate_synthetic (synthetic.hpp:58-158)
+random_factors                         random_factors (factor.hpp:71-84)
+build_mode_plans / ModePlan            build_mode_plans / ModePlan (layout.hpp:47-149)
+mode_degrees                           mode_degrees (layout.hpp:106-111)
+mttkrp_mode                            mttkrp_mode (kernel.hpp:161-169)
+mttkrp_all_modes                       mttkrp_all_modes (kernel.hpp:177-197)
+run_timed                              run_timed (kernel.hpp:239-287)
+verify_against / verify_tolerance      verify_against / verify_tolerance (verify.hpp)
+(absent)                   cpd_als / Context.cpd_als_iter
+=====================================  ===============================================
+
+Errors raise :class:`MttkrpError` (the reference's ``mttkrp::error``) with the
+reference's message texts.  There is no CPU fallback: every compute call goes through
+the CUDA library and fails loudly when it is missing or no GPU is present.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import enum
+import os
+import threading
+from dataclasses import dataclass, field
+from typing import List, Optional, Sequence
+
+import numpy as np
+
+__all__ = [
+    "MttkrpError", "Scheme", "Strategy", "SchemePolicy", "ExecConfig", "SparseTensorCOO",
+    "FactorMatrix", "ModePlan", "Context", "build_mode_plans", "mttkrp_mode",
+    "mttkrp_all_modes", "run_timed", "generate_synthetic", "generate_powerlaw",
+    "random_factors", "verify_against", "verify_tolerance", "mode_degrees", "cpd_als",
+    "load_library", "library_path", "EXPORTED_SYMBOLS",
+]
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+_LIB_NAME = "libmttkrp_b200.so"
+
+MK_OK, MK_EINVAL, MK_ENOMEM, MK_ECUDA, MK_ENONFINITE, MK_ESTATE, MK_ENCCL = range(7)
+EXEC_FAST, EXEC_DETERMINISTIC = 0, 1
+
+EXPORTED_SYMBOLS = [
+    "mk_last_error", "mk_version", "mk_device_count", "mk_create", "mk_destroy",
+    "mk_set_stream", "mk_synchronize", "mk_tensor_upload", "mk_tensor_norm2",
+    "mk_build_plans", "mk_get_plan_info", "mk_plan_export", "mk_mode_degrees",
+    "mk_copy_export", "mk_factors_upload", "mk_factor_upload", "mk_factor_download",
+    "mk_mttkrp_mode", "mk_mttkrp_all_modes", "mk_sweep_async", "mk_mttkrp_mode_async",
+    "mk_output_download",
+    "mk_sweep_host", "mk_run_timed", "mk_flush_l2", "mk_cpd_als_iter", "mk_cpd_als",
+    "mk_generate_synthetic", "mk_generate_powerlaw", "mk_random_factors",
+]
+
+
+class MttkrpError(RuntimeError):
+    """mttkrp::error (types.hpp:18-21).  ``status`` is the C-ABI mk_status."""
+
+    def __init__(self, msg: str, status: int = MK_EINVAL):
+        super().__init__(msg)
+        self.status = status
+
+
+class Scheme(enum.IntEnum):  # layout.hpp:17
+    scheme1 = 1
+    scheme2 = 2
+
+
+class Strategy(enum.IntEnum):  # layout.hpp:22
+    cyclic = 0
+    least_loaded = 1
+
+
+class SchemePolicy(enum.IntEnum):  # layout.hpp:24
+    adaptive = 0
+    scheme1_only = 1
+    scheme2_only = 2
+
+
+class _PlanInfo(C.Structure):
+    _fields_ = [("scheme", C.c_int), ("kappa", C.c_uint64), ("nnz", C.c_uint64),
+                ("owned_total", C.c_uint64), ("distinct_rows", C.c_uint64),
+                ("split_rows", C.c_uint64), ("device_bytes", C.c_uint64)]
+
+
+_lib_lock = threading.Lock()
+_lib_handle: Optional[C.CDLL] = None
+
+
+def library_path() -> str:
+    return os.path.join(HERE, _LIB_NAME)
+
+
+def load_library() -> C.CDLL:
+    """Load libmttkrp_b200.so (raises if it was not built — no fallback)."""
+    global _lib_handle
+    with _lib_lock:
+        if _lib_handle is not None:
+            return _lib_handle
+        path = library_path()
+        if not os.path.exists(path):
+            raise MttkrpError(f"CUDA extension not built: {path} (run __graft_entry__.build())",
+                              MK_ESTATE)
+        lib = C.CDLL(path)
+        vp, u32, u64, i32 = C.c_void_p, C.c_uint32, C.c_uint64, C.c_int
+        P = C.POINTER
+        sig = {
+            "mk_last_error": (C.c_char_p, []),
+            "mk_version": (C.c_char_p, []),
+            "mk_device_count": (i32, [P(i32)]),
+            "mk_create": (i32, [i32, P(vp)]),
+            "mk_destroy": (i32, [vp]),
+            "mk_set_stream": (i32, [vp, vp]),
+            "mk_synchronize": (i32, [vp]),
+            "mk_tensor_upload": (i32, [vp, u32, vp, u64, vp, vp]),
+            "mk_tensor_norm2": (i32, [vp, P(C.c_double)]),
+            "mk_build_plans": (i32, [vp, u64, i32, i32]),
+            "mk_get_plan_info": (i32, [vp, u32, P(_PlanInfo)]),
+            "mk_plan_export": (i32, [vp, u32, vp, vp, vp, vp]),
+            "mk_mode_degrees": (i32, [vp, u32, vp]),
+            "mk_copy_export": (i32, [vp, u32, vp, vp]),
+            "mk_factors_upload": (i32, [vp, u32, vp]),
+            "mk_factor_upload": (i32, [vp, u32, vp]),
+            "mk_factor_download": (i32, [vp, u32, vp]),
+            "mk_mttkrp_mode": (i32, [vp, u32, i32, vp]),
+            "mk_mttkrp_all_modes": (i32, [vp, i32, i32, vp]),
+            "mk_sweep_async": (i32, [vp, i32, i32]),
+            "mk_mttkrp_mode_async": (i32, [vp, u32, i32]),
+            "mk_output_download": (i32, [vp, u32, vp]),
+            "mk_sweep_host": (i32, [vp, vp, vp, i32, i32]),
+            "mk_run_timed": (i32, [vp, u64, i32, i32, vp, vp]),
+            "mk_flush_l2": (i32, [vp]),
+            "mk_cpd_als_iter": (i32, [vp, P(C.c_double), vp]),
+            "mk_cpd_als": (i32, [vp, u64, C.c_double, P(C.c_double), P(u64), vp]),
+            "mk_generate_synthetic": (i32, [u32, vp, u64, i32, u64, u64, u64, vp, vp]),
+            "mk_generate_powerlaw": (i32, [u32, vp, u64, C.c_double, u64, vp, vp]),
+            "mk_random_factors": (i32, [u32, vp, u64, u64, vp]),
+        }
+        for name, (res, args) in sig.items():
+            fn = getattr(lib, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib_handle = lib
+        return lib
+
+
+def _check(rc: int) -> None:
+    if rc != MK_OK:
+        msg = load_library().mk_last_error().decode()
+        raise MttkrpError(msg, rc)
+
+
+def _ptr(a: np.ndarray) -> int:
+    return a.ctypes.data
+
+
+def _ptr_array(arrs: Sequence[np.ndarray]):
+    return (C.c_void_p * len(arrs))(*[_ptr(a) for a in arrs])
+
+
+# ----------------------------------------------------------------------------- data model
+class SparseTensorCOO:
+    """COO tensor (tensor.hpp:34-111): shape + nnz×N uint32 coordinates + fp32 values."""
+
+    def __init__(self, dims: Sequence[int], coords=None, values=None, validate: bool = True):
+        dims = [int(d) for d in dims]
+        if not dims:
+            raise MttkrpError("shape: a tensor needs at least one mode")
+        if any(d <= 0 for d in dims):
+            raise MttkrpError("shape: zero extent")
+        if any(d > 0xFFFFFFFF for d in dims):
+            raise MttkrpError("shape: extent exceeds 2^32-1")
+        self.dims = dims
+        n = len(dims)
+        if coords is None:
+            coords = np.zeros((0, n), dtype=np.uint32)
+            values = np.zeros(0, dtype=np.float32)
+        coords = np.ascontiguousarray(np.asarray(coords, dtype=np.int64).reshape(-1, n)
+                                      if not (isinstance(coords, np.ndarray)
+                                              and coords.dtype == np.uint32)
+                                      else coords.reshape(-1, n))
+        values = np.ascontiguousarray(np.asarray(values, dtype=np.float32).reshape(-1))
+        if coords.shape[0] != values.shape[0]:
+            raise MttkrpError("tensor: coordinate/value storage size mismatch")
+        if validate:
+            self._validate(coords, values)
+        self.coords = np.ascontiguousarray(coords.astype(np.uint32, copy=False))
+        self.values = values
+        self._ctx: Optional["Context"] = None
+
+    from_parts = classmethod(lambda cls, dims, coords, values: cls(dims, coords, values))
+
+    def _validate(self, coords, values):  # tensor.hpp:97-106, first bad element first
+        if coords.size == 0:
+            return
+        dims = np.asarray(self.dims, dtype=np.int64)
+        c64 = coords.astype(np.int64, copy=False)
+        bad_c = (c64 < 0) | (c64 >= dims[None, :])
+        bad_row_c = bad_c.any(axis=1)
+        bad_v = ~np.isfinite(values)
+        first_c = int(np.argmax(bad_row_c)) if bad_row_c.any() else None
+        first_v = int(np.argmax(bad_v)) if bad_v.any() else None
+        if first_c is not None and (first_v is None or first_c <= first_v):
+            h = int(np.argmax(bad_c[first_c]))
+            raise MttkrpError(f"tensor: coordinate {int(c64[first_c, h])} out of range for mode {h}")
+        if first_v is not None:
+            raise MttkrpError("tensor: non-finite element value")
+
+    @property
+    def nnz(self) -> int:
+        return int(self.values.shape[0])
+
+    def mode_count(self) -> int:
+        return len(self.dims)
+
+    def extent(self, d: int) -> int:
+        return self.dims[d]
+
+    def index(self, i: int, mode: int) -> int:
+        return int(self.coords[i, mode])
+
+
+@dataclass
+class FactorMatrix:
+    """Dense row-major I_d × R factor (factor.hpp:16-48)."""
+    mode: int
+    data: np.ndarray  # float32 (rows, rank)
+
+    def __post_init__(self):
+        self.data = np.ascontiguousarray(np.asarray(self.data, dtype=np.float32))
+        if self.data.ndim != 2:
+            raise MttkrpError("factor: matrix must be 2-D")
+
+    @property
+    def rows(self) -> int:
+        return int(self.data.shape[0])
+
+    @property
+    def rank(self) -> int:
+        return int(self.data.shape[1])
+
+    @staticmethod
+    def zeros(mode: int, rows: int, rank: int) -> "FactorMatrix":
+        return FactorMatrix(mode, np.zeros((rows, rank), dtype=np.float32))
+
+    def at(self, i: int, r: int) -> float:
+        return float(self.data[i, r])
+
+
+@dataclass
+class ExecConfig:
+    """kernel.hpp:23-34.  kappa must match the plans; batch_p is accepted for API parity
+    (it has no semantic effect in the reference either, kernel.hpp:95-97)."""
+    kappa: int = 1
+    batch_p: int = 32
+    deterministic: bool = False
+
+    def validate(self):
+        if self.kappa < 1:
+            raise MttkrpError("kernel: kappa must be at least 1")
+        if self.batch_p < 1:
+            raise MttkrpError("kernel: batch size P must be at least 1")
+
+
+# ----------------------------------------------------------------------------- device context
+class Context:
+    """One mk_context: device-resident tensor, mode copies, factors and outputs."""
+
+    def __init__(self, device: int = 0):
+        self.lib = load_library()
+        h = C.c_void_p()
+        _check(self.lib.mk_create(device, C.byref(h)))
+        self.h = h
+        self.device = device
+        self.dims: List[int] = []
+        self.nnz = 0
+        self.rank = 0
+        self.kappa = 0
+        self._factor_key = None
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.lib.mk_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def set_stream(self, stream_ptr: Optional[int]):
+        _check(self.lib.mk_set_stream(self.h, C.c_void_p(stream_ptr or 0)))
+
+    def synchronize(self):
+        _check(self.lib.mk_synchronize(self.h))
+
+    # tensor / plans
+    def upload_tensor(self, t: SparseTensorCOO):
+        dims = np.asarray(t.dims, dtype=np.uint32)
+        _check(self.lib.mk_tensor_upload(self.h, len(t.dims), _ptr(dims), t.nnz, _ptr(t.coords),
+                                         _ptr(t.values)))
+        self.dims = list(t.dims)
+        self.nnz = t.nnz
+        self.rank = 0
+        self._factor_key = None
+
+    def norm2(self) -> float:
+        v = C.c_double()
+        _check(self.lib.mk_tensor_norm2(self.h, C.byref(v)))
+        return v.value
+
+    def build_plans(self, kappa: int, strategy=Strategy.cyclic, policy=SchemePolicy.adaptive):
+        if kappa < 1:
+            raise MttkrpError("layout: kappa must be at least 1")
+        _check(self.lib.mk_build_plans(self.h, int(kappa), int(strategy), int(policy)))
+        self.kappa = int(kappa)
+
+    def plan_info(self, mode: int) -> _PlanInfo:
+        info = _PlanInfo()
+        _check(self.lib.mk_get_plan_info(self.h, mode, C.byref(info)))
+        return info
+
+    def plan_export(self, mode: int):
+        info = self.plan_info(mode)
+        order = np.empty(max(self.nnz, 1), dtype=np.uint64)
+        offs = np.empty(info.kappa + 1, dtype=np.uint64)
+        owned = np.empty(max(info.owned_total, 1), dtype=np.uint32)
+        owned_off = np.empty(info.kappa + 1, dtype=np.uint64)
+        _check(self.lib.mk_plan_export(self.h, mode, _ptr(order), _ptr(offs), _ptr(owned),
+                                       _ptr(owned_off)))
+        return {"scheme": info.scheme, "order": order[:self.nnz], "offsets": offs,
+                "owned": owned[:info.owned_total], "owned_offsets": owned_off}
+
+    def copy_export(self, mode: int):
+        n = len(self.dims)
+        idx = np.empty((n, max(self.nnz, 1)), dtype=np.uint32)
+        vals = np.empty(max(self.nnz, 1), dtype=np.float32)
+        _check(self.lib.mk_copy_export(self.h, mode, _ptr(idx), _ptr(vals)))
+        return idx[:, :self.nnz], vals[:self.nnz]
+
+    def mode_degrees(self, mode: int) -> np.ndarray:
+        out = np.empty(self.dims[mode], dtype=np.uint64)
+        _check(self.lib.mk_mode_degrees(self.h, mode, _ptr(out)))
+        return out
+
+    # factors
+    def upload_factors(self, factors: Sequence[np.ndarray]):
+        mats = [np.ascontiguousarray(np.asarray(f, dtype=np.float32)) for f in factors]
+        rank = int(mats[0].shape[1])
+        _check(self.lib.mk_factors_upload(self.h, rank, _ptr_array(mats)))
+        self.rank = rank
+
+    def download_factor(self, mode: int) -> np.ndarray:
+        out = np.empty((self.dims[mode], self.rank), dtype=np.float32)
+        _check(self.lib.mk_factor_download(self.h, mode, _ptr(out)))
+        return out
+
+    # compute
+    def mttkrp_mode(self, mode: int, deterministic: bool = False) -> np.ndarray:
+        out = np.empty((self.dims[mode], self.rank), dtype=np.float32)
+        _check(self.lib.mk_mttkrp_mode(self.h, mode, int(deterministic), _ptr(out)))
+        return out
+
+    def mttkrp_all_modes(self, chain: bool = False, deterministic: bool = False):
+        outs = [np.empty((d, self.rank), dtype=np.float32) for d in self.dims]
+        _check(self.lib.mk_mttkrp_all_modes(self.h, int(chain), int(deterministic),
+                                            _ptr_array(outs)))
+        return outs
+
+    def sweep_async(self, chain: bool = False, deterministic: bool = False):
+        _check(self.lib.mk_sweep_async(self.h, int(chain), int(deterministic)))
+
+    def mttkrp_mode_async(self, mode: int, deterministic: bool = False):
+        _check(self.lib.mk_mttkrp_mode_async(self.h, mode, int(deterministic)))
+
+    def output(self, mode: int) -> np.ndarray:
+        out = np.empty((self.dims[mode], self.rank), dtype=np.float32)
+        _check(self.lib.mk_output_download(self.h, mode, _ptr(out)))
+        return out
+
+    def sweep_host(self, factors_host: Sequence[np.ndarray], outs_host: Sequence[np.ndarray],
+                   chain: bool = False, deterministic: bool = False):
+        _check(self.lib.mk_sweep_host(self.h, _ptr_array(factors_host), _ptr_array(outs_host),
+                                      int(chain), int(deterministic)))
+
+    def run_timed(self, iters: int, deterministic: bool = False, flush_l2: bool = True):
+        n = len(self.dims)
+        mode_ms = np.zeros((iters, n), dtype=np.float64)
+        total = np.zeros(iters, dtype=np.float64)
+        _check(self.lib.mk_run_timed(self.h, iters, int(deterministic), int(flush_l2),
+                                     _ptr(mode_ms), _ptr(total)))
+        return mode_ms, total
+
+    def flush_l2(self):
+        _check(self.lib.mk_flush_l2(self.h))
+
+    def cpd_als_iter(self):
+        fit = C.c_double()
+        lam = np.empty(self.rank, dtype=np.float32)
+        _check(self.lib.mk_cpd_als_iter(self.h, C.byref(fit), _ptr(lam)))
+        return fit.value, lam
+
+    def cpd_als(self, max_iters: int, tol: float = 1e-5):
+        fit = C.c_double()
+        done = C.c_uint64()
+        lam = np.empty(self.rank, dtype=np.float32)
+        _check(self.lib.mk_cpd_als(self.h, max_iters, tol, C.byref(fit), C.byref(done), _ptr(lam)))
+        return fit.value, int(done.value), lam
+
+
+# ----------------------------------------------------------------------------- plans
+class ModePlan:
+    """layout.hpp:47-64.  The copy lives on the device; order / offsets / owned indices
+    are exported on first access (bit-exact with the reference's ModePlan)."""
+
+    def __init__(self, ctx: Context, mode: int, tensor: SparseTensorCOO):
+        self._ctx = ctx
+        self._tensor = tensor
+        self.mode = mode
+        info = ctx.plan_info(mode)
+        self.scheme = Scheme(info.scheme)
+        self.kappa = int(info.kappa)
+        self._nnz = int(info.nnz)
+        self._export = None
+
+    def _ex(self):
+        if self._export is None:
+            self._export = self._ctx.plan_export(self.mode)
+        return self._export
+
+    @property
+    def order(self) -> np.ndarray:
+        return self._ex()["order"]
+
+    @property
+    def partition_offsets(self) -> np.ndarray:
+        return self._ex()["offsets"]
+
+    @property
+    def owned_indices(self) -> List[np.ndarray]:
+        ex = self._ex()
+        if self.scheme != Scheme.scheme1:
+            return []
+        o, off = ex["owned"], ex["owned_offsets"]
+        return [o[int(off[z]):int(off[z + 1])] for z in range(self.kappa)]
+
+    def nnz(self) -> int:
+        return self._nnz
+
+    def partition_size(self, z: int) -> int:
+        off = self.partition_offsets
+        return int(off[z + 1] - off[z])
+
+
+def _context_for(t: SparseTensorCOO) -> Context:
+    if t._ctx is None:
+        t._ctx = Context()
+        t._ctx.upload_tensor(t)
+    return t._ctx
+
+
+def build_mode_plans(t: SparseTensorCOO, kappa: int, strategy=Strategy.cyclic,
+                     policy=SchemePolicy.adaptive) -> List[ModePlan]:
+    """layout.hpp:131-149 — all N mode copies built on the device."""
+    if kappa < 1:
+        raise MttkrpError("layout: kappa must be at least 1")
+    ctx = _context_for(t)
+    ctx.build_plans(kappa, strategy, policy)
+    return [ModePlan(ctx, d, t) for d in range(t.mode_count())]
+
+
+def mode_degrees(t: SparseTensorCOO, d: int) -> np.ndarray:
+    """layout.hpp:106-111 (needs plans built for the tensor)."""
+    if d >= t.mode_count():
+        raise MttkrpError("layout: mode out of range")
+    return _context_for(t).mode_degrees(d)
+
+
+# ----------------------------------------------------------------------------- kernels
+def _validate_factors(t: SparseTensorCOO, factors: Sequence[FactorMatrix]):  # kernel.hpp:44-61
+    if len(factors) != t.mode_count():
+        raise MttkrpError("kernel: expected one factor matrix per mode")
+    rank = factors[0].rank if factors else 0
+    if rank < 1:
+        raise MttkrpError("kernel: rank must be at least 1")
+    for w, f in enumerate(factors):
+        if f.mode != w:
+            raise MttkrpError(f"kernel: factor matrix {w} labeled mode {f.mode}")
+        if f.rows != t.extent(w):
+            raise MttkrpError(f"kernel: factor matrix {w} has {f.rows} rows, tensor extent is "
+                              f"{t.extent(w)}")
+        if f.rank != rank:
+            raise MttkrpError("kernel: factor matrices disagree on rank")
+
+
+def _validate_plan(t: SparseTensorCOO, plan: ModePlan, config: ExecConfig):  # kernel.hpp:63-73
+    if plan.mode >= t.mode_count():
+        raise MttkrpError("kernel: plan mode out of range")
+    if plan._tensor is not t or plan.nnz() != t.nnz:
+        raise MttkrpError("kernel: plan does not cover this tensor")
+    off = plan.partition_offsets
+    if len(off) != plan.kappa + 1 or int(off[0]) != 0 or int(off[-1]) != t.nnz:
+        raise MttkrpError("kernel: malformed partition offsets")
+    if plan.kappa != config.kappa:
+        raise MttkrpError(f"kernel: plan built for kappa {plan.kappa}, config requests "
+                          f"{config.kappa}")
+
+
+def _as_factors(factors) -> List[FactorMatrix]:
+    return [f if isinstance(f, FactorMatrix) else FactorMatrix(i, f) for i, f in enumerate(factors)]
+
+
+def _upload_if_changed(ctx: Context, factors: Sequence[FactorMatrix]):
+    ctx.upload_factors([f.data for f in factors])
+
+
+def mttkrp_mode(t: SparseTensorCOO, plan: ModePlan, factors, config: ExecConfig) -> FactorMatrix:
+    """kernel.hpp:161-169 on the device."""
+    factors = _as_factors(factors)
+    config.validate()
+    _validate_factors(t, factors)
+    _validate_plan(t, plan, config)
+    ctx = plan._ctx
+    _upload_if_changed(ctx, factors)
+    return FactorMatrix(plan.mode, ctx.mttkrp_mode(plan.mode, config.deterministic))
+
+
+def mttkrp_all_modes(t: SparseTensorCOO, plans: Sequence[ModePlan], factors, config: ExecConfig,
+                     chain_outputs: bool) -> List[FactorMatrix]:
+    """kernel.hpp:177-197 on the device (stream order = the global barrier)."""
+    factors = _as_factors(factors)
+    if len(plans) != t.mode_count():
+        raise MttkrpError("kernel: expected one plan per mode")
+    for d, p in enumerate(plans):
+        if p.mode != d:
+            raise MttkrpError("kernel: plans out of mode order")
+    config.validate()
+    _validate_factors(t, factors)
+    for p in plans:
+        _validate_plan(t, p, config)
+    ctx = plans[0]._ctx
+    _upload_if_changed(ctx, factors)
+    outs = ctx.mttkrp_all_modes(chain_outputs, config.deterministic)
+    return [FactorMatrix(d, o) for d, o in enumerate(outs)]
+
+
+@dataclass
+class ModeTiming:  # kernel.hpp:199-207
+    mode: int
+    scheme: Scheme
+    wall_ms: List[float]
+    min_ms: float
+    median_ms: float
+    busy_workers: int
+    elements_per_worker: List[int]
+
+
+@dataclass
+class TimingReport:  # kernel.hpp:209-218
+    iters: int
+    modes: List[ModeTiming]
+    total_ms: List[float]
+    total_min_ms: float
+    total_median_ms: float
+    outputs_bit_identical: bool = True
+
+
+def run_timed(t: SparseTensorCOO, plans: Sequence[ModePlan], factors, config: ExecConfig,
+              iters: int, flush_l2: bool = True):
+    """kernel.hpp:239-287: per-mode times from CUDA events (the reference uses
+    steady_clock around each host call).  Returns (TimingReport, outputs)."""
+    if iters < 1:
+        raise MttkrpError("kernel: iters must be at least 1")
+    factors = _as_factors(factors)
+    config.validate()
+    _validate_factors(t, factors)
+    for p in plans:
+        _validate_plan(t, p, config)
+    ctx = plans[0]._ctx
+    _upload_if_changed(ctx, factors)
+    mode_ms, total = ctx.run_timed(iters, config.deterministic, flush_l2)
+    modes = []
+    for d, p in enumerate(plans):
+        sizes = [p.partition_size(z) for z in range(p.kappa)]
+        w = [float(x) for x in mode_ms[:, d]]
+        modes.append(ModeTiming(d, p.scheme, w, min(w), float(np.median(w)),
+                                sum(1 for s in sizes if s > 0), sizes))
+    report = TimingReport(iters, modes, [float(x) for x in total], float(total.min()),
+                          float(np.median(total)))
+    outs = [FactorMatrix(d, ctx.output(d)) for d in range(t.mode_count())]
+    return report, outs
+
+
+def cpd_als(t: SparseTensorCOO, plans: Sequence[ModePlan], factors, max_iters: int,
+            tol: float = 1e-5):
+    """CPD-ALS driver on the device (no reference counterpart)."""
+    factors = _as_factors(factors)
+    _validate_factors(t, factors)
+    ctx = plans[0]._ctx
+    ctx.upload_factors([f.data for f in factors])
+    fit, iters, lam = ctx.cpd_als(max_iters, tol)
+    out = [FactorMatrix(d, ctx.download_factor(d)) for d in range(t.mode_count())]
+    return fit, iters, lam, out
+
+
+# ----------------------------------------------------------------------------- ingest (host)
+def generate_synthetic(dims, nnz, dist="uniform", skew_mode=0, skew_distinct=2,
+                       seed=0) -> SparseTensorCOO:
+    """synthetic.hpp:58-158, bit-identical (host C++ in libmttkrp_b200.so)."""
+    lib = load_library()
+    d = np.asarray(dims, dtype=np.uint32)
+    coords = np.empty((nnz, len(dims)), dtype=np.uint32)
+    vals = np.empty(nnz, dtype=np.float32)
+    dist_i = {"uniform": 0, "mode_skewed": 1}[dist] if isinstance(dist, str) else int(dist)
+    _check(lib.mk_generate_synthetic(len(dims), _ptr(d), nnz, dist_i, skew_mode, skew_distinct,
+                                     seed, _ptr(coords), _ptr(vals)))
+    return SparseTensorCOO(dims, coords, vals, validate=False)
+
+
+def generate_powerlaw(dims, nnz, exponent=1.0, seed=0) -> SparseTensorCOO:
+    """DESIGN.md §5 power-law generator (nips-shaped config)."""
+    lib = load_library()
+    d = np.asarray(dims, dtype=np.uint32)
+    coords = np.empty((nnz, len(dims)), dtype=np.uint32)
+    vals = np.empty(nnz, dtype=np.float32)
+    _check(lib.mk_generate_powerlaw(len(dims), _ptr(d), nnz, float(exponent), seed,
+                                    _ptr(coords), _ptr(vals)))
+    return SparseTensorCOO(dims, coords, vals, validate=False)
+
+
+def random_factors(dims, rank, seed) -> List[FactorMatrix]:
+    """factor.hpp:71-84, bit-identical."""
+    lib = load_library()
+    if rank < 1:
+        raise MttkrpError("factor: rank must be at least 1")
+    d = np.asarray(dims, dtype=np.uint32)
+    mats = [np.empty((int(x), rank), dtype=np.float32) for x in dims]
+    _check(lib.mk_random_factors(len(dims), _ptr(d), rank, seed, _ptr_array(mats)))
+    return [FactorMatrix(i, m) for i, m in enumerate(mats)]
+
+
+# ----------------------------------------------------------------------------- verify
+def verify_against(got, want):
+    """verify.hpp:21-39: (max_rel_err, worst_row, worst_col) with |g-w|/max(1,|w|)."""
+    g = np.asarray(got.data if isinstance(got, FactorMatrix) else got, dtype=np.float64)
+    w = np.asarray(want.data if isinstance(want, FactorMatrix) else want, dtype=np.float64)
+    if g.shape != w.shape:
+        raise MttkrpError("verify: matrix shapes differ")
+    if g.size == 0:
+        return 0.0, 0, 0
+    err = np.abs(g - w) / np.maximum(1.0, np.abs(w))
+    k = int(np.argmax(err))
+    return float(err.reshape(-1)[k]), k // g.shape[1], k % g.shape[1]
+
+
+def verify_tolerance(dtype=np.float32) -> float:
+    """verify.hpp:42-45."""
+    return 1e-5 if np.dtype(dtype).itemsize == 4 else 1e-12

@@ -1,0 +1,501 @@
+// C-ABI entry points (include/mttkrp_b200.h).  Each converts internal exceptions into an
+// mk_status plus a thread-local message, mirroring how the reference surfaces
+// mttkrp::error (types.hpp:18-21).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "context.cuh"
+
+struct mk_context {
+  mkb::Context c;
+};
+
+namespace mkb {
+thread_local std::string g_last_error;
+std::string& last_error_ref() { return g_last_error; }
+
+template <typename F>
+int guarded(F&& f) {
+  try {
+    f();
+    g_last_error.clear();
+    return MK_OK;
+  } catch (const Error& e) {
+    g_last_error = e.what();
+    return e.status;
+  } catch (const std::bad_alloc&) {
+    g_last_error = "host allocation failed";
+    return MK_ENOMEM;
+  } catch (const std::exception& e) {
+    g_last_error = e.what();
+    return MK_EINVAL;
+  }
+}
+
+void need_ctx(mk_context* ctx) {
+  if (!ctx) fail(MK_EINVAL, "null context");
+  MKB_CUDA(cudaSetDevice(ctx->c.device));
+}
+void need_plans(Context& c) {
+  if (!c.plans_built) fail(MK_ESTATE, "kernel: plans not built (call mk_build_plans)");
+}
+void need_mode(Context& c, uint32_t mode) {
+  if (mode >= c.n) fail(MK_EINVAL, "kernel: plan mode out of range");
+}
+void need_factors(Context& c) {
+  if (c.rank == 0) fail(MK_ESTATE, "kernel: factors not uploaded");
+  for (uint32_t w = 0; w < c.n; ++w)
+    if (!c.factors_set[w]) fail(MK_ESTATE, "kernel: expected one factor matrix per mode");
+}
+
+void check_nonfinite(Context& c) {
+  unsigned long long tagged = ~0ull;
+  MKB_CUDA(cudaMemcpyAsync(&tagged, c.nonfinite.get(), sizeof tagged, cudaMemcpyDeviceToHost,
+                           c.stream));
+  MKB_CUDA(cudaStreamSynchronize(c.stream));
+  if (tagged != ~0ull) {
+    const uint64_t mode = tagged >> 32, pos = tagged & 0xffffffffull;
+    uint32_t elem = 0;
+    MKB_CUDA(cudaMemcpy(&elem, c.copies[mode].order.get() + pos, sizeof elem,
+                        cudaMemcpyDeviceToHost));
+    fail(MK_ENONFINITE, "kernel: non-finite partial product at tensor element " +
+                            std::to_string(elem) + " (mode " + std::to_string(mode) +
+                            ", copy position " + std::to_string(pos) + ")");
+  }
+}
+
+// One sweep of Algorithm 1: modes in order, stream order is the global
+// barrier.  With chain, later modes read the fresh outputs of earlier modes
+// (kernel.hpp:186-195).  Non-finite detection reports the first failing mode.
+void sweep(Context& c, int chain, int exec) {
+  const float* in[kMaxModes];
+  for (uint32_t w = 0; w < c.n; ++w) in[w] = c.factors[w].get();
+  for (uint32_t d = 0; d < c.n; ++d) {
+    launch_mttkrp(c, d, in, c.outputs[d].get(), exec);
+    if (chain) in[d] = c.outputs[d].get();
+  }
+}
+
+}  // namespace mkb
+
+using namespace mkb;
+
+extern "C" {
+
+const char* mk_last_error(void) { return g_last_error.c_str(); }
+const char* mk_version(void) { return "mttkrp_b200 0.1 (sm_100a)"; }
+
+int mk_device_count(int* count) {
+  return guarded([&] { MKB_CUDA(cudaGetDeviceCount(count)); });
+}
+
+int mk_create(int device, mk_context** out) {
+  return guarded([&] {
+    if (!out) fail(MK_EINVAL, "null output");
+    *out = nullptr;
+    MKB_CUDA(cudaSetDevice(device));
+    auto* ctx = new mk_context();
+    Context& c = ctx->c;
+    c.device = device;
+    try {
+      MKB_CUDA(cudaStreamCreateWithFlags(&c.own_stream, cudaStreamNonBlocking));
+      c.stream = c.own_stream;
+      MKB_CUDA(cudaDeviceGetAttribute(&c.num_sms, cudaDevAttrMultiProcessorCount, device));
+      int l2 = 0;
+      MKB_CUDA(cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, device));
+      c.l2_bytes = static_cast<size_t>(l2);
+      reset_nonfinite(c);
+    } catch (...) {
+      delete ctx;
+      throw;
+    }
+    *out = ctx;
+  });
+}
+
+int mk_destroy(mk_context* ctx) {
+  return guarded([&] {
+    if (!ctx) return;
+    cudaSetDevice(ctx->c.device);
+    cudaStreamSynchronize(ctx->c.stream);
+    cudaStream_t own = ctx->c.own_stream;
+    delete ctx;
+    if (own) cudaStreamDestroy(own);
+  });
+}
+
+int mk_set_stream(mk_context* ctx, void* stream) {
+  return guarded([&] {
+    need_ctx(ctx);
+    ctx->c.stream = stream ? static_cast<cudaStream_t>(stream) : ctx->c.own_stream;
+  });
+}
+
+int mk_synchronize(mk_context* ctx) {
+  return guarded([&] {
+    need_ctx(ctx);
+    MKB_CUDA(cudaStreamSynchronize(ctx->c.stream));
+    check_nonfinite(ctx->c);
+  });
+}
+
+int mk_tensor_upload(mk_context* ctx, uint32_t n, const uint32_t* dims, uint64_t nnz,
+                     const uint32_t* coords, const float* values) {
+  return guarded([&] {
+    need_ctx(ctx);
+    if (!dims) fail(MK_EINVAL, "shape: null dims");
+    tensor_upload(ctx->c, n, dims, nnz, coords, values);
+  });
+}
+
+int mk_tensor_norm2(mk_context* ctx, double* norm2) {
+  return guarded([&] {
+    need_ctx(ctx);
+    *norm2 = ctx->c.norm2;
+  });
+}
+
+int mk_build_plans(mk_context* ctx, uint64_t kappa, int strategy, int policy) {
+  return guarded([&] {
+    need_ctx(ctx);
+    if (strategy != MK_CYCLIC && strategy != MK_LEAST_LOADED)
+      fail(MK_EINVAL, "layout: unknown strategy");
+    if (policy < MK_ADAPTIVE || policy > MK_SCHEME2_ONLY) fail(MK_EINVAL, "layout: unknown policy");
+    build_plans(ctx->c, kappa, strategy, policy);
+  });
+}
+
+int mk_get_plan_info(mk_context* ctx, uint32_t mode, mk_plan_info* info) {
+  return guarded([&] {
+    need_ctx(ctx);
+    Context& c = ctx->c;
+    need_plans(c);
+    need_mode(c, mode);
+    const ModeCopy& mc = c.copies[mode];
+    info->scheme = mc.scheme;
+    info->kappa = mc.kappa;
+    info->nnz = c.nnz;
+    info->owned_total = mc.owned_total;
+    info->distinct_rows = mc.distinct;
+    info->split_rows = mc.n_split_rows;
+    uint64_t b = 0;
+    for (uint32_t w = 0; w < c.n; ++w) b += mc.idx[w].bytes();
+    b += mc.val.bytes();
+    info->device_bytes = b;
+  });
+}
+
+int mk_plan_export(mk_context* ctx, uint32_t mode, uint64_t* order, uint64_t* partition_offsets,
+                   uint32_t* owned_flat, uint64_t* owned_offsets) {
+  return guarded([&] {
+    need_ctx(ctx);
+    Context& c = ctx->c;
+    need_plans(c);
+    need_mode(c, mode);
+    const ModeCopy& mc = c.copies[mode];
+    if (order && c.nnz) {
+      std::vector<uint32_t> o(c.nnz);
+      MKB_CUDA(cudaMemcpyAsync(o.data(), mc.order.get(), c.nnz * sizeof(uint32_t),
+                               cudaMemcpyDeviceToHost, c.stream));
+      MKB_CUDA(cudaStreamSynchronize(c.stream));
+      for (uint64_t j = 0; j < c.nnz; ++j) order[j] = o[j];
+    }
+    if (partition_offsets)
+      std::memcpy(partition_offsets, mc.partition_offsets.data(),
+                  (mc.kappa + 1) * sizeof(uint64_t));
+    if (owned_offsets) {
+      if (mc.scheme == MK_SCHEME1)
+        std::memcpy(owned_offsets, mc.owned_offsets.data(), (mc.kappa + 1) * sizeof(uint64_t));
+      else
+        std::fill(owned_offsets, owned_offsets + mc.kappa + 1, 0ull);
+    }
+    if (owned_flat && mc.scheme == MK_SCHEME1 && mc.owned_total) {
+      MKB_CUDA(cudaMemcpyAsync(owned_flat, mc.row_seq.get(), mc.owned_total * sizeof(uint32_t),
+                               cudaMemcpyDeviceToHost, c.stream));
+      MKB_CUDA(cudaStreamSynchronize(c.stream));
+    }
+  });
+}
+
+int mk_mode_degrees(mk_context* ctx, uint32_t mode, uint64_t* degrees) {
+  return guarded([&] {
+    need_ctx(ctx);
+    Context& c = ctx->c;
+    need_plans(c);
+    need_mode(c, mode);
+    const uint32_t ext = c.dims[mode];
+    std::vector<uint32_t> d(ext);
+    MKB_CUDA(cudaMemcpyAsync(d.data(), c.copies[mode].degrees.get(), ext * sizeof(uint32_t),
+                             cudaMemcpyDeviceToHost, c.stream));
+    MKB_CUDA(cudaStreamSynchronize(c.stream));
+    for (uint32_t i = 0; i < ext; ++i) degrees[i] = d[i];
+  });
+}
+
+int mk_copy_export(mk_context* ctx, uint32_t mode, uint32_t* idx, float* values) {
+  return guarded([&] {
+    need_ctx(ctx);
+    Context& c = ctx->c;
+    need_plans(c);
+    need_mode(c, mode);
+    if (!c.nnz) return;
+    const ModeCopy& mc = c.copies[mode];
+    for (uint32_t w = 0; w < c.n && idx; ++w)
+      MKB_CUDA(cudaMemcpyAsync(idx + static_cast<uint64_t>(w) * c.nnz, mc.idx[w].get(),
+                               c.nnz * sizeof(uint32_t), cudaMemcpyDeviceToHost, c.stream));
+    if (values)
+      MKB_CUDA(cudaMemcpyAsync(values, mc.val.get(), c.nnz * sizeof(float), cudaMemcpyDeviceToHost,
+                               c.stream));
+    MKB_CUDA(cudaStreamSynchronize(c.stream));
+  });
+}
+
+int mk_factors_upload(mk_context* ctx, uint32_t rank, const float* const* factors) {
+  return guarded([&] {
+    need_ctx(ctx);
+    Context& c = ctx->c;
+    if (c.n == 0) fail(MK_ESTATE, "kernel: no tensor uploaded");
+    if (rank < 1) fail(MK_EINVAL, "kernel: rank must be at least 1");
+    if (!factors) fail(MK_EINVAL, "kernel: expected one factor matrix per mode");
+    c.rank = rank;
+    for (uint32_t w = 0; w < c.n; ++w) {
+      const size_t cnt = static_cast<size_t>(c.dims[w]) * rank;
+      c.factors[w].resize(cnt);
+      c.outputs[w].resize(cnt);
+      if (!factors[w]) fail(MK_EINVAL, "kernel: expected one factor matrix per mode");
+      MKB_CUDA(cudaMemcpyAsync(c.factors[w].get(), factors[w], cnt * sizeof(float),
+                               cudaMemcpyHostToDevice, c.stream));
+      c.factors_set[w] = true;
+    }
+    c.grams_valid = false;
+    MKB_CUDA(cudaStreamSynchronize(c.stream));
+  });
+}
+
+int mk_factor_upload(mk_context* ctx, uint32_t mode, const float* factor) {
+  return guarded([&] {
+    need_ctx(ctx);
+    Context& c = ctx->c;
+    need_mode(c, mode);
+    if (c.rank == 0) fail(MK_ESTATE, "kernel: factors not uploaded");
+    c.grams_valid = false;
+    MKB_CUDA(cudaMemcpyAsync(c.factors[mode].get(), factor,
+                             static_cast<size_t>(c.dims[mode]) * c.rank * sizeof(float),
+                             cudaMemcpyHostToDevice, c.stream));
+    MKB_CUDA(cudaStreamSynchronize(c.stream));
+  });
+}
+
+int mk_factor_download(mk_context* ctx, uint32_t mode, float* factor) {
+  return guarded([&] {
+    need_ctx(ctx);
+    Context& c = ctx->c;
+    need_mode(c, mode);
+    if (c.rank == 0) fail(MK_ESTATE, "kernel: factors not uploaded");
+    MKB_CUDA(cudaMemcpyAsync(factor, c.factors[mode].get(),
+                             static_cast<size_t>(c.dims[mode]) * c.rank * sizeof(float),
+                             cudaMemcpyDeviceToHost, c.stream));
+    MKB_CUDA(cudaStreamSynchronize(c.stream));
+  });
+}
+
+int mk_mttkrp_mode(mk_context* ctx, uint32_t mode, int exec, float* out) {
+  return guarded([&] {
+    need_ctx(ctx);
+    Context& c = ctx->c;
+    need_plans(c);
+    need_mode(c, mode);
+    need_factors(c);
+    const float* in[kMaxModes];
+    for (uint32_t w = 0; w < c.n; ++w) in[w] = c.factors[w].get();
+    reset_nonfinite(c);
+    launch_mttkrp(c, mode, in, c.outputs[mode].get(), exec);
+    check_nonfinite(c);
+    if (out)
+      MKB_CUDA(cudaMemcpyAsync(out, c.outputs[mode].get(),
+                               static_cast<size_t>(c.dims[mode]) * c.rank * sizeof(float),
+                               cudaMemcpyDeviceToHost, c.stream));
+    MKB_CUDA(cudaStreamSynchronize(c.stream));
+  });
+}
+
+static void all_modes_checked(Context& c, int chain, int exec) {
+  // Run mode by mode so a non-finite product is attributed to its mode, exactly as the
+  // reference throws from inside the failing mode's executor.
+  const float* in[kMaxModes];
+  for (uint32_t w = 0; w < c.n; ++w) in[w] = c.factors[w].get();
+  for (uint32_t d = 0; d < c.n; ++d) {
+    reset_nonfinite(c);
+    launch_mttkrp(c, d, in, c.outputs[d].get(), exec);
+    check_nonfinite(c);
+    if (chain) in[d] = c.outputs[d].get();
+  }
+}
+
+int mk_mttkrp_all_modes(mk_context* ctx, int chain, int exec, float* const* outs) {
+  return guarded([&] {
+    need_ctx(ctx);
+    Context& c = ctx->c;
+    need_plans(c);
+    need_factors(c);
+    all_modes_checked(c, chain, exec);
+    for (uint32_t d = 0; d < c.n && outs; ++d)
+      if (outs[d])
+        MKB_CUDA(cudaMemcpyAsync(outs[d], c.outputs[d].get(),
+                                 static_cast<size_t>(c.dims[d]) * c.rank * sizeof(float),
+                                 cudaMemcpyDeviceToHost, c.stream));
+    MKB_CUDA(cudaStreamSynchronize(c.stream));
+  });
+}
+
+int mk_sweep_async(mk_context* ctx, int chain, int exec) {
+  return guarded([&] {
+    need_ctx(ctx);
+    Context& c = ctx->c;
+    need_plans(c);
+    need_factors(c);
+    sweep(c, chain, exec);
+  });
+}
+
+int mk_mttkrp_mode_async(mk_context* ctx, uint32_t mode, int exec) {
+  return guarded([&] {
+    need_ctx(ctx);
+    Context& c = ctx->c;
+    need_plans(c);
+    need_mode(c, mode);
+    need_factors(c);
+    const float* in[kMaxModes];
+    for (uint32_t w = 0; w < c.n; ++w) in[w] = c.factors[w].get();
+    launch_mttkrp(c, mode, in, c.outputs[mode].get(), exec);
+  });
+}
+
+int mk_output_download(mk_context* ctx, uint32_t mode, float* out) {
+  return guarded([&] {
+    need_ctx(ctx);
+    Context& c = ctx->c;
+    need_mode(c, mode);
+    if (c.rank == 0) fail(MK_ESTATE, "kernel: factors not uploaded");
+    MKB_CUDA(cudaMemcpyAsync(out, c.outputs[mode].get(),
+                             static_cast<size_t>(c.dims[mode]) * c.rank * sizeof(float),
+                             cudaMemcpyDeviceToHost, c.stream));
+    MKB_CUDA(cudaStreamSynchronize(c.stream));
+  });
+}
+
+int mk_sweep_host(mk_context* ctx, const float* const* factors, float* const* outs, int chain,
+                  int exec) {
+  return guarded([&] {
+    need_ctx(ctx);
+    Context& c = ctx->c;
+    need_plans(c);
+    need_factors(c);
+    for (uint32_t w = 0; w < c.n; ++w)
+      MKB_CUDA(cudaMemcpyAsync(c.factors[w].get(), factors[w],
+                               static_cast<size_t>(c.dims[w]) * c.rank * sizeof(float),
+                               cudaMemcpyHostToDevice, c.stream));
+    sweep(c, chain, exec);
+    for (uint32_t d = 0; d < c.n; ++d)
+      MKB_CUDA(cudaMemcpyAsync(outs[d], c.outputs[d].get(),
+                               static_cast<size_t>(c.dims[d]) * c.rank * sizeof(float),
+                               cudaMemcpyDeviceToHost, c.stream));
+    check_nonfinite(c);
+  });
+}
+
+int mk_flush_l2(mk_context* ctx) {
+  return guarded([&] {
+    need_ctx(ctx);
+    Context& c = ctx->c;
+    const size_t bytes = std::max<size_t>(2 * c.l2_bytes, 64u << 20);
+    c.flush_buf.resize(bytes);
+    MKB_CUDA(cudaMemsetAsync(c.flush_buf.get(), 0x5a, bytes, c.stream));
+  });
+}
+
+int mk_run_timed(mk_context* ctx, uint64_t iters, int exec, int flush_l2, double* mode_ms,
+                 double* total_ms) {
+  return guarded([&] {
+    need_ctx(ctx);
+    Context& c = ctx->c;
+    need_plans(c);
+    need_factors(c);
+    if (iters < 1) fail(MK_EINVAL, "kernel: iters must be at least 1");
+    const uint32_t n = c.n;
+    std::vector<cudaEvent_t> ev(iters * (n + 1));
+    for (auto& e : ev) MKB_CUDA(cudaEventCreate(&e));
+    reset_nonfinite(c);
+    const float* in[kMaxModes];
+    for (uint32_t w = 0; w < n; ++w) in[w] = c.factors[w].get();
+    for (uint64_t it = 0; it < iters; ++it) {
+      if (flush_l2) {
+        const size_t bytes = std::max<size_t>(2 * c.l2_bytes, 64u << 20);
+        c.flush_buf.resize(bytes);
+        MKB_CUDA(cudaMemsetAsync(c.flush_buf.get(), static_cast<int>(it & 0xff), bytes,
+                                 c.stream));
+      }
+      MKB_CUDA(cudaEventRecord(ev[it * (n + 1)], c.stream));
+      for (uint32_t d = 0; d < n; ++d) {
+        launch_mttkrp(c, d, in, c.outputs[d].get(), exec);
+        MKB_CUDA(cudaEventRecord(ev[it * (n + 1) + d + 1], c.stream));
+      }
+    }
+    MKB_CUDA(cudaStreamSynchronize(c.stream));
+    for (uint64_t it = 0; it < iters; ++it) {
+      float tot = 0.f;
+      for (uint32_t d = 0; d < n; ++d) {
+        float ms = 0.f;
+        MKB_CUDA(cudaEventElapsedTime(&ms, ev[it * (n + 1) + d], ev[it * (n + 1) + d + 1]));
+        if (mode_ms) mode_ms[it * n + d] = ms;
+        tot += ms;
+      }
+      if (total_ms) total_ms[it] = tot;
+    }
+    for (auto& e : ev) cudaEventDestroy(e);
+    check_nonfinite(c);
+  });
+}
+
+}  // extern "C"
+
+extern "C" {
+
+int mk_cpd_als_iter(mk_context* ctx, double* fit, float* lambda) {
+  return guarded([&] {
+    need_ctx(ctx);
+    Context& c = ctx->c;
+    need_plans(c);
+    need_factors(c);
+    double f = 0.0;
+    als_iteration(c, &f, lambda);
+    if (fit) *fit = f;
+  });
+}
+
+int mk_cpd_als(mk_context* ctx, uint64_t max_iters, double tol, double* fit,
+               uint64_t* iters_done, float* lambda) {
+  return guarded([&] {
+    need_ctx(ctx);
+    Context& c = ctx->c;
+    need_plans(c);
+    need_factors(c);
+    double prev = 0.0, f = 0.0;
+    uint64_t it = 0;
+    while (it < max_iters) {
+      als_iteration(c, &f, lambda);
+      ++it;
+      if (it > 1 && std::fabs(f - prev) < tol) break;
+      prev = f;
+    }
+    if (fit) *fit = f;
+    if (iters_done) *iters_done = it;
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,81 @@
+// Shared plumbing for the sm_100a spMTTKRP library: status/errors, device buffers.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstdio>
+#include <stdexcept>
+#include <string>
+#include <utility>
+
+#include "mttkrp_b200.h"
+
+namespace mkb {
+
+// Internal exception carrying an mk_status; converted at the C-ABI boundary.
+struct Error : std::runtime_error {
+  int status;
+  Error(int s, const std::string& m) : std::runtime_error(m), status(s) {}
+};
+
+[[noreturn]] inline void fail(int status, const std::string& msg) { throw Error(status, msg); }
+
+inline void cuda_check(cudaError_t e, const char* what, const char* file, int line) {
+  if (e != cudaSuccess) {
+    char buf[512];
+    std::snprintf(buf, sizeof buf, "cuda: %s failed: %s (%s:%d)", what, cudaGetErrorString(e),
+                  file, line);
+    if (e == cudaErrorMemoryAllocation) throw Error(MK_ENOMEM, buf);
+    throw Error(MK_ECUDA, buf);
+  }
+}
+#define MKB_CUDA(x) ::mkb::cuda_check((x), #x, __FILE__, __LINE__)
+#define MKB_LAUNCH() ::mkb::cuda_check(cudaGetLastError(), "kernel launch", __FILE__, __LINE__)
+
+// Owning device allocation (cudaMalloc; 256-byte aligned, so float4 rows are aligned
+// whenever the row stride is a multiple of 4 floats).
+template <typename T>
+class DevBuf {
+ public:
+  DevBuf() = default;
+  explicit DevBuf(size_t n) { resize(n); }
+  ~DevBuf() { release(); }
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  DevBuf(DevBuf&& o) noexcept : p_(o.p_), n_(o.n_) { o.p_ = nullptr; o.n_ = 0; }
+  DevBuf& operator=(DevBuf&& o) noexcept {
+    if (this != &o) { release(); p_ = o.p_; n_ = o.n_; o.p_ = nullptr; o.n_ = 0; }
+    return *this;
+  }
+  void resize(size_t n) {
+    if (n <= n_ && p_) return;
+    release();
+    if (n == 0) return;
+    MKB_CUDA(cudaMalloc(&p_, n * sizeof(T)));
+    n_ = n;
+  }
+  void release() {
+    if (p_) cudaFree(p_);
+    p_ = nullptr;
+    n_ = 0;
+  }
+  T* get() const { return p_; }
+  size_t size() const { return n_; }
+  size_t bytes() const { return n_ * sizeof(T); }
+
+ private:
+  T* p_ = nullptr;
+  size_t n_ = 0;
+};
+
+inline unsigned ceil_div(uint64_t a, uint64_t b) { return static_cast<unsigned>((a + b - 1) / b); }
+
+// Number of bits needed to hold values in [0, v].
+inline int bits_for(uint64_t v) {
+  int b = 0;
+  while (v) { ++b; v >>= 1; }
+  return b;
+}
+
+}  // namespace mkb

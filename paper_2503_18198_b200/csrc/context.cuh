@@ -1,0 +1,102 @@
+// Device-resident state of one mk_context: the uploaded tensor, the N mode-specific
+// copies (the "tensor copies T_d" of Algorithm 1), factors and outputs.
+//
+// HBM layout per mode d (all arrays in copy order j = 0..nnz-1, i.e. the order of
+// ModePlan::order, layout.hpp:51-52):
+//   idx[w][j]   uint32  coordinate of mode w of element order[j]       (N arrays, SoA)
+//   val[j]      fp32    value of element order[j]
+//   order[j]    uint32  original element position (exported as uint64)
+//   row_seq[k]  uint32  k-th non-empty output row in copy order       (V entries)
+//   row_ptr[k]  uint32  first copy position of row_seq[k]               (V+1 entries)
+//   zero_rows   uint32  rows the fast kernel must pre-zero: empty rows + tile-split rows
+// A Scheme 1 copy has rows grouped by partition (owned rows ascending inside a partition);
+// a Scheme 2 copy has rows ascending.  Both are one contiguous run per output row, which
+// is what lets one kernel serve both schemes.
+#pragma once
+
+#include <cstdint>
+#include <vector>
+
+#include "common.cuh"
+#include "sort.cuh"
+
+namespace mkb {
+
+constexpr int kMaxModes = 8;
+
+struct ModeCopy {
+  int scheme = MK_SCHEME1;
+  uint64_t kappa = 1;
+  uint64_t owned_total = 0;
+  uint64_t distinct = 0;  // V: rows with degree > 0
+  DevBuf<uint32_t> idx[kMaxModes];
+  DevBuf<float> val;
+  DevBuf<uint32_t> order;
+  DevBuf<uint32_t> row_seq;  // rows in copy order: [0,V) non-empty, [V,extent) empty
+  DevBuf<uint32_t> row_ptr;  // V+1
+  DevBuf<uint32_t> zero_rows;
+  uint64_t n_zero_rows = 0;
+  uint64_t n_split_rows = 0;
+  uint32_t tile = 256;  // fast-kernel tile length (nnz), chosen per copy at build time
+  std::vector<uint64_t> partition_offsets;  // kappa+1 (host)
+  std::vector<uint64_t> owned_offsets;      // kappa+1 (host); rows = row_seq[...]
+  DevBuf<uint32_t> degrees;                 // extent
+  bool built = false;
+};
+
+struct Context {
+  int device = 0;
+  cudaStream_t own_stream = nullptr;
+  cudaStream_t stream = nullptr;
+  int num_sms = 148;
+  size_t l2_bytes = 0;
+
+  // tensor
+  uint32_t n = 0;
+  std::vector<uint32_t> dims;
+  uint64_t nnz = 0;
+  DevBuf<uint32_t> cols[kMaxModes];  // original element order, SoA
+  DevBuf<float> values;
+  double norm2 = 0.0;
+
+  // plans
+  ModeCopy copies[kMaxModes];
+  bool plans_built = false;
+  uint64_t kappa = 0;
+
+  // factors / outputs (row-major I_d x R)
+  uint32_t rank = 0;
+  DevBuf<float> factors[kMaxModes];
+  DevBuf<float> outputs[kMaxModes];
+  bool factors_set[kMaxModes] = {};
+
+  // device scalars: [0] = min non-finite copy position (uint64, ~0 = none), [1] = mode
+  DevBuf<unsigned long long> nonfinite;
+  DevBuf<uint8_t> flush_buf;
+  SortScratch scratch;
+
+  // CPD-ALS state
+  DevBuf<double> gram;    // N x R x R (fp64)
+  DevBuf<float> solve;    // R x R inverse of V (fp32 for the row apply)
+  DevBuf<float> lambda;   // R
+  DevBuf<double> als_scalars;
+  DevBuf<int> als_status;
+  bool grams_valid = false;
+};
+
+// One CPD-ALS iteration over all modes (als.cu); fit and optional lambda[R] to host.
+void als_iteration(Context& c, double* fit, float* lambda_host);
+
+// Fast-kernel tile length: ~one tile per resident lane group, clamped to [32, 1024].
+uint32_t choose_tile(uint64_t nnz, int num_sms);
+
+void tensor_upload(Context& c, uint32_t n, const uint32_t* dims, uint64_t nnz,
+                   const uint32_t* coords_aos, const float* values);
+void build_plans(Context& c, uint64_t kappa, int strategy, int policy);
+
+// Enqueue MTTKRP of `mode` reading factors in[w] and writing out (I_d x R).
+void launch_mttkrp(Context& c, uint32_t mode, const float* const* in, float* out, int exec);
+void reset_nonfinite(Context& c);
+void check_nonfinite(Context& c);  // synchronises; throws MK_ENONFINITE
+
+}  // namespace mkb

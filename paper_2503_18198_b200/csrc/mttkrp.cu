@@ -1,0 +1,383 @@
+// spMTTKRP kernels for sm_100a (north-star subsystem 3; reference executor
+// detail::mttkrp_mode_impl, kernel.hpp:75-127, and Algorithm 2).
+//
+// Work unit: a "lane group" of G lanes owns the rank dimension of one output row
+// (lane l holds ranks [l*VEC, l*VEC+VEC) of each KREP slice; VEC=4 -> 128-bit gathers).
+//
+// FAST kernel (k_mttkrp_tiles): the mode copy is cut into fixed tiles of `tile` nnz.
+// A group walks its tile in copy order: lanes load G elements' indices/values coalesced,
+// then for each element broadcast them with width-G shuffles, gather the N-1 input rows
+// (one LDG.128 per lane per input mode, L1-cached), form
+//     term = val * Y_w0[c_w0] * Y_w1[c_w1] * ...        (w ascending, kernel.hpp:102-107)
+// and accumulate in registers while the output row is unchanged.  Because every output
+// row is ONE contiguous run of the copy (Scheme 1: inside its owning partition; Scheme 2:
+// globally sorted), a run that lies strictly inside a tile is owned by this group and is
+// written with a plain 128-bit store (Local_Update); only the first/last run of a tile
+// can continue into a neighbour tile and is added with a vector atomic (Global_Update) —
+// atomics at partition boundaries only, no intermediate global traffic.
+// Non-finite partial products (kernel.hpp:109-114) are detected on the row sum and, if
+// found, the run is rescanned to report the first offending copy position.
+//
+// DETERMINISTIC kernel (k_mttkrp_rows): one group per output row, elements in copy order,
+// __fmul_rn/__fadd_rn (no FMA contraction): bit-identical to ExecConfig{deterministic}
+// (kernel.hpp:26-28) and to oracle_mttkrp (oracle.hpp:20-43), whose per-row summation
+// order is also element order.
+#include <algorithm>
+
+#include "context.cuh"
+
+namespace mkb {
+namespace {
+
+struct MttkrpArgs {
+  const uint32_t* in_idx[kMaxModes];  // copy-order coordinates of the input modes (w != d)
+  const float* in_Y[kMaxModes];       // matching input factors, row-major I_w x R
+  const uint32_t* out_idx;            // copy-order output coordinates (mode d)
+  const float* val;
+  float* out;
+  const uint32_t* row_seq;
+  const uint32_t* row_ptr;
+  unsigned long long* nonfinite;  // min (mode << 32 | offending copy position)
+  unsigned long long tag;         // mode << 32
+  uint64_t nnz;
+  uint32_t rank;
+  uint32_t tile;
+  uint32_t ntiles;
+  uint32_t nrows;
+  uint32_t n_in;
+};
+
+template <int VEC>
+struct Vec;
+template <>
+struct Vec<4> {
+  using T = float4;
+  static __device__ __forceinline__ float4 load(const float* p) {
+    return __ldg(reinterpret_cast<const float4*>(p));
+  }
+};
+
+template <int VEC, int KREP>
+struct Frag {
+  float v[KREP * VEC];
+};
+
+// lane-local rank of slot (k, q): k-th KREP slice, q-th component
+template <int VEC, int G>
+__device__ __forceinline__ uint32_t rank_of(int lane_g, int k, int q) {
+  return static_cast<uint32_t>(k * G * VEC + lane_g * VEC + q);
+}
+
+template <int VEC, int G, int KREP>
+__device__ __forceinline__ void load_row(const float* __restrict__ Y, uint32_t row, uint32_t R,
+                                         int lane_g, float (&dst)[KREP * VEC]) {
+  const float* base = Y + static_cast<size_t>(row) * R;
+#pragma unroll
+  for (int k = 0; k < KREP; ++k) {
+    if constexpr (VEC == 4) {
+      const float4 y = Vec<4>::load(base + rank_of<VEC, G>(lane_g, k, 0));
+      dst[k * 4 + 0] = y.x;
+      dst[k * 4 + 1] = y.y;
+      dst[k * 4 + 2] = y.z;
+      dst[k * 4 + 3] = y.w;
+    } else {
+      const uint32_t r = rank_of<VEC, G>(lane_g, k, 0);
+      dst[k] = r < R ? __ldg(base + r) : 0.0f;
+    }
+  }
+}
+
+template <int VEC, int G, int KREP>
+__device__ __forceinline__ void store_row(float* __restrict__ out, uint32_t row, uint32_t R,
+                                          int lane_g, const float (&acc)[KREP * VEC],
+                                          bool atomic) {
+  float* base = out + static_cast<size_t>(row) * R;
+#pragma unroll
+  for (int k = 0; k < KREP; ++k) {
+    if constexpr (VEC == 4) {
+      float4 a = make_float4(acc[k * 4 + 0], acc[k * 4 + 1], acc[k * 4 + 2], acc[k * 4 + 3]);
+      float4* p = reinterpret_cast<float4*>(base + rank_of<VEC, G>(lane_g, k, 0));
+      if (atomic)
+        atomicAdd(p, a);
+      else
+        *p = a;
+    } else {
+      const uint32_t r = rank_of<VEC, G>(lane_g, k, 0);
+      if (r < R) {
+        if (atomic)
+          atomicAdd(base + r, acc[k]);
+        else
+          base[r] = acc[k];
+      }
+    }
+  }
+}
+
+// Slow path: a lane whose row sum is non-finite recomputes the run's terms in element
+// order and reports the first copy position whose partial product is non-finite.
+template <int NI, int VEC, int G, int KREP>
+__device__ __noinline__ void rescan_nonfinite(const MttkrpArgs& a, uint64_t s, uint64_t e,
+                                              int lane_g) {
+  for (uint64_t j = s; j < e; ++j) {
+    float t[KREP * VEC];
+#pragma unroll
+    for (int q = 0; q < KREP * VEC; ++q) t[q] = a.val[j];
+#pragma unroll
+    for (int i = 0; i < NI; ++i) {
+      float y[KREP * VEC];
+      load_row<VEC, G, KREP>(a.in_Y[i], a.in_idx[i][j], a.rank, lane_g, y);
+#pragma unroll
+      for (int q = 0; q < KREP * VEC; ++q) t[q] = __fmul_rn(t[q], y[q]);
+    }
+    bool bad = false;
+#pragma unroll
+    for (int q = 0; q < KREP * VEC; ++q) bad |= !isfinite(t[q]);
+    if (bad) {
+      atomicMin(a.nonfinite, a.tag | static_cast<unsigned long long>(j));
+      return;
+    }
+  }
+}
+
+template <int NI, int VEC, int G, int KREP>
+__global__ void __launch_bounds__(256) k_mttkrp_tiles(const MttkrpArgs a) {
+  constexpr int F = KREP * VEC;
+  // elements gathered per inner batch (bounded so the term buffer stays in registers)
+  constexpr int SB = G < 8 ? G : (F <= 4 ? 8 : (F <= 8 ? 4 : 2));
+  const int lane = threadIdx.x & 31;
+  const int lane_g = lane % G;
+  const int gbase = lane - lane_g;  // first lane of this group within the warp
+  const unsigned gmask = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << gbase);
+  const uint32_t groups = (gridDim.x * blockDim.x) / G;
+  const uint32_t gid = (blockIdx.x * blockDim.x + threadIdx.x) / G;
+
+  for (uint32_t t = gid; t < a.ntiles; t += groups) {
+    const uint64_t ta = static_cast<uint64_t>(t) * a.tile;
+    const uint64_t tb = min(ta + a.tile, a.nnz);
+    const bool head_split = ta > 0 && __ldg(a.out_idx + ta - 1) == __ldg(a.out_idx + ta);
+    const bool tail_split = tb < a.nnz && __ldg(a.out_idx + tb) == __ldg(a.out_idx + tb - 1);
+    uint32_t cur = __ldg(a.out_idx + ta);
+    uint64_t run_start = ta;
+    bool first_run = true;
+    float acc[F];
+#pragma unroll
+    for (int q = 0; q < F; ++q) acc[q] = 0.0f;
+
+    for (uint64_t base = ta; base < tb; base += G) {
+      // cooperative, coalesced load of G elements' indices and values
+      const uint64_t jl = base + lane_g;
+      const bool vl = jl < tb;
+      uint32_t my_c[NI > 0 ? NI : 1];
+#pragma unroll
+      for (int i = 0; i < NI; ++i) my_c[i] = vl ? __ldg(a.in_idx[i] + jl) : 0u;
+      const uint32_t my_cd = vl ? __ldg(a.out_idx + jl) : 0u;
+      const float my_v = vl ? __ldg(a.val + jl) : 0.0f;
+
+#pragma unroll
+      for (int sb = 0; sb < G; sb += SB) {
+        float term[SB][F];
+        uint32_t rows[SB];
+#pragma unroll
+        for (int k = 0; k < SB; ++k) {
+          const float v = __shfl_sync(gmask, my_v, gbase + sb + k);
+          rows[k] = __shfl_sync(gmask, my_cd, gbase + sb + k);
+#pragma unroll
+          for (int q = 0; q < F; ++q) term[k][q] = v;
+#pragma unroll
+          for (int i = 0; i < NI; ++i) {
+            const uint32_t c = __shfl_sync(gmask, my_c[i], gbase + sb + k);
+            float y[F];
+            load_row<VEC, G, KREP>(a.in_Y[i], c, a.rank, lane_g, y);
+#pragma unroll
+            for (int q = 0; q < F; ++q) term[k][q] *= y[q];
+          }
+        }
+#pragma unroll
+        for (int k = 0; k < SB; ++k) {
+          const uint64_t j = base + sb + k;
+          if (j < tb) {
+            if (rows[k] != cur) {
+              bool bad = false;
+#pragma unroll
+              for (int q = 0; q < F; ++q) bad |= !isfinite(acc[q]);
+              if (bad) rescan_nonfinite<NI, VEC, G, KREP>(a, run_start, j, lane_g);
+              store_row<VEC, G, KREP>(a.out, cur, a.rank, lane_g, acc, first_run && head_split);
+              first_run = false;
+              cur = rows[k];
+              run_start = j;
+#pragma unroll
+              for (int q = 0; q < F; ++q) acc[q] = 0.0f;
+            }
+#pragma unroll
+            for (int q = 0; q < F; ++q) acc[q] += term[k][q];
+          }
+        }
+      }
+    }
+    bool bad = false;
+#pragma unroll
+    for (int q = 0; q < F; ++q) bad |= !isfinite(acc[q]);
+    if (bad) rescan_nonfinite<NI, VEC, G, KREP>(a, run_start, tb, lane_g);
+    store_row<VEC, G, KREP>(a.out, cur, a.rank, lane_g, acc,
+                            tail_split || (first_run && head_split));
+  }
+}
+
+template <int NI, int VEC, int G, int KREP>
+__global__ void __launch_bounds__(256) k_mttkrp_rows(const MttkrpArgs a) {
+  constexpr int F = KREP * VEC;
+  const int lane = threadIdx.x & 31;
+  const int lane_g = lane % G;
+  const int gbase = lane - lane_g;
+  const unsigned gmask = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << gbase);
+  const uint32_t groups = (gridDim.x * blockDim.x) / G;
+  const uint32_t gid = (blockIdx.x * blockDim.x + threadIdx.x) / G;
+
+  for (uint32_t k = gid; k < a.nrows; k += groups) {
+    const uint32_t row = __ldg(a.row_seq + k);
+    const uint64_t s = __ldg(a.row_ptr + k), e = __ldg(a.row_ptr + k + 1);
+    float acc[F];
+#pragma unroll
+    for (int q = 0; q < F; ++q) acc[q] = 0.0f;
+    unsigned long long first_bad = ~0ull;
+    for (uint64_t base = s; base < e; base += G) {
+      const uint64_t jl = base + lane_g;
+      const bool vl = jl < e;
+      uint32_t my_c[NI > 0 ? NI : 1];
+#pragma unroll
+      for (int i = 0; i < NI; ++i) my_c[i] = vl ? __ldg(a.in_idx[i] + jl) : 0u;
+      const float my_v = vl ? __ldg(a.val + jl) : 0.0f;
+      const int cnt = static_cast<int>(e - base < G ? e - base : G);
+      for (int kk = 0; kk < cnt; ++kk) {
+        const float v = __shfl_sync(gmask, my_v, gbase + kk);
+        float t[F];
+#pragma unroll
+        for (int q = 0; q < F; ++q) t[q] = v;
+#pragma unroll
+        for (int i = 0; i < NI; ++i) {
+          const uint32_t c = __shfl_sync(gmask, my_c[i], gbase + kk);
+          float y[F];
+          load_row<VEC, G, KREP>(a.in_Y[i], c, a.rank, lane_g, y);
+#pragma unroll
+          for (int q = 0; q < F; ++q) t[q] = __fmul_rn(t[q], y[q]);
+        }
+        bool bad = false;
+#pragma unroll
+        for (int q = 0; q < F; ++q) {
+          bad |= !isfinite(t[q]);
+          acc[q] = __fadd_rn(acc[q], t[q]);
+        }
+        if (bad && first_bad == ~0ull) first_bad = base + kk;
+      }
+    }
+    if (first_bad != ~0ull) atomicMin(a.nonfinite, a.tag | first_bad);
+    store_row<VEC, G, KREP>(a.out, row, a.rank, lane_g, acc, false);
+  }
+}
+
+template <int VEC, int G, int KREP>
+__global__ void k_zero_rows(float* __restrict__ out, uint32_t R,
+                            const uint32_t* __restrict__ rows, uint64_t n) {
+  const int lane_g = (threadIdx.x & 31) % G;
+  const uint64_t groups = static_cast<uint64_t>(gridDim.x) * blockDim.x / G;
+  float z[KREP * VEC];
+#pragma unroll
+  for (int q = 0; q < KREP * VEC; ++q) z[q] = 0.0f;
+  for (uint64_t i = (blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x) / G; i < n;
+       i += groups) {
+    const uint32_t r = rows[i];
+    if (r != 0xffffffffu) store_row<VEC, G, KREP>(out, r, R, lane_g, z, false);
+  }
+}
+
+__global__ void k_init_nonfinite(unsigned long long* p) { *p = ~0ull; }
+
+template <int NI, int VEC, int G, int KREP>
+void launch_cfg(Context& c, const MttkrpArgs& a, const ModeCopy& mc, int exec) {
+  cudaStream_t st = c.stream;
+  const int per_block = 256 / G;
+  if (mc.n_zero_rows) {
+    const unsigned blocks =
+        static_cast<unsigned>(std::min<uint64_t>(ceil_div(mc.n_zero_rows, per_block),
+                                                 c.num_sms * 8ull));
+    k_zero_rows<VEC, G, KREP><<<blocks, 256, 0, st>>>(a.out, a.rank, mc.zero_rows.get(),
+                                                      mc.n_zero_rows);
+    MKB_LAUNCH();
+  }
+  if (!a.nnz) return;
+  if (exec == MK_EXEC_DETERMINISTIC) {
+    const unsigned blocks = static_cast<unsigned>(
+        std::min<uint64_t>(ceil_div(a.nrows, per_block), c.num_sms * 16ull));
+    k_mttkrp_rows<NI, VEC, G, KREP><<<std::max(1u, blocks), 256, 0, st>>>(a);
+  } else {
+    const unsigned blocks = static_cast<unsigned>(
+        std::min<uint64_t>(ceil_div(a.ntiles, per_block), c.num_sms * 8ull));
+    k_mttkrp_tiles<NI, VEC, G, KREP><<<std::max(1u, blocks), 256, 0, st>>>(a);
+  }
+  MKB_LAUNCH();
+}
+
+template <int NI>
+void launch_ni(Context& c, const MttkrpArgs& a, const ModeCopy& mc, int exec) {
+  const uint32_t R = a.rank;
+  if constexpr (NI >= 2 && NI <= 4) {  // N = 3, 4, 5: 128-bit gather paths
+    switch (R) {
+      case 16: return launch_cfg<NI, 4, 4, 1>(c, a, mc, exec);
+      case 32: return launch_cfg<NI, 4, 8, 1>(c, a, mc, exec);
+      case 64: return launch_cfg<NI, 4, 16, 1>(c, a, mc, exec);
+      case 128: return launch_cfg<NI, 4, 32, 1>(c, a, mc, exec);
+      default: break;
+    }
+  }
+  if (R <= 32) return launch_cfg<NI, 1, 32, 1>(c, a, mc, exec);
+  if (R <= 64) return launch_cfg<NI, 1, 32, 2>(c, a, mc, exec);
+  if (R <= 128) return launch_cfg<NI, 1, 32, 4>(c, a, mc, exec);
+  if (R <= 256) return launch_cfg<NI, 1, 32, 8>(c, a, mc, exec);
+  fail(MK_EINVAL, "kernel: rank above 256 is not supported on the device path");
+}
+
+}  // namespace
+
+void reset_nonfinite(Context& c) {
+  c.nonfinite.resize(2);
+  k_init_nonfinite<<<1, 1, 0, c.stream>>>(c.nonfinite.get());
+  MKB_LAUNCH();
+}
+
+void launch_mttkrp(Context& c, uint32_t mode, const float* const* in, float* out, int exec) {
+  const ModeCopy& mc = c.copies[mode];
+  MttkrpArgs a{};
+  uint32_t ni = 0;
+  for (uint32_t w = 0; w < c.n; ++w) {
+    if (w == mode) continue;
+    a.in_idx[ni] = mc.idx[w].get();
+    a.in_Y[ni] = in[w];
+    ++ni;
+  }
+  a.n_in = ni;
+  a.out_idx = mc.idx[mode].get();
+  a.val = mc.val.get();
+  a.out = out;
+  a.row_seq = mc.row_seq.get();
+  a.row_ptr = mc.row_ptr.get();
+  a.nonfinite = c.nonfinite.get();
+  a.tag = static_cast<unsigned long long>(mode) << 32;
+  a.nnz = c.nnz;
+  a.rank = c.rank;
+  a.tile = mc.tile;
+  a.ntiles = c.nnz ? ceil_div(c.nnz, mc.tile) : 0;
+  a.nrows = static_cast<uint32_t>(mc.distinct);
+  switch (ni) {
+    case 0: return launch_ni<0>(c, a, mc, exec);
+    case 1: return launch_ni<1>(c, a, mc, exec);
+    case 2: return launch_ni<2>(c, a, mc, exec);
+    case 3: return launch_ni<3>(c, a, mc, exec);
+    case 4: return launch_ni<4>(c, a, mc, exec);
+    case 5: return launch_ni<5>(c, a, mc, exec);
+    case 6: return launch_ni<6>(c, a, mc, exec);
+    case 7: return launch_ni<7>(c, a, mc, exec);
+    default: fail(MK_EINVAL, "kernel: too many modes");
+  }
+}
+
+}  // namespace mkb

@@ -1,0 +1,74 @@
+"""GPU: CPD-ALS on the device vs the fp64 restatement (oracle/als.py).  Parity for this
+subsystem is unpinned against the reference (it has no ALS)."""
+import numpy as np
+import pytest
+
+from oracle import als as als_oracle
+
+pytestmark = pytest.mark.gpu
+
+
+def dense_lowrank_tensor(mk, dims, rank, seed):
+    g = np.random.default_rng(seed)
+    A = [g.normal(size=(d, rank)) for d in dims]
+    X = np.einsum("ir,jr,kr->ijk", *A)
+    coords = np.argwhere(np.ones(dims, bool)).astype(np.uint32)
+    vals = X[tuple(coords.T)].astype(np.float32)
+    return mk.SparseTensorCOO(dims, coords, vals)
+
+
+@pytest.mark.parametrize("rank,seed", [(4, 0), (8, 1), (16, 2), (32, 3)])
+def test_one_iteration_matches_fp64(mk, rank, seed):
+    g = np.random.default_rng(seed)
+    dims = [30, 40, 50]
+    t = mk.generate_synthetic(dims, 6000, seed=seed)
+    f0 = [g.normal(size=(d, rank)).astype(np.float32) for d in dims]  # well-conditioned Grams
+    plans = mk.build_mode_plans(t, 8)
+    ctx = plans[0]._ctx
+    ctx.upload_factors(f0)
+    fit, lam = ctx.cpd_als_iter()
+    Y, lam64, fit64, _ = als_oracle.als_iteration(dims, t.coords, t.values, f0)
+    for d in range(3):
+        got = ctx.download_factor(d)
+        assert np.max(np.abs(got - Y[d])) < 2e-3, d
+    assert np.allclose(lam, lam64, rtol=1e-3)
+    assert abs(fit - fit64) < 1e-4
+
+
+def test_exact_lowrank_recovered(mk):
+    t = dense_lowrank_tensor(mk, [12, 14, 16], 3, 7)
+    plans = mk.build_mode_plans(t, 8)
+    g = np.random.default_rng(1)
+    f0 = [g.normal(size=(d, 3)).astype(np.float32) for d in t.dims]
+    fit, iters, lam, _ = mk.cpd_als(t, plans, f0, 200, 1e-9)
+    assert fit > 0.999, (fit, iters)
+
+
+def test_fit_monotone_on_random_tensor(mk):
+    t = mk.generate_synthetic([60, 70, 80], 20000, seed=4)
+    plans = mk.build_mode_plans(t, 148)
+    ctx = plans[0]._ctx
+    f0 = [m.data for m in mk.random_factors(t.dims, 16, 2)]
+    ctx.upload_factors(f0)
+    fits = [ctx.cpd_als_iter()[0] for _ in range(8)]
+    assert all(b >= a - 1e-4 for a, b in zip(fits, fits[1:])), fits
+    Y = [ctx.download_factor(d) for d in range(3)]
+    for y in Y:  # columns normalised
+        assert np.allclose(np.linalg.norm(y, axis=0), 1.0, atol=1e-4)
+
+
+def test_rank_deficient_uses_pinv(mk):
+    # duplicate columns make V singular: the device falls back to the pseudo-inverse
+    dims = [20, 20, 20]
+    t = mk.generate_synthetic(dims, 3000, seed=5)
+    g = np.random.default_rng(3)
+    f0 = []
+    for d in dims:
+        a = g.normal(size=(d, 2)).astype(np.float32)
+        f0.append(np.concatenate([a, a[:, :1]], axis=1))
+    plans = mk.build_mode_plans(t, 8)
+    ctx = plans[0]._ctx
+    ctx.upload_factors(f0)
+    fit, lam = ctx.cpd_als_iter()
+    Y, lam64, fit64, _ = als_oracle.als_iteration(dims, t.coords, t.values, f0)
+    assert np.isfinite(fit) and abs(fit - fit64) < 5e-3
