@@ -76,7 +76,7 @@ class ClockSampler:
                0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
                0x100: "display_clock_setting"}
 
-    def __init__(self, index=0, period=0.05):
+    def __init__(self, index=0, period=0.002):
         self.samples, self.reasons, self.ok = [], 0, False
         self.max_mhz = None
         self.period = period
@@ -218,7 +218,11 @@ def our_arm(args, cfg, rank, world, local_rank):
     t = make_tensor(mk, cfg)
     factors = [m.data for m in mk.random_factors(dims, R, 1)]
     dev = torch.device("cuda", local_rank)
-    stream = torch.cuda.current_stream(dev)
+    # A dedicated (non-default) stream shared by torch's events and the library: the
+    # legacy default stream's handle is NULL, which the C ABI reads as "own stream".
+    stream = torch.cuda.Stream(dev)
+    torch.cuda.set_stream(stream)
+    assert stream.cuda_stream != 0
 
     ctx = mk.Context(local_rank)
     ctx.set_stream(stream.cuda_stream)
@@ -258,6 +262,14 @@ def our_arm(args, cfg, rank, world, local_rank):
     for _ in range(max(args.warmup, 3)):
         ctx.sweep_async(False, False)
     ctx.synchronize()
+    if args.profile:
+        # short, L2-flushed sweeps for ncu (never a bench number)
+        for _ in range(args.steps):
+            ctx.flush_l2()
+            ctx.sweep_async(False, False)
+        ctx.synchronize()
+        log(f"profile run done: {args.steps} sweeps of {n} modes")
+        return 0
 
     if world > 1:
         import torch.distributed as dist
@@ -366,6 +378,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--config", default="cfg2", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--profile", action="store_true",
+                    help="only build + run --steps flushed sweeps (for ncu); prints no JSON")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

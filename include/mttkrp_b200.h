@@ -63,8 +63,10 @@ const char* mk_version(void);
 int mk_device_count(int* count);
 int mk_create(int device, mk_context** out);
 int mk_destroy(mk_context* ctx);
-/* Run all work on an external CUDA stream (cudaStream_t passed as void*); NULL restores
- * the context's own stream. */
+/* Run all work on an external CUDA stream (cudaStream_t passed as void*).  NULL is the
+ * CUDA default (legacy) stream, as everywhere in CUDA; MK_OWN_STREAM restores the
+ * context's own non-blocking stream. */
+#define MK_OWN_STREAM ((void*)(intptr_t)-1)
 int mk_set_stream(mk_context* ctx, void* cuda_stream);
 int mk_synchronize(mk_context* ctx);
 

@@ -297,7 +297,10 @@ class Context:
             pass
 
     def set_stream(self, stream_ptr: Optional[int]):
-        _check(self.lib.mk_set_stream(self.h, C.c_void_p(stream_ptr or 0)))
+        """Enqueue on the given cudaStream_t (0 = CUDA legacy default stream, None = the
+        context's own stream)."""
+        handle = C.c_void_p(-1) if stream_ptr is None else C.c_void_p(stream_ptr)
+        _check(self.lib.mk_set_stream(self.h, handle))
 
     def synchronize(self):
         _check(self.lib.mk_synchronize(self.h))

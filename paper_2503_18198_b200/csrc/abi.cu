@@ -132,7 +132,8 @@ int mk_destroy(mk_context* ctx) {
 int mk_set_stream(mk_context* ctx, void* stream) {
   return guarded([&] {
     need_ctx(ctx);
-    ctx->c.stream = stream ? static_cast<cudaStream_t>(stream) : ctx->c.own_stream;
+    ctx->c.stream =
+        stream == MK_OWN_STREAM ? ctx->c.own_stream : static_cast<cudaStream_t>(stream);
   });
 }
 

@@ -41,6 +41,12 @@ struct ModeCopy {
   std::vector<uint64_t> partition_offsets;  // kappa+1 (host)
   std::vector<uint64_t> owned_offsets;      // kappa+1 (host); rows = row_seq[...]
   DevBuf<uint32_t> degrees;                 // extent
+  // packed element records for the streaming kernel (stream.cu): part A 16 B/element,
+  // part B 0/4/8/16 B/element; padded to a multiple of 4 elements
+  DevBuf<uint32_t> recA, recB;
+  DevBuf<uint32_t> stream_zero;  // pre-zero rows for the streaming kernel's segmentation
+  uint64_t stream_nzero = 0;
+  int stream_S = 0;
   bool built = false;
 };
 
@@ -97,6 +103,9 @@ void build_plans(Context& c, uint64_t kappa, int strategy, int policy);
 // Enqueue MTTKRP of `mode` reading factors in[w] and writing out (I_d x R).
 void launch_mttkrp(Context& c, uint32_t mode, const float* const* in, float* out, int exec);
 void reset_nonfinite(Context& c);
+// Streaming TMA kernel (stream.cu); false when the shape has no specialisation.
+bool launch_stream(Context& c, uint32_t mode, const float* const* in, float* out);
+void pack_records(Context& c, uint32_t mode);
 void check_nonfinite(Context& c);  // synchronises; throws MK_ENONFINITE
 
 }  // namespace mkb
