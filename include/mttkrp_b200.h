@@ -132,6 +132,29 @@ int mk_cpd_als_iter(mk_context* ctx, double* fit, float* lambda);
 int mk_cpd_als(mk_context* ctx, uint64_t max_iters, double tol, double* fit,
                uint64_t* iters_done, float* lambda);
 
+/* ---- multi-GPU row-range shards (no reference counterpart) ---------------
+ * Rank `rank` of `world` owns, in every mode copy, the copy rows [k_rank, k_rank+1) with
+ * k_r = first copy row starting at or after floor(r * nnz / world).  Subsequent fast and
+ * deterministic MTTKRP calls compute only the owned rows.  world = 1 restores the full copy. */
+int mk_set_shard(mk_context* ctx, uint32_t rank, uint32_t world);
+/* Copy-row range [k0, k1) owned by `rank` in `mode` (any rank of the current world). */
+int mk_shard_rows(mk_context* ctx, uint32_t mode, uint32_t rank, uint64_t* k0, uint64_t* k1);
+/* Pack this rank's output rows of `mode` (copy-row order, R floats each) into dst (device). */
+int mk_shard_pack(mk_context* ctx, uint32_t mode, float* dst_device);
+/* Scatter an all-gathered buffer (world blocks of stride_rows rows, device) into the
+ * output of `mode` in row-index order. */
+int mk_shard_unpack(mk_context* ctx, uint32_t mode, const float* src_device,
+                    uint64_t stride_rows);
+/* Host helper: the cut points above for a CSR row pointer (row_ptr[nrows] = nnz);
+ * cuts[world + 1]. */
+int mk_shard_cuts(const uint32_t* row_ptr, uint64_t nrows, uint32_t world, uint64_t* cuts);
+/* CPD-ALS pieces for a sharded driver: the Gram/solve/normalise update of mode d from the
+ * (gathered) MTTKRP output, and the fit after the last mode. */
+int mk_als_update_mode(mk_context* ctx, uint32_t mode);
+int mk_als_fit(mk_context* ctx, double* fit, float* lambda);
+/* Device pointer of the MTTKRP output of `mode` (I_d x R fp32), for external collectives. */
+int mk_output_device_ptr(mk_context* ctx, uint32_t mode, void** ptr);
+
 /* ---- host-side tensor ingest (synthetic.hpp:58-158, factor.hpp:71-84) ---------------
  * Bit-identical to the reference generator (same draw sequence), multi-threaded dedup.
  * dist: 0 uniform, 1 mode_skewed. */

@@ -57,6 +57,8 @@ EXPORTED_SYMBOLS = [
     "mk_output_download",
     "mk_sweep_host", "mk_run_timed", "mk_flush_l2", "mk_cpd_als_iter", "mk_cpd_als",
     "mk_generate_synthetic", "mk_generate_powerlaw", "mk_random_factors",
+    "mk_set_shard", "mk_shard_rows", "mk_shard_pack", "mk_shard_unpack", "mk_shard_cuts",
+    "mk_als_update_mode", "mk_als_fit", "mk_output_device_ptr",
 ]
 
 
@@ -142,6 +144,14 @@ def load_library() -> C.CDLL:
             "mk_generate_synthetic": (i32, [u32, vp, u64, i32, u64, u64, u64, vp, vp]),
             "mk_generate_powerlaw": (i32, [u32, vp, u64, C.c_double, u64, vp, vp]),
             "mk_random_factors": (i32, [u32, vp, u64, u64, vp]),
+            "mk_set_shard": (i32, [vp, u32, u32]),
+            "mk_shard_rows": (i32, [vp, u32, u32, P(u64), P(u64)]),
+            "mk_shard_pack": (i32, [vp, u32, vp]),
+            "mk_shard_unpack": (i32, [vp, u32, vp, u64]),
+            "mk_shard_cuts": (i32, [vp, u64, u32, vp]),
+            "mk_als_update_mode": (i32, [vp, u32]),
+            "mk_als_fit": (i32, [vp, P(C.c_double), vp]),
+            "mk_output_device_ptr": (i32, [vp, u32, P(vp)]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(lib, name)
@@ -405,6 +415,39 @@ class Context:
     def flush_l2(self):
         _check(self.lib.mk_flush_l2(self.h))
 
+    # multi-GPU shards
+    def set_shard(self, rank: int, world: int):
+        _check(self.lib.mk_set_shard(self.h, rank, world))
+
+    def shard_rows(self, mode: int, rank: int):
+        k0, k1 = C.c_uint64(), C.c_uint64()
+        _check(self.lib.mk_shard_rows(self.h, mode, rank, C.byref(k0), C.byref(k1)))
+        return int(k0.value), int(k1.value)
+
+    def shard_pack(self, mode: int, dst):
+        """dst: device pointer or CUDA tensor (>= owned rows x R fp32)."""
+        ptr = dst.data_ptr() if hasattr(dst, "data_ptr") else int(dst)
+        _check(self.lib.mk_shard_pack(self.h, mode, C.c_void_p(ptr)))
+
+    def shard_unpack(self, mode: int, src, stride_rows: int):
+        """src: device pointer or CUDA tensor (world x stride_rows x R fp32)."""
+        ptr = src.data_ptr() if hasattr(src, "data_ptr") else int(src)
+        _check(self.lib.mk_shard_unpack(self.h, mode, C.c_void_p(ptr), stride_rows))
+
+    def output_device_ptr(self, mode: int) -> int:
+        p = C.c_void_p()
+        _check(self.lib.mk_output_device_ptr(self.h, mode, C.byref(p)))
+        return int(p.value or 0)
+
+    def als_update_mode(self, mode: int):
+        _check(self.lib.mk_als_update_mode(self.h, mode))
+
+    def als_fit(self):
+        fit = C.c_double()
+        lam = np.empty(self.rank, dtype=np.float32)
+        _check(self.lib.mk_als_fit(self.h, C.byref(fit), _ptr(lam)))
+        return fit.value, lam
+
     def cpd_als_iter(self):
         fit = C.c_double()
         lam = np.empty(self.rank, dtype=np.float32)
@@ -648,6 +691,15 @@ def random_factors(dims, rank, seed) -> List[FactorMatrix]:
     mats = [np.empty((int(x), rank), dtype=np.float32) for x in dims]
     _check(lib.mk_random_factors(len(dims), _ptr(d), rank, seed, _ptr_array(mats)))
     return [FactorMatrix(i, m) for i, m in enumerate(mats)]
+
+
+def shard_cuts(row_ptr, world: int) -> np.ndarray:
+    """mk_shard_cuts: copy-row cut points of a CSR row pointer for `world` ranks (host)."""
+    lib = load_library()
+    rp = np.ascontiguousarray(np.asarray(row_ptr, dtype=np.uint32))
+    cuts = np.empty(world + 1, dtype=np.uint64)
+    _check(lib.mk_shard_cuts(_ptr(rp), rp.size - 1, world, _ptr(cuts)))
+    return cuts
 
 
 # ----------------------------------------------------------------------------- verify

@@ -500,3 +500,84 @@ int mk_cpd_als(mk_context* ctx, uint64_t max_iters, double tol, double* fit,
 }
 
 }  // extern "C"
+
+extern "C" {
+
+int mk_set_shard(mk_context* ctx, uint32_t rank, uint32_t world) {
+  return guarded([&] {
+    need_ctx(ctx);
+    set_shard(ctx->c, rank, world);
+  });
+}
+
+int mk_shard_rows(mk_context* ctx, uint32_t mode, uint32_t rank, uint64_t* k0, uint64_t* k1) {
+  return guarded([&] {
+    need_ctx(ctx);
+    Context& c = ctx->c;
+    need_plans(c);
+    need_mode(c, mode);
+    const ModeCopy& mc = c.copies[mode];
+    if (mc.shard_cuts.empty()) {
+      if (rank != 0) fail(MK_EINVAL, "shard: rank must be below world size");
+      *k0 = 0;
+      *k1 = mc.distinct;
+      return;
+    }
+    if (rank + 1 >= mc.shard_cuts.size()) fail(MK_EINVAL, "shard: rank must be below world size");
+    *k0 = mc.shard_cuts[rank];
+    *k1 = mc.shard_cuts[rank + 1];
+  });
+}
+
+int mk_shard_pack(mk_context* ctx, uint32_t mode, float* dst) {
+  return guarded([&] {
+    need_ctx(ctx);
+    need_plans(ctx->c);
+    need_mode(ctx->c, mode);
+    need_factors(ctx->c);
+    shard_pack(ctx->c, mode, dst);
+  });
+}
+
+int mk_shard_unpack(mk_context* ctx, uint32_t mode, const float* src, uint64_t stride_rows) {
+  return guarded([&] {
+    need_ctx(ctx);
+    need_plans(ctx->c);
+    need_mode(ctx->c, mode);
+    need_factors(ctx->c);
+    if (ctx->c.copies[mode].shard_cuts.empty()) fail(MK_ESTATE, "shard: mk_set_shard not called");
+    shard_unpack(ctx->c, mode, src, stride_rows);
+  });
+}
+
+int mk_als_update_mode(mk_context* ctx, uint32_t mode) {
+  return guarded([&] {
+    need_ctx(ctx);
+    need_plans(ctx->c);
+    need_mode(ctx->c, mode);
+    need_factors(ctx->c);
+    als_update_mode(ctx->c, mode);
+  });
+}
+
+int mk_als_fit(mk_context* ctx, double* fit, float* lambda) {
+  return guarded([&] {
+    need_ctx(ctx);
+    need_plans(ctx->c);
+    need_factors(ctx->c);
+    double f = 0.0;
+    als_fit(ctx->c, &f, lambda);
+    if (fit) *fit = f;
+  });
+}
+
+int mk_output_device_ptr(mk_context* ctx, uint32_t mode, void** ptr) {
+  return guarded([&] {
+    need_ctx(ctx);
+    need_mode(ctx->c, mode);
+    need_factors(ctx->c);
+    *ptr = ctx->c.outputs[mode].get();
+  });
+}
+
+}  // extern "C"

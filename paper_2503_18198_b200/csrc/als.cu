@@ -261,42 +261,54 @@ void gram_of(Context& c, uint32_t w) {
 
 }  // namespace
 
-void als_iteration(Context& c, double* fit, float* lambda_host) {
-  const uint32_t R = c.rank, n = c.n;
+void als_prepare(Context& c) {
+  const uint32_t R = c.rank;
   if (R > 64) fail(MK_EINVAL, "cpd: rank above 64 is not supported by the device ALS solve");
   if (c.norm2 <= 0.0) fail(MK_EINVAL, "cpd: tensor has zero norm");
-  cudaStream_t st = c.stream;
   if (!c.grams_valid) {
     c.gram.resize(static_cast<size_t>(kMaxModes) * R * R);
-    for (uint32_t w = 0; w < n; ++w) gram_of(c, w);
+    for (uint32_t w = 0; w < c.n; ++w) gram_of(c, w);
     c.grams_valid = true;
   }
   c.solve.resize(static_cast<size_t>(R) * R);
   c.lambda.resize(R);
   c.als_scalars.resize(2);
   c.als_status.resize(1);
-  const float* in[kMaxModes];
-  for (uint32_t w = 0; w < n; ++w) in[w] = c.factors[w].get();
-  reset_nonfinite(c);
+}
+
+// Y_d = M_d V⁻¹ with V = ⊛_{w≠d} G_w, then G_d and the column normalisation.  M_d is the
+// (possibly all-gathered) MTTKRP output in c.outputs[d].
+void als_update_mode(Context& c, uint32_t d) {
+  als_prepare(c);
+  const uint32_t R = c.rank, n = c.n;
+  cudaStream_t st = c.stream;
   const size_t solve_smem = 3 * sizeof(double) * R * R;
   const size_t apply_smem = sizeof(float) * (R * R + kGramRows * R);
-  for (uint32_t d = 0; d < n; ++d) {
-    launch_mttkrp(c, d, in, c.outputs[d].get(), MK_EXEC_FAST);
-    k_solve<<<1, 256, solve_smem, st>>>(c.gram.get(), n, d, R, c.solve.get(), c.als_status.get());
-    MKB_LAUNCH();
-    k_apply<<<blocks_for(c.dims[d], c.num_sms), 256, apply_smem, st>>>(
-        c.outputs[d].get(), c.dims[d], R, c.solve.get(), c.factors[d].get());
-    MKB_LAUNCH();
-    gram_of(c, d);
-    double* G = c.gram.get() + static_cast<size_t>(d) * R * R;
-    k_lambda<<<1, 256, 0, st>>>(G, R, c.lambda.get());
-    MKB_LAUNCH();
-    const size_t cnt = static_cast<size_t>(c.dims[d]) * R;
-    k_scale_cols<<<std::max(1, std::min<int>(static_cast<int>((cnt + 255) / 256), c.num_sms * 8)),
-                   256, 0, st>>>(c.factors[d].get(), cnt, R, c.lambda.get());
-    MKB_LAUNCH();
+  static int smem_set[64] = {};
+  if (!smem_set[c.device & 63]) {  // up to 3 x 64 x 64 doubles = 96 KB
+    MKB_CUDA(cudaFuncSetAttribute(k_solve, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  3 * 64 * 64 * static_cast<int>(sizeof(double))));
+    smem_set[c.device & 63] = 1;
   }
-  const uint32_t last = n - 1;
+  k_solve<<<1, 256, solve_smem, st>>>(c.gram.get(), n, d, R, c.solve.get(), c.als_status.get());
+  MKB_LAUNCH();
+  k_apply<<<blocks_for(c.dims[d], c.num_sms), 256, apply_smem, st>>>(
+      c.outputs[d].get(), c.dims[d], R, c.solve.get(), c.factors[d].get());
+  MKB_LAUNCH();
+  gram_of(c, d);
+  double* G = c.gram.get() + static_cast<size_t>(d) * R * R;
+  k_lambda<<<1, 256, 0, st>>>(G, R, c.lambda.get());
+  MKB_LAUNCH();
+  const size_t cnt = static_cast<size_t>(c.dims[d]) * R;
+  k_scale_cols<<<std::max(1, std::min<int>(static_cast<int>((cnt + 255) / 256), c.num_sms * 8)),
+                 256, 0, st>>>(c.factors[d].get(), cnt, R, c.lambda.get());
+  MKB_LAUNCH();
+}
+
+// fit after the last mode (its MTTKRP output is still in c.outputs[N-1])
+void als_fit(Context& c, double* fit, float* lambda_host) {
+  const uint32_t R = c.rank, n = c.n, last = n - 1;
+  cudaStream_t st = c.stream;
   MKB_CUDA(cudaMemsetAsync(c.als_scalars.get(), 0, 2 * sizeof(double), st));
   const size_t cnt = static_cast<size_t>(c.dims[last]) * R;
   k_inner<<<std::max(1, std::min<int>(static_cast<int>((cnt + 255) / 256), c.num_sms * 4)), 256, 0,
@@ -313,6 +325,18 @@ void als_iteration(Context& c, double* fit, float* lambda_host) {
   check_nonfinite(c);  // synchronises
   const double resid2 = std::max(0.0, c.norm2 - 2.0 * sc[0] + sc[1]);
   *fit = 1.0 - std::sqrt(resid2) / std::sqrt(c.norm2);
+}
+
+void als_iteration(Context& c, double* fit, float* lambda_host) {
+  als_prepare(c);
+  const float* in[kMaxModes];
+  for (uint32_t w = 0; w < c.n; ++w) in[w] = c.factors[w].get();
+  reset_nonfinite(c);
+  for (uint32_t d = 0; d < c.n; ++d) {
+    launch_mttkrp(c, d, in, c.outputs[d].get(), MK_EXEC_FAST);
+    als_update_mode(c, d);
+  }
+  als_fit(c, fit, lambda_host);
 }
 
 }  // namespace mkb

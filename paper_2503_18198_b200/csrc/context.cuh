@@ -44,9 +44,18 @@ struct ModeCopy {
   // packed element records for the streaming kernel (stream.cu): part A 16 B/element,
   // part B 0/4/8/16 B/element; padded to a multiple of 4 elements
   DevBuf<uint32_t> recA, recB;
-  DevBuf<uint32_t> stream_zero;  // pre-zero rows for the streaming kernel's segmentation
-  uint64_t stream_nzero = 0;
-  int stream_S = 0;
+  // pre-zero row lists (empty rows + rows split by the kernel's segmentation), cached per
+  // (kernel, segment length, shard range)
+  struct ZeroList {
+    DevBuf<uint32_t> rows;
+    uint64_t n = 0;
+    uint64_t key_seg = 0, key_tile = 0, key_e0 = ~0ull, key_e1 = ~0ull;
+  };
+  ZeroList zl_stream, zl_tiles;
+  // multi-GPU row-range shard of this copy: copy rows [k0, k1) = elements [e0, e1)
+  uint64_t shard_k0 = 0, shard_k1 = 0, shard_e0 = 0, shard_e1 = 0;
+  std::vector<uint64_t> shard_cuts;  // world+1 copy-row cut points (all ranks)
+  std::vector<uint32_t> row_ptr_host;
   bool built = false;
 };
 
@@ -69,6 +78,8 @@ struct Context {
   ModeCopy copies[kMaxModes];
   bool plans_built = false;
   uint64_t kappa = 0;
+  uint32_t shard_rank = 0, shard_world = 1;
+  DevBuf<uint64_t> shard_cuts_dev[kMaxModes];
 
   // factors / outputs (row-major I_d x R)
   uint32_t rank = 0;
@@ -103,6 +114,18 @@ void build_plans(Context& c, uint64_t kappa, int strategy, int policy);
 // Enqueue MTTKRP of `mode` reading factors in[w] and writing out (I_d x R).
 void launch_mttkrp(Context& c, uint32_t mode, const float* const* in, float* out, int exec);
 void reset_nonfinite(Context& c);
+// Empty rows + rows that continue across a segment start.  Segment starts are
+// e0a + t*tile + g*seg (g < tile/seg) inside [e0, e1).
+void ensure_zero_list(Context& c, uint32_t mode, ModeCopy::ZeroList& zl, uint32_t seg,
+                      uint32_t tile, uint64_t e0a, uint64_t e0, uint64_t e1);
+// Multi-GPU row-range shards (shard.cu).
+void set_shard(Context& c, uint32_t rank, uint32_t world);
+void shard_pack(Context& c, uint32_t mode, float* dst);
+void shard_unpack(Context& c, uint32_t mode, const float* src, uint64_t stride_rows);
+// ALS pieces (als.cu), used by the single-GPU iteration and the sharded driver.
+void als_prepare(Context& c);
+void als_update_mode(Context& c, uint32_t d);
+void als_fit(Context& c, double* fit, float* lambda_host);
 // Streaming TMA kernel (stream.cu); false when the shape has no specialisation.
 bool launch_stream(Context& c, uint32_t mode, const float* const* in, float* out);
 void pack_records(Context& c, uint32_t mode);

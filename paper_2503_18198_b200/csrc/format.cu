@@ -459,8 +459,14 @@ void build_plans(Context& c, uint64_t kappa, int strategy, int policy) {
     MKB_CUDA(cudaStreamSynchronize(st));
     mc.n_zero_rows = nempty + ntiles;
     mc.n_split_rows = nsplit;
+    mc.shard_k0 = 0;  // whole copy owned until mk_set_shard
+    mc.shard_k1 = nv;
+    mc.shard_e0 = 0;
+    mc.shard_e1 = nnz;
     mc.built = true;
   }
+  c.shard_rank = 0;
+  c.shard_world = 1;
   c.plans_built = true;
 }
 

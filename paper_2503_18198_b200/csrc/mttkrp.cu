@@ -39,7 +39,9 @@ struct MttkrpArgs {
   const uint32_t* row_ptr;
   unsigned long long* nonfinite;  // min (mode << 32 | offending copy position)
   unsigned long long tag;         // mode << 32
-  uint64_t nnz;
+  uint64_t nnz;       // total elements of the copy
+  uint64_t e0, e1;    // owned element range (whole copy unless sharded)
+  uint32_t k0;        // first owned copy row (deterministic kernel)
   uint32_t rank;
   uint32_t tile;
   uint32_t ntiles;
@@ -152,8 +154,8 @@ __global__ void __launch_bounds__(256) k_mttkrp_tiles(const MttkrpArgs a) {
   const uint32_t gid = (blockIdx.x * blockDim.x + threadIdx.x) / G;
 
   for (uint32_t t = gid; t < a.ntiles; t += groups) {
-    const uint64_t ta = static_cast<uint64_t>(t) * a.tile;
-    const uint64_t tb = min(ta + a.tile, a.nnz);
+    const uint64_t ta = a.e0 + static_cast<uint64_t>(t) * a.tile;
+    const uint64_t tb = min(ta + a.tile, a.e1);
     const bool head_split = ta > 0 && __ldg(a.out_idx + ta - 1) == __ldg(a.out_idx + ta);
     const bool tail_split = tb < a.nnz && __ldg(a.out_idx + tb) == __ldg(a.out_idx + tb - 1);
     uint32_t cur = __ldg(a.out_idx + ta);
@@ -233,7 +235,7 @@ __global__ void __launch_bounds__(256) k_mttkrp_rows(const MttkrpArgs a) {
   const uint32_t groups = (gridDim.x * blockDim.x) / G;
   const uint32_t gid = (blockIdx.x * blockDim.x + threadIdx.x) / G;
 
-  for (uint32_t k = gid; k < a.nrows; k += groups) {
+  for (uint32_t k = a.k0 + gid; k < a.k0 + a.nrows; k += groups) {
     const uint32_t row = __ldg(a.row_seq + k);
     const uint64_t s = __ldg(a.row_ptr + k), e = __ldg(a.row_ptr + k + 1);
     float acc[F];
@@ -293,18 +295,18 @@ __global__ void k_zero_rows(float* __restrict__ out, uint32_t R,
 __global__ void k_init_nonfinite(unsigned long long* p) { *p = ~0ull; }
 
 template <int NI, int VEC, int G, int KREP>
-void launch_cfg(Context& c, const MttkrpArgs& a, const ModeCopy& mc, int exec) {
+void launch_cfg(Context& c, const MttkrpArgs& a, ModeCopy& mc, uint32_t mode, int exec) {
   cudaStream_t st = c.stream;
   const int per_block = 256 / G;
-  if (mc.n_zero_rows) {
-    const unsigned blocks =
-        static_cast<unsigned>(std::min<uint64_t>(ceil_div(mc.n_zero_rows, per_block),
-                                                 c.num_sms * 8ull));
-    k_zero_rows<VEC, G, KREP><<<blocks, 256, 0, st>>>(a.out, a.rank, mc.zero_rows.get(),
-                                                      mc.n_zero_rows);
+  ModeCopy::ZeroList& zl = mc.zl_tiles;
+  ensure_zero_list(c, mode, zl, a.tile, a.tile, a.e0, a.e0, a.e1);
+  if (zl.n) {
+    const unsigned blocks = static_cast<unsigned>(
+        std::min<uint64_t>(ceil_div(zl.n, per_block), c.num_sms * 8ull));
+    k_zero_rows<VEC, G, KREP><<<blocks, 256, 0, st>>>(a.out, a.rank, zl.rows.get(), zl.n);
     MKB_LAUNCH();
   }
-  if (!a.nnz) return;
+  if (a.e1 <= a.e0) return;
   if (exec == MK_EXEC_DETERMINISTIC) {
     const unsigned blocks = static_cast<unsigned>(
         std::min<uint64_t>(ceil_div(a.nrows, per_block), c.num_sms * 16ull));
@@ -318,21 +320,21 @@ void launch_cfg(Context& c, const MttkrpArgs& a, const ModeCopy& mc, int exec) {
 }
 
 template <int NI>
-void launch_ni(Context& c, const MttkrpArgs& a, const ModeCopy& mc, int exec) {
+void launch_ni(Context& c, const MttkrpArgs& a, ModeCopy& mc, uint32_t mode, int exec) {
   const uint32_t R = a.rank;
   if constexpr (NI >= 2 && NI <= 4) {  // N = 3, 4, 5: 128-bit gather paths
     switch (R) {
-      case 16: return launch_cfg<NI, 4, 4, 1>(c, a, mc, exec);
-      case 32: return launch_cfg<NI, 4, 8, 1>(c, a, mc, exec);
-      case 64: return launch_cfg<NI, 4, 16, 1>(c, a, mc, exec);
-      case 128: return launch_cfg<NI, 4, 32, 1>(c, a, mc, exec);
+      case 16: return launch_cfg<NI, 4, 4, 1>(c, a, mc, mode, exec);
+      case 32: return launch_cfg<NI, 4, 8, 1>(c, a, mc, mode, exec);
+      case 64: return launch_cfg<NI, 4, 16, 1>(c, a, mc, mode, exec);
+      case 128: return launch_cfg<NI, 4, 32, 1>(c, a, mc, mode, exec);
       default: break;
     }
   }
-  if (R <= 32) return launch_cfg<NI, 1, 32, 1>(c, a, mc, exec);
-  if (R <= 64) return launch_cfg<NI, 1, 32, 2>(c, a, mc, exec);
-  if (R <= 128) return launch_cfg<NI, 1, 32, 4>(c, a, mc, exec);
-  if (R <= 256) return launch_cfg<NI, 1, 32, 8>(c, a, mc, exec);
+  if (R <= 32) return launch_cfg<NI, 1, 32, 1>(c, a, mc, mode, exec);
+  if (R <= 64) return launch_cfg<NI, 1, 32, 2>(c, a, mc, mode, exec);
+  if (R <= 128) return launch_cfg<NI, 1, 32, 4>(c, a, mc, mode, exec);
+  if (R <= 256) return launch_cfg<NI, 1, 32, 8>(c, a, mc, mode, exec);
   fail(MK_EINVAL, "kernel: rank above 256 is not supported on the device path");
 }
 
@@ -346,7 +348,7 @@ void reset_nonfinite(Context& c) {
 
 void launch_mttkrp(Context& c, uint32_t mode, const float* const* in, float* out, int exec) {
   if (exec == MK_EXEC_FAST && launch_stream(c, mode, in, out)) return;
-  const ModeCopy& mc = c.copies[mode];
+  ModeCopy& mc = c.copies[mode];
   MttkrpArgs a{};
   uint32_t ni = 0;
   for (uint32_t w = 0; w < c.n; ++w) {
@@ -366,17 +368,20 @@ void launch_mttkrp(Context& c, uint32_t mode, const float* const* in, float* out
   a.nnz = c.nnz;
   a.rank = c.rank;
   a.tile = mc.tile;
-  a.ntiles = c.nnz ? ceil_div(c.nnz, mc.tile) : 0;
-  a.nrows = static_cast<uint32_t>(mc.distinct);
+  a.e0 = mc.shard_e0;
+  a.e1 = mc.shard_e1;
+  a.k0 = static_cast<uint32_t>(mc.shard_k0);
+  a.ntiles = a.e1 > a.e0 ? ceil_div(a.e1 - a.e0, mc.tile) : 0;
+  a.nrows = static_cast<uint32_t>(mc.shard_k1 - mc.shard_k0);
   switch (ni) {
-    case 0: return launch_ni<0>(c, a, mc, exec);
-    case 1: return launch_ni<1>(c, a, mc, exec);
-    case 2: return launch_ni<2>(c, a, mc, exec);
-    case 3: return launch_ni<3>(c, a, mc, exec);
-    case 4: return launch_ni<4>(c, a, mc, exec);
-    case 5: return launch_ni<5>(c, a, mc, exec);
-    case 6: return launch_ni<6>(c, a, mc, exec);
-    case 7: return launch_ni<7>(c, a, mc, exec);
+    case 0: return launch_ni<0>(c, a, mc, mode, exec);
+    case 1: return launch_ni<1>(c, a, mc, mode, exec);
+    case 2: return launch_ni<2>(c, a, mc, mode, exec);
+    case 3: return launch_ni<3>(c, a, mc, mode, exec);
+    case 4: return launch_ni<4>(c, a, mc, mode, exec);
+    case 5: return launch_ni<5>(c, a, mc, mode, exec);
+    case 6: return launch_ni<6>(c, a, mc, mode, exec);
+    case 7: return launch_ni<7>(c, a, mc, mode, exec);
     default: fail(MK_EINVAL, "kernel: too many modes");
   }
 }

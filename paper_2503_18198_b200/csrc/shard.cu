@@ -1,0 +1,152 @@
+// Multi-GPU sharding of the mode copies and the kernels' pre-zero lists.
+//
+// Rank r of `world` owns, in every mode copy, the copy rows [k_r, k_{r+1}) where
+// k_r = first copy row whose start is >= floor(r * nnz / world) (mk_shard_cuts): element
+// ranges are nnz-balanced and cut at row boundaries, so each rank owns its output rows
+// outright (no cross-GPU reduction).  After a mode's local spMTTKRP, every rank packs its
+// rows (copy-row order) into a contiguous buffer, the buffers are all-gathered over NVLink
+// (NCCL), and every rank scatters the gathered rows back into row-index order.
+#include <algorithm>
+#include <vector>
+
+#include "context.cuh"
+
+namespace mkb {
+namespace {
+
+__global__ void k_segment_split_rows(const uint32_t* __restrict__ cd, uint64_t e0a, uint64_t e0,
+                                     uint64_t e1, uint32_t seg, uint32_t tile, uint64_t nseg,
+                                     uint32_t* out) {
+  const uint64_t s = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+  if (s >= nseg) return;
+  const uint32_t per = tile / seg;
+  const uint64_t p = e0a + (s / per) * tile + (s % per) * seg;
+  uint32_t row = 0xffffffffu;
+  if (p > e0 && p < e1 && cd[p - 1] == cd[p]) row = cd[p];
+  out[s] = row;
+}
+
+// out[i - k0] (row-major R) = src[row_seq[i]] for copy rows i in [k0, k1)
+__global__ void k_pack_rows(const float* __restrict__ src, const uint32_t* __restrict__ row_seq,
+                            uint64_t k0, uint64_t k1, uint32_t R, float* __restrict__ dst) {
+  const uint64_t total = (k1 - k0) * R;
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint64_t k = i / R, r = i - k * R;
+    dst[i] = src[static_cast<uint64_t>(row_seq[k0 + k]) * R + r];
+  }
+}
+
+// dst[row_seq[i]] = block_r[i - k_r] for every rank r, copy rows i in [k_r, k_{r+1})
+__global__ void k_unpack_rows(const float* __restrict__ src, const uint32_t* __restrict__ row_seq,
+                              const uint64_t* __restrict__ cuts, uint32_t world, uint64_t stride,
+                              uint32_t R, float* __restrict__ dst) {
+  const uint32_t r = blockIdx.y;
+  const uint64_t k0 = cuts[r], k1 = cuts[r + 1];
+  const uint64_t total = (k1 - k0) * R;
+  const float* blk = src + static_cast<uint64_t>(r) * stride * R;
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint64_t k = i / R, c = i - k * R;
+    dst[static_cast<uint64_t>(row_seq[k0 + k]) * R + c] = blk[i];
+  }
+}
+
+}  // namespace
+
+void ensure_zero_list(Context& c, uint32_t mode, ModeCopy::ZeroList& zl, uint32_t seg,
+                      uint32_t tile, uint64_t e0a, uint64_t e0, uint64_t e1) {
+  if (zl.key_seg == seg && zl.key_tile == tile && zl.key_e0 == e0 && zl.key_e1 == e1) return;
+  ModeCopy& mc = c.copies[mode];
+  cudaStream_t st = c.stream;
+  const uint64_t nempty = c.dims[mode] - mc.distinct;
+  const uint64_t ntiles = e1 > e0a ? (e1 - e0a + tile - 1) / tile : 0;
+  const uint64_t nseg = ntiles * (tile / seg);
+  zl.rows.resize(nempty + nseg + 1);
+  if (nempty)
+    MKB_CUDA(cudaMemcpyAsync(zl.rows.get(), mc.row_seq.get() + mc.distinct,
+                             nempty * sizeof(uint32_t), cudaMemcpyDeviceToDevice, st));
+  if (nseg) {
+    k_segment_split_rows<<<ceil_div(nseg, 256), 256, 0, st>>>(
+        mc.idx[mode].get(), e0a, e0, e1, seg, tile, nseg, zl.rows.get() + nempty);
+    MKB_LAUNCH();
+  }
+  zl.n = nempty + nseg;
+  zl.key_seg = seg;
+  zl.key_tile = tile;
+  zl.key_e0 = e0;
+  zl.key_e1 = e1;
+}
+
+void set_shard(Context& c, uint32_t rank, uint32_t world) {
+  if (world < 1 || rank >= world) fail(MK_EINVAL, "shard: rank must be below world size");
+  if (!c.plans_built) fail(MK_ESTATE, "shard: plans not built");
+  for (uint32_t d = 0; d < c.n; ++d) {
+    ModeCopy& mc = c.copies[d];
+    const uint64_t V = mc.distinct;
+    mc.row_ptr_host.resize(V + 1);
+    MKB_CUDA(cudaMemcpyAsync(mc.row_ptr_host.data(), mc.row_ptr.get(), (V + 1) * sizeof(uint32_t),
+                             cudaMemcpyDeviceToHost, c.stream));
+    MKB_CUDA(cudaStreamSynchronize(c.stream));
+    mc.shard_cuts.assign(world + 1, 0);
+    if (mk_shard_cuts(mc.row_ptr_host.data(), V, world, mc.shard_cuts.data()) != MK_OK)
+      fail(MK_EINVAL, "shard: cut computation failed");
+    c.shard_cuts_dev[d].resize(world + 1);
+    MKB_CUDA(cudaMemcpyAsync(c.shard_cuts_dev[d].get(), mc.shard_cuts.data(),
+                             (world + 1) * sizeof(uint64_t), cudaMemcpyHostToDevice, c.stream));
+    MKB_CUDA(cudaStreamSynchronize(c.stream));
+    mc.shard_k0 = mc.shard_cuts[rank];
+    mc.shard_k1 = mc.shard_cuts[rank + 1];
+    mc.shard_e0 = mc.row_ptr_host[mc.shard_k0];
+    mc.shard_e1 = mc.row_ptr_host[mc.shard_k1];
+  }
+  c.shard_rank = rank;
+  c.shard_world = world;
+}
+
+}  // namespace mkb
+
+using namespace mkb;
+
+extern "C" {
+
+int mk_shard_cuts(const uint32_t* row_ptr, uint64_t nrows, uint32_t world, uint64_t* cuts) {
+  if (!row_ptr || !cuts || world < 1) return MK_EINVAL;
+  const uint64_t nnz = row_ptr[nrows];
+  cuts[0] = 0;
+  for (uint32_t r = 1; r < world; ++r) {
+    const uint64_t target = (static_cast<unsigned __int128>(r) * nnz) / world;
+    const uint32_t* it = std::lower_bound(row_ptr, row_ptr + nrows + 1, target,
+                                          [](uint32_t a, uint64_t b) { return a < b; });
+    cuts[r] = std::max<uint64_t>(static_cast<uint64_t>(it - row_ptr), cuts[r - 1]);
+  }
+  cuts[world] = nrows;
+  return MK_OK;
+}
+
+}  // extern "C"
+
+namespace mkb {
+void shard_pack(Context& c, uint32_t mode, float* dst) {
+  ModeCopy& mc = c.copies[mode];
+  const uint64_t rows = mc.shard_k1 - mc.shard_k0;
+  if (!rows) return;
+  const unsigned blocks =
+      static_cast<unsigned>(std::min<uint64_t>((rows * c.rank + 255) / 256, c.num_sms * 8ull));
+  k_pack_rows<<<blocks, 256, 0, c.stream>>>(c.outputs[mode].get(), mc.row_seq.get(), mc.shard_k0,
+                                            mc.shard_k1, c.rank, dst);
+  MKB_LAUNCH();
+}
+
+void shard_unpack(Context& c, uint32_t mode, const float* src, uint64_t stride_rows) {
+  ModeCopy& mc = c.copies[mode];
+  const uint32_t world = static_cast<uint32_t>(mc.shard_cuts.size() - 1);
+  const DevBuf<uint64_t>& cuts = c.shard_cuts_dev[mode];
+  const unsigned bx = static_cast<unsigned>(
+      std::min<uint64_t>((stride_rows * c.rank + 255) / 256 + 1, c.num_sms * 4ull));
+  k_unpack_rows<<<dim3(bx, world), 256, 0, c.stream>>>(src, mc.row_seq.get(), cuts.get(), world,
+                                                       stride_rows, c.rank,
+                                                       c.outputs[mode].get());
+  MKB_LAUNCH();
+}
+}  // namespace mkb

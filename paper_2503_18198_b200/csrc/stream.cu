@@ -61,7 +61,10 @@ struct StreamArgs {
   float* out;
   unsigned long long* nonfinite;
   unsigned long long tag;
-  uint32_t nnz;
+  uint32_t nnz;   // total elements of the copy
+  uint32_t e0a;   // tile origin: e0 rounded down to 4 elements (TMA 16-byte alignment)
+  uint32_t e0;    // owned element range [e0, e1) (whole copy unless sharded)
+  uint32_t e1;
   uint32_t rank;
 };
 
@@ -153,8 +156,8 @@ __global__ void __launch_bounds__(256, 3) k_mttkrp_stream(const StreamArgs a) {
   const int tid = threadIdx.x;
   const int lane_g = tid % G;
   const int g = tid / G;
-  const uint32_t nnz = a.nnz, R = a.rank;
-  const uint32_t ntiles = (nnz + TILE - 1) / TILE;
+  const uint32_t nnz = a.nnz, R = a.rank, e0a = a.e0a, e0 = a.e0, e1 = a.e1;
+  const uint32_t ntiles = (e1 - e0a + TILE - 1) / TILE;
 
   const float* Y[NI];
 #pragma unroll
@@ -166,8 +169,8 @@ __global__ void __launch_bounds__(256, 3) k_mttkrp_stream(const StreamArgs a) {
   unsigned long long* gnf = a.nonfinite;
   const unsigned long long tag = a.tag;
   auto issue = [=](uint32_t tile, int stage) {
-    const uint32_t base = tile * TILE;
-    const uint32_t cnt = nnz - base < TILE ? nnz - base : TILE;
+    const uint32_t base = e0a + tile * TILE;
+    const uint32_t cnt = e1 - base < TILE ? e1 - base : TILE;
     const uint32_t cnt4 = (cnt + 3u) & ~3u;  // arrays are padded to 4 elements
     const uint32_t ba = cnt4 * 16u, bb = cnt4 * 4u * BW;
     mbar_arrive_tx(&bar[stage], ba + bb);
@@ -191,9 +194,13 @@ __global__ void __launch_bounds__(256, 3) k_mttkrp_stream(const StreamArgs a) {
   for (uint32_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
     const int stage = it & 1;
     mbar_wait(&bar[stage], (it >> 1) & 1);
-    const uint32_t base = tile * TILE;
-    const uint32_t p0 = base + g * S;
-    const uint32_t p1 = nnz - p0 < S ? nnz : p0 + S;
+    const uint32_t base = e0a + tile * TILE;
+    const uint32_t s0 = base + g * S;
+    const uint32_t p0 = s0 < e0 ? e0 : s0;
+    const uint32_t p1 = s0 >= e1 ? p0 : (e1 - s0 < S ? e1 : s0 + S);  // empty past e1
+    bool have = false, last_atomic = false;
+    uint32_t cur = 0xffffffffu;
+    float2 acc0 = make_float2(0.f, 0.f), acc1 = make_float2(0.f, 0.f);
     if (p0 < p1) {
       const uint4* A = stageA(stage);
       const uint32_t* B = stageB(stage);
@@ -201,10 +208,9 @@ __global__ void __launch_bounds__(256, 3) k_mttkrp_stream(const StreamArgs a) {
       const bool tail_split = p1 < nnz && __ldg(gcd + p1) == __ldg(gcd + p1 - 1);
       uint32_t w[8];
       read_record<NI, BW>(A, B, static_cast<int>(p0 - base), w);
-      uint32_t cur = w[Layout<NI>::CD];
+      cur = w[Layout<NI>::CD];
       uint32_t run_start = p0;
       bool first = true;
-      float2 acc0 = make_float2(0.f, 0.f), acc1 = make_float2(0.f, 0.f);
       for (uint32_t j = p0; j < p1; ++j) {
         if (j > p0) read_record<NI, BW>(A, B, static_cast<int>(j - base), w);
         const float v = __uint_as_float(w[Layout<NI>::VAL]);
@@ -233,24 +239,33 @@ __global__ void __launch_bounds__(256, 3) k_mttkrp_stream(const StreamArgs a) {
       }
       if (!isfinite(acc0.x + acc0.y + acc1.x + acc1.y))
         stream_rescan<NI, G>(gA, gB, Y, R, lane_g, run_start, p1, gnf, tag);
-      flush_row(gout, cur, R, lane_g, acc0, acc1, tail_split || (first && head_split));
+      have = true;
+      last_atomic = tail_split || (first && head_split);
     }
+    // Last run of each group.  When every group of the warp ends inside the same split row
+    // (long rows: Scheme 2 modes, power-law heads) combine the partial sums with a
+    // butterfly and issue ONE vector atomic per warp instead of one per group.
+    bool combined = false;
+    if constexpr (G < 32) {
+      const uint32_t key = (have && last_atomic) ? cur : 0xffffffffu;
+      int same = 0;
+      __match_all_sync(0xffffffffu, key, &same);
+      if (same && key != 0xffffffffu) {
+#pragma unroll
+        for (int off = G; off < 32; off <<= 1) {
+          acc0.x += __shfl_xor_sync(0xffffffffu, acc0.x, off);
+          acc0.y += __shfl_xor_sync(0xffffffffu, acc0.y, off);
+          acc1.x += __shfl_xor_sync(0xffffffffu, acc1.x, off);
+          acc1.y += __shfl_xor_sync(0xffffffffu, acc1.y, off);
+        }
+        if ((tid & 31) < G) flush_row(gout, cur, R, lane_g, acc0, acc1, true);
+        combined = true;
+      }
+    }
+    if (have && !combined) flush_row(gout, cur, R, lane_g, acc0, acc1, last_atomic);
     __syncthreads();  // every group is done with this stage
     if (tid == 0 && tile + 2 * gridDim.x < ntiles) issue(tile + 2 * gridDim.x, stage);
   }
-}
-
-// Split rows for segment length S and tile TILE: row at each group start p (p > 0)
-// that continues from p-1.
-__global__ void k_stream_split_rows(const uint32_t* __restrict__ cd, uint32_t nnz, uint32_t S,
-                                    uint32_t tile, uint32_t nseg, uint32_t* out) {
-  const uint32_t s = blockIdx.x * blockDim.x + threadIdx.x;
-  if (s >= nseg) return;
-  const uint32_t per = tile / S;
-  const uint64_t p = static_cast<uint64_t>(s / per) * tile + static_cast<uint64_t>(s % per) * S;
-  uint32_t row = 0xffffffffu;
-  if (p > 0 && p < nnz && cd[p - 1] == cd[p]) row = cd[p];
-  out[s] = row;
 }
 
 template <int G>
@@ -277,30 +292,17 @@ void launch_stream_cfg(Context& c, ModeCopy& mc, uint32_t mode, const float* con
                        float* out) {
   constexpr int TILE = (256 / G) * S;
   cudaStream_t st = c.stream;
-  // split-row list for this segmentation (cached per copy)
-  if (mc.stream_S != S) {
-    const uint32_t ntiles = (c.nnz + TILE - 1) / TILE;
-    const uint32_t nseg = ntiles * (TILE / S);
-    const uint64_t nempty = c.dims[mode] - mc.distinct;
-    mc.stream_zero.resize(nempty + nseg + 1);
-    if (nempty)
-      MKB_CUDA(cudaMemcpyAsync(mc.stream_zero.get(), mc.row_seq.get() + mc.distinct,
-                               nempty * sizeof(uint32_t), cudaMemcpyDeviceToDevice, st));
-    if (nseg) {
-      k_stream_split_rows<<<ceil_div(nseg, 256), 256, 0, st>>>(mc.idx[mode].get(), c.nnz, S, TILE,
-                                                               nseg, mc.stream_zero.get() + nempty);
-      MKB_LAUNCH();
-    }
-    mc.stream_nzero = nempty + nseg;
-    mc.stream_S = S;
-  }
-  if (mc.stream_nzero) {
-    const unsigned blocks = static_cast<unsigned>(
-        std::min<uint64_t>(ceil_div(mc.stream_nzero, 256 / G), c.num_sms * 8ull));
-    k_stream_zero<G><<<blocks, 256, 0, st>>>(out, c.rank, mc.stream_zero.get(), mc.stream_nzero);
+  const uint32_t e0 = static_cast<uint32_t>(mc.shard_e0), e1 = static_cast<uint32_t>(mc.shard_e1);
+  const uint32_t e0a = e0 & ~3u;
+  ModeCopy::ZeroList& zl = mc.zl_stream;
+  ensure_zero_list(c, mode, zl, S, TILE, e0a, e0, e1);
+  if (zl.n) {
+    const unsigned blocks =
+        static_cast<unsigned>(std::min<uint64_t>(ceil_div(zl.n, 256 / G), c.num_sms * 8ull));
+    k_stream_zero<G><<<blocks, 256, 0, st>>>(out, c.rank, zl.rows.get(), zl.n);
     MKB_LAUNCH();
   }
-  if (!c.nnz) return;
+  if (e1 <= e0) return;
   StreamArgs a{};
   a.recA = reinterpret_cast<const uint4*>(mc.recA.get());
   a.recB = mc.recB.get();
@@ -312,6 +314,9 @@ void launch_stream_cfg(Context& c, ModeCopy& mc, uint32_t mode, const float* con
   a.nonfinite = c.nonfinite.get();
   a.tag = static_cast<unsigned long long>(mode) << 32;
   a.nnz = static_cast<uint32_t>(c.nnz);
+  a.e0a = e0a;
+  a.e0 = e0;
+  a.e1 = e1;
   a.rank = c.rank;
   const size_t smem = smem_bytes<NI, G, S>();
   // per-device launch setup, done once (keeps the per-launch host cost to the launch)
@@ -325,7 +330,7 @@ void launch_stream_cfg(Context& c, ModeCopy& mc, uint32_t mode, const float* con
                                                            smem));
     if (per_sm < 1) per_sm = 1;
   }
-  const uint32_t ntiles = (c.nnz + TILE - 1) / TILE;
+  const uint32_t ntiles = (e1 - e0a + TILE - 1) / TILE;
   const unsigned grid =
       static_cast<unsigned>(std::max<uint64_t>(1, std::min<uint64_t>(ntiles, c.num_sms * std::max(per_sm, 1))));
   k_mttkrp_stream<NI, G, S><<<grid, 256, smem, st>>>(a);
@@ -379,7 +384,6 @@ void pack_records(Context& c, uint32_t mode) {
   ModeCopy& mc = c.copies[mode];
   mc.recA.release();
   mc.recB.release();
-  mc.stream_S = 0;
   if (c.n < 3 || c.n > 5 || c.nnz == 0) return;
   const uint32_t words = c.n + 1;  // (n-1) inputs + value + c_d
   const uint32_t bw = words <= 4 ? 0 : (words - 4 <= 2 ? words - 4 : 4);
