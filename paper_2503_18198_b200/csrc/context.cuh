@@ -44,6 +44,7 @@ struct ModeCopy {
   // packed element records for the streaming kernel (stream.cu): part A 16 B/element,
   // part B 0/4/8/16 B/element; padded to a multiple of 4 elements
   DevBuf<uint32_t> recA, recB;
+  DevBuf<uint32_t> kperm;  // kernel (fiber) order -> reference copy position
   // pre-zero row lists (empty rows + rows split by the kernel's segmentation), cached per
   // (kernel, segment length, shard range)
   struct ZeroList {
@@ -128,7 +129,7 @@ void als_update_mode(Context& c, uint32_t d);
 void als_fit(Context& c, double* fit, float* lambda_host);
 // Streaming TMA kernel (stream.cu); false when the shape has no specialisation.
 bool launch_stream(Context& c, uint32_t mode, const float* const* in, float* out);
-void pack_records(Context& c, uint32_t mode);
+void pack_records(Context& c, uint32_t mode, const uint32_t* rank_of_row);
 void check_nonfinite(Context& c);  // synchronises; throws MK_ENONFINITE
 
 }  // namespace mkb

@@ -438,7 +438,7 @@ void build_plans(Context& c, uint64_t kappa, int strategy, int policy) {
       MKB_LAUNCH();
     }
     // 5b. packed records for the streaming kernel
-    pack_records(c, d);
+    pack_records(c, d, rank_of_row.get());
     // zero-row list: empty rows (row_seq[nv:ext]) + rows split at fast-kernel tile starts
     mc.tile = choose_tile(nnz, c.num_sms);
     const uint32_t ntiles = nnz ? ceil_div(nnz, mc.tile) : 0;

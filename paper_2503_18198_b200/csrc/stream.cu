@@ -57,6 +57,7 @@ struct StreamArgs {
   const uint4* recA;         // nnz (padded to 4) x 16 B
   const uint32_t* recB;      // nnz (padded) x BW words, BW = 0/1/2/4
   const uint32_t* out_idx;   // copy-order c_d (head/tail split tests)
+  const uint32_t* kperm;     // kernel position -> reference copy position
   const float* in_Y[kMaxModes];
   float* out;
   unsigned long long* nonfinite;
@@ -105,8 +106,11 @@ template <int NI, int G>
 __device__ __forceinline__ void stream_rescan(const uint4* recA, const uint32_t* recB,
                                               const float* const (&Y)[NI], uint32_t R,
                                               int lane_g, uint32_t s, uint32_t e,
-                                              unsigned long long* nf, unsigned long long tag) {
+                                              const uint32_t* kperm, unsigned long long* nf,
+                                              unsigned long long tag) {
   constexpr int BW = Layout<NI>::BW;
+  // every offending element of the run reports its REFERENCE copy position (kperm), so the
+  // minimum over the launch is the reference's first failing position
   for (uint32_t j = s; j < e; ++j) {
     uint32_t w[8];
     read_record<NI, BW>(recA, recB, static_cast<int>(j), w);
@@ -120,10 +124,8 @@ __device__ __forceinline__ void stream_rescan(const uint4* recA, const uint32_t*
       t[2] = __fmul_rn(t[2], y.z);
       t[3] = __fmul_rn(t[3], y.w);
     }
-    if (!isfinite(t[0]) || !isfinite(t[1]) || !isfinite(t[2]) || !isfinite(t[3])) {
-      atomicMin(nf, tag | static_cast<unsigned long long>(j));
-      return;
-    }
+    if (!isfinite(t[0]) || !isfinite(t[1]) || !isfinite(t[2]) || !isfinite(t[3]))
+      atomicMin(nf, tag | static_cast<unsigned long long>(kperm[j]));
   }
 }
 
@@ -165,6 +167,7 @@ __global__ void __launch_bounds__(256, 3) k_mttkrp_stream(const StreamArgs a) {
   const uint4* gA = a.recA;
   const uint32_t* gB = a.recB;
   const uint32_t* gcd = a.out_idx;
+  const uint32_t* gkp = a.kperm;
   float* gout = a.out;
   unsigned long long* gnf = a.nonfinite;
   const unsigned long long tag = a.tag;
@@ -211,22 +214,30 @@ __global__ void __launch_bounds__(256, 3) k_mttkrp_stream(const StreamArgs a) {
       cur = w[Layout<NI>::CD];
       uint32_t run_start = p0;
       bool first = true;
+      // factor rows held in registers across elements: re-gathered only when the
+      // coordinate changes (fiber order makes the small modes' rows repeat)
+      float4 yv[NI];
+      uint32_t yc[NI];
+#pragma unroll
+      for (int i = 0; i < NI; ++i) yc[i] = 0xffffffffu;
       for (uint32_t j = p0; j < p1; ++j) {
         if (j > p0) read_record<NI, BW>(A, B, static_cast<int>(j - base), w);
         const float v = __uint_as_float(w[Layout<NI>::VAL]);
         float2 t0 = make_float2(v, v), t1 = t0;
 #pragma unroll
         for (int i = 0; i < NI; ++i) {
-          const float4 y =
-              __ldg(reinterpret_cast<const float4*>(Y[i] + static_cast<size_t>(w[i]) * R) +
-                    lane_g);
-          t0 = __fmul2_rn(t0, make_float2(y.x, y.y));
-          t1 = __fmul2_rn(t1, make_float2(y.z, y.w));
+          if (w[i] != yc[i]) {
+            yv[i] = __ldg(reinterpret_cast<const float4*>(Y[i] + static_cast<size_t>(w[i]) * R) +
+                          lane_g);
+            yc[i] = w[i];
+          }
+          t0 = __fmul2_rn(t0, make_float2(yv[i].x, yv[i].y));
+          t1 = __fmul2_rn(t1, make_float2(yv[i].z, yv[i].w));
         }
         const uint32_t row = w[Layout<NI>::CD];
         if (row != cur) {
           if (!isfinite(acc0.x + acc0.y + acc1.x + acc1.y))
-            stream_rescan<NI, G>(gA, gB, Y, R, lane_g, run_start, j, gnf, tag);
+            stream_rescan<NI, G>(gA, gB, Y, R, lane_g, run_start, j, gkp, gnf, tag);
           flush_row(gout, cur, R, lane_g, acc0, acc1, first && head_split);
           first = false;
           cur = row;
@@ -238,7 +249,7 @@ __global__ void __launch_bounds__(256, 3) k_mttkrp_stream(const StreamArgs a) {
         acc1 = __fadd2_rn(acc1, t1);
       }
       if (!isfinite(acc0.x + acc0.y + acc1.x + acc1.y))
-        stream_rescan<NI, G>(gA, gB, Y, R, lane_g, run_start, p1, gnf, tag);
+        stream_rescan<NI, G>(gA, gB, Y, R, lane_g, run_start, p1, gkp, gnf, tag);
       have = true;
       last_atomic = tail_split || (first && head_split);
     }
@@ -307,6 +318,7 @@ void launch_stream_cfg(Context& c, ModeCopy& mc, uint32_t mode, const float* con
   a.recA = reinterpret_cast<const uint4*>(mc.recA.get());
   a.recB = mc.recB.get();
   a.out_idx = mc.idx[mode].get();
+  a.kperm = mc.kperm.get();
   uint32_t ni = 0;
   for (uint32_t w = 0; w < c.n; ++w)
     if (w != mode) a.in_Y[ni++] = in[w];
@@ -361,30 +373,78 @@ bool launch_stream(Context& c, uint32_t mode, const float* const* in, float* out
   }
 }
 
-// Pack the SoA copy of `mode` into part A / part B records (format build, step 5b).
+// Kernel order of a mode copy (format build, step 5b).  The exported plan order and the
+// SoA copy stay the reference's (layout.cpp:141-151); the streaming kernel additionally
+// reads its records in "fiber order": inside every output row (row runs and their order
+// are unchanged) the elements are stably sorted by the coordinates of the two smallest
+// input modes.  Consecutive elements then share those factor rows, which the kernel keeps
+// in registers instead of re-gathering (CSF-style reuse without a tree), and the larger
+// factors are visited in narrow windows (L1 locality).  kperm[i] = reference copy position.
+__global__ void k_gather_keys(const uint32_t* __restrict__ src, const uint32_t* __restrict__ perm,
+                              uint64_t n, uint32_t* __restrict__ keys) {
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
+    keys[i] = src[perm[i]];
+}
+__global__ void k_gather_rank_keys(const uint32_t* __restrict__ cd,
+                                   const uint32_t* __restrict__ rank_of_row,
+                                   const uint32_t* __restrict__ perm, uint64_t n,
+                                   uint32_t* __restrict__ keys) {
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
+    keys[i] = rank_of_row[cd[perm[i]]];
+}
+
+// Pack the SoA copy of `mode` into part A / part B records in kernel order.
 __global__ void k_pack_records(const uint32_t* const* idx, const float* __restrict__ val,
-                               uint32_t n, uint32_t mode, uint64_t nnz, uint64_t padded,
-                               uint32_t bw, uint4* recA, uint32_t* recB) {
+                               const uint32_t* __restrict__ perm, uint32_t n, uint32_t mode,
+                               uint64_t nnz, uint64_t padded, uint32_t bw, uint4* recA,
+                               uint32_t* recB) {
   for (uint64_t j = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; j < padded;
        j += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
     uint32_t w[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     if (j < nnz) {
+      const uint32_t s = perm[j];
       uint32_t k = 0;
       for (uint32_t m = 0; m < n; ++m)
-        if (m != mode) w[k++] = idx[m][j];
-      w[k++] = __float_as_uint(val[j]);
-      w[k++] = idx[mode][j];
+        if (m != mode) w[k++] = idx[m][s];
+      w[k++] = __float_as_uint(val[s]);
+      w[k++] = idx[mode][s];
     }
     recA[j] = make_uint4(w[0], w[1], w[2], w[3]);
     for (uint32_t q = 0; q < bw; ++q) recB[j * bw + q] = w[4 + q];
   }
 }
 
-void pack_records(Context& c, uint32_t mode) {
+void pack_records(Context& c, uint32_t mode, const uint32_t* rank_of_row) {
   ModeCopy& mc = c.copies[mode];
   mc.recA.release();
   mc.recB.release();
+  mc.kperm.release();
   if (c.n < 3 || c.n > 5 || c.nnz == 0) return;
+  cudaStream_t st = c.stream;
+  const uint64_t nnz = c.nnz;
+  const unsigned gblocks = static_cast<unsigned>(std::min<uint64_t>((nnz + 255) / 256, c.num_sms * 16ull));
+  // fiber order: LSD stable sorts by (second-smallest input, smallest input, row rank)
+  std::vector<uint32_t> inputs;
+  for (uint32_t w = 0; w < c.n; ++w)
+    if (w != mode) inputs.push_back(w);
+  std::stable_sort(inputs.begin(), inputs.end(),
+                   [&](uint32_t a, uint32_t b) { return c.dims[a] < c.dims[b]; });
+  mc.kperm.resize(nnz);
+  DevBuf<uint32_t> keys(nnz);
+  iota_u32(mc.kperm.get(), nnz, st);
+  for (int k = std::min<int>(2, static_cast<int>(inputs.size())) - 1; k >= 0; --k) {
+    const uint32_t w = inputs[k];
+    k_gather_keys<<<gblocks, 256, 0, st>>>(mc.idx[w].get(), mc.kperm.get(), nnz, keys.get());
+    MKB_LAUNCH();
+    radix_sort_pairs(keys.get(), mc.kperm.get(), nnz, bits_for(c.dims[w] - 1), c.scratch, st);
+  }
+  k_gather_rank_keys<<<gblocks, 256, 0, st>>>(mc.idx[mode].get(), rank_of_row, mc.kperm.get(), nnz,
+                                             keys.get());
+  MKB_LAUNCH();
+  radix_sort_pairs(keys.get(), mc.kperm.get(), nnz, bits_for(mc.distinct ? mc.distinct - 1 : 0),
+                   c.scratch, st);
   const uint32_t words = c.n + 1;  // (n-1) inputs + value + c_d
   const uint32_t bw = words <= 4 ? 0 : (words - 4 <= 2 ? words - 4 : 4);
   const uint64_t padded = (c.nnz + 3) & ~3ull;
@@ -396,8 +456,9 @@ void pack_records(Context& c, uint32_t mode) {
   MKB_CUDA(cudaMemcpyAsync(ptrs.get(), hp, c.n * sizeof(uint32_t*), cudaMemcpyHostToDevice,
                            c.stream));
   const unsigned blocks = static_cast<unsigned>(std::min<uint64_t>((padded + 255) / 256, c.num_sms * 16ull));
-  k_pack_records<<<blocks, 256, 0, c.stream>>>(ptrs.get(), mc.val.get(), c.n, mode, c.nnz, padded,
-                                               bw, reinterpret_cast<uint4*>(mc.recA.get()),
+  k_pack_records<<<blocks, 256, 0, c.stream>>>(ptrs.get(), mc.val.get(), mc.kperm.get(), c.n, mode,
+                                               c.nnz, padded, bw,
+                                               reinterpret_cast<uint4*>(mc.recA.get()),
                                                mc.recB.get());
   MKB_LAUNCH();
   MKB_CUDA(cudaStreamSynchronize(c.stream));  // ptrs is freed on return
