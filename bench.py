@@ -361,7 +361,7 @@ def our_arm(args, cfg, rank, world, local_rank):
         "cpd_als_ms_per_iter": als_ms,
         "parity_fast_vs_deterministic_max_rel_err": parity,
     }
-    if world == 1:
+    if world == 1 and not args.no_cpu:
         try:
             line["cpu_baseline"] = cpu_baseline_sample(cfg, t, factors)
         except Exception as e:  # pragma: no cover
@@ -378,6 +378,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--config", default="cfg2", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu", action="store_true",
+                    help="skip the cpu_baseline sample (kernel-tuning runs only)")
     ap.add_argument("--profile", action="store_true",
                     help="only build + run --steps flushed sweeps (for ncu); prints no JSON")
     args = ap.parse_args()

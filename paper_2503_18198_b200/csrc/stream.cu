@@ -13,8 +13,9 @@
 // Inside a tile each lane group (G = R/4 lanes, 128-bit per lane) owns S consecutive
 // elements (S odd: the groups of a warp read their records from different bank quads).
 // Per element a group gathers the N-1 input factor rows with 128-bit L1-cached loads —
-// software-pipelined one element ahead and skipped while the coordinate repeats (fiber
-// order) — multiplies with packed FMUL2, and accumulates the output row in registers while
+// issued in batches of B elements before any is consumed (fiber order keeps the large
+// factors in a narrow, L1-resident window) — multiplies with packed FMUL2, and
+// accumulates the output row in registers while
 // c_d is unchanged.  A run that starts and ends inside the group's S elements is owned and
 // stored with a plain 128-bit store (Local_Update); runs crossing an S boundary are added
 // with a vector atomic (Global_Update), combined across the warp first when all its groups
@@ -148,8 +149,9 @@ __device__ __forceinline__ void flush_row(float4* outv, uint32_t row, float2 a0,
 }
 
 // MINB = minimum resident CTAs per SM the register budget is tuned for (3: <= 85 regs,
-// 4: <= 64 regs); selected at run time (MKB_STREAM_MINB, default below).
-template <int NI, int G, int S, int MINB>
+// 4: <= 64 regs); B = elements per gather batch.  Variant picked at run time
+// (MKB_STREAM_VARIANT, stream_variant()).
+template <int NI, int G, int S, int MINB, int B, int PD>
 __global__ void __launch_bounds__(256, MINB) k_mttkrp_stream(const StreamArgs a) {
   constexpr int BW = Layout<NI>::BW;
   constexpr int VAL = Layout<NI>::VAL, CD = Layout<NI>::CD;
@@ -218,60 +220,83 @@ __global__ void __launch_bounds__(256, MINB) k_mttkrp_stream(const StreamArgs a)
       const bool head_split = p0 > 0 && __ldg(gcd + p0 - 1) == __ldg(gcd + p0);
       const bool tail_split = p1 < nnz && __ldg(gcd + p1) == __ldg(gcd + p1 - 1);
       const uint32_t n = p1 - p0;
-      uint32_t w[NI + 2];
-      read_record<NI>(ra, rb, 0, w);
-      cur = w[CD];
+      {
+        uint32_t w0[NI + 2];
+        read_record<NI>(ra, rb, 0, w0);
+        cur = w0[CD];
+      }
       uint32_t run_start = p0;
       bool first = true;
-      float4 y[NI];
+      // Batches of B elements: all B records are read and all B*(N-1) gathers issued before
+      // any of them is consumed (memory-level parallelism without a rotating pipeline).
+      if constexpr (PD > 0) {
+        // prologue of the L1 prefetch stream (elements [0, PD))
 #pragma unroll
-      for (int i = 0; i < NI; ++i) y[i] = __ldg(Yv[i] + static_cast<size_t>(w[i]) * G);
-      for (uint32_t k = 0; k < n; ++k) {
-        // --- software pipeline: next record and its gathers are issued before the math
-        //     of element k (rows re-used while the coordinate repeats)
-        uint32_t wn[NI + 2];
-        float4 yn[NI];
-        const bool more = k + 1 < n;
-        if (more) {
-          read_record<NI>(ra, rb, k + 1, wn);
-        } else {
+        for (int kp = 0; kp < PD; ++kp) {
+          if (static_cast<uint32_t>(kp) < n) {
+            uint32_t wp[NI + 2];
+            read_record<NI>(ra, rb, kp, wp);
 #pragma unroll
-          for (int q = 0; q < NI + 2; ++q) wn[q] = w[q];
+            for (int i = 0; i < NI; ++i)
+              asm volatile("prefetch.global.L1 [%0];" ::"l"(Yv[i] +
+                                                            static_cast<size_t>(wp[i]) * G));
+          }
+        }
+      }
+      for (uint32_t k = 0; k < n; k += B) {
+        if constexpr (PD > 0) {
+          // rows PD elements ahead are pulled into L1 without holding registers, so the
+          // real gathers below mostly hit L1 (latency hiding beyond the register budget)
+#pragma unroll
+          for (int b = 0; b < B; ++b) {
+            const uint32_t kp = k + PD + b;
+            if (kp < n) {
+              uint32_t wp[NI + 2];
+              read_record<NI>(ra, rb, kp, wp);
+#pragma unroll
+              for (int i = 0; i < NI; ++i)
+                asm volatile("prefetch.global.L1 [%0];" ::"l"(Yv[i] +
+                                                              static_cast<size_t>(wp[i]) * G));
+            }
+          }
+        }
+        uint32_t w[B][NI + 2];
+        float4 y[B][NI];
+#pragma unroll
+        for (int b = 0; b < B; ++b) {
+          const uint32_t kk = k + b < n ? k + b : n - 1;  // clamp: tail lanes re-read the last
+          read_record<NI>(ra, rb, kk, w[b]);
         }
 #pragma unroll
-        for (int i = 0; i < NI; ++i) {
-          if (wn[i] != w[i])
-            yn[i] = __ldg(Yv[i] + static_cast<size_t>(wn[i]) * G);
-          else
-            yn[i] = y[i];
-        }
-        // --- element k
-        const float v = __uint_as_float(w[VAL]);
-        float2 t0 = make_float2(v, v), t1 = t0;
+        for (int b = 0; b < B; ++b)
 #pragma unroll
-        for (int i = 0; i < NI; ++i) {
-          t0 = __fmul2_rn(t0, make_float2(y[i].x, y[i].y));
-          t1 = __fmul2_rn(t1, make_float2(y[i].z, y[i].w));
-        }
-        const uint32_t row = w[CD];
-        if (row != cur) {
-          if (!isfinite(acc0.x + acc0.y + acc1.x + acc1.y))
-            stream_rescan<NI, G>(gA, gB, a.in_Y[0], NI > 1 ? a.in_Y[1] : nullptr,
-                                 NI > 2 ? a.in_Y[2] : nullptr, NI > 3 ? a.in_Y[3] : nullptr,
-                                 lane_g, run_start, p0 + k, a.kperm, a.nonfinite, a.tag);
-          flush_row(outv, cur, acc0, acc1, first && head_split, G);
-          first = false;
-          cur = row;
-          run_start = p0 + k;
-          acc0 = make_float2(0.f, 0.f);
-          acc1 = acc0;
-        }
-        acc0 = __fadd2_rn(acc0, t0);
-        acc1 = __fadd2_rn(acc1, t1);
+          for (int i = 0; i < NI; ++i) y[b][i] = __ldg(Yv[i] + static_cast<size_t>(w[b][i]) * G);
 #pragma unroll
-        for (int q = 0; q < NI + 2; ++q) w[q] = wn[q];
+        for (int b = 0; b < B; ++b) {
+          if (B > 1 && k + b >= n) break;
+          const float v = __uint_as_float(w[b][VAL]);
+          float2 t0 = make_float2(v, v), t1 = t0;
 #pragma unroll
-        for (int i = 0; i < NI; ++i) y[i] = yn[i];
+          for (int i = 0; i < NI; ++i) {
+            t0 = __fmul2_rn(t0, make_float2(y[b][i].x, y[b][i].y));
+            t1 = __fmul2_rn(t1, make_float2(y[b][i].z, y[b][i].w));
+          }
+          const uint32_t row = w[b][CD];
+          if (row != cur) {
+            if (!isfinite(acc0.x + acc0.y + acc1.x + acc1.y))
+              stream_rescan<NI, G>(gA, gB, a.in_Y[0], NI > 1 ? a.in_Y[1] : nullptr,
+                                   NI > 2 ? a.in_Y[2] : nullptr, NI > 3 ? a.in_Y[3] : nullptr,
+                                   lane_g, run_start, p0 + k + b, a.kperm, a.nonfinite, a.tag);
+            flush_row(outv, cur, acc0, acc1, first && head_split, G);
+            first = false;
+            cur = row;
+            run_start = p0 + k + b;
+            acc0 = make_float2(0.f, 0.f);
+            acc1 = acc0;
+          }
+          acc0 = __fadd2_rn(acc0, t0);
+          acc1 = __fadd2_rn(acc1, t1);
+        }
       }
       if (!isfinite(acc0.x + acc0.y + acc1.x + acc1.y))
         stream_rescan<NI, G>(gA, gB, a.in_Y[0], NI > 1 ? a.in_Y[1] : nullptr,
@@ -326,30 +351,30 @@ size_t smem_bytes() {
   return 2u * TILE * 16u + 2u * TILE * 4u * Layout<NI>::BW + 64;
 }
 
-template <int NI, int G, int S, int MINB>
+template <int NI, int G, int S, int MINB, int B, int PD>
 void launch_stream_kernel(Context& c, const StreamArgs& a, uint32_t ntiles, cudaStream_t st) {
   const size_t smem = smem_bytes<NI, G, S>();
   // per-device launch setup, done once (keeps the per-launch host cost to the launch)
   static int per_sm_cache[64] = {};
   int& per_sm = per_sm_cache[c.device & 63];
   if (!per_sm) {
-    MKB_CUDA(cudaFuncSetAttribute(k_mttkrp_stream<NI, G, S, MINB>,
+    MKB_CUDA(cudaFuncSetAttribute(k_mttkrp_stream<NI, G, S, MINB, B, PD>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(smem)));
     MKB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-        &per_sm, k_mttkrp_stream<NI, G, S, MINB>, 256, smem));
+        &per_sm, k_mttkrp_stream<NI, G, S, MINB, B, PD>, 256, smem));
     if (per_sm < 1) per_sm = 1;
   }
   const unsigned grid = static_cast<unsigned>(
       std::max<uint64_t>(1, std::min<uint64_t>(ntiles, static_cast<uint64_t>(c.num_sms) * per_sm)));
-  k_mttkrp_stream<NI, G, S, MINB><<<grid, 256, smem, st>>>(a);
+  k_mttkrp_stream<NI, G, S, MINB, B, PD><<<grid, 256, smem, st>>>(a);
   MKB_LAUNCH();
 }
 
-int stream_minb() {
+int stream_variant() {
   static int v = [] {
-    const char* e = std::getenv("MKB_STREAM_MINB");
-    return e && std::atoi(e) == 4 ? 4 : 3;
+    const char* e = std::getenv("MKB_STREAM_VARIANT");
+    return e ? std::atoi(e) : 0;
   }();
   return v;
 }
@@ -386,10 +411,12 @@ void launch_stream_cfg(Context& c, ModeCopy& mc, uint32_t mode, const float* con
   a.e0 = e0;
   a.e1 = e1;
   const uint32_t ntiles = (e1 - e0a + TILE - 1) / TILE;
-  if (stream_minb() == 4)
-    launch_stream_kernel<NI, G, S, 4>(c, a, ntiles, st);
-  else
-    launch_stream_kernel<NI, G, S, 3>(c, a, ntiles, st);
+  switch (stream_variant()) {
+    // measured on B200 (profiles/README.md): B=2 at 3 CTAs/SM is the best of
+    // {B=1,2,4} x {2,3,4 CTAs/SM}; L1 software prefetch (PD>0) lost 2.5x and is off.
+    case 1: launch_stream_kernel<NI, G, S, 4, 1, 0>(c, a, ntiles, st); break;
+    default: launch_stream_kernel<NI, G, S, 3, 2, 0>(c, a, ntiles, st); break;
+  }
 }
 
 template <int NI>

@@ -2,7 +2,7 @@
 # usage: tools/bench_configs.sh "cfg2 cfg1 ..." [tag]   (run on the GPU box, repo root)
 cfgs=${1:-"cfg2 cfg1 cfg3 cfg4"}; tag=${2:-run}
 for c in $cfgs; do
-  timeout 600 python bench.py --config $c --steps 20 --warmup 5 > gpurun_out/bench_${tag}_$c.json 2> gpurun_out/bench_${tag}_$c.err
+  timeout 600 python bench.py --config $c --steps 20 --warmup 5 $BENCH_FLAGS > gpurun_out/bench_${tag}_$c.json 2> gpurun_out/bench_${tag}_$c.err
   python - "$c" "gpurun_out/bench_${tag}_$c.json" <<'PY' || tail -3 gpurun_out/bench_${tag}_$c.err
 import json, sys
 d = json.load(open(sys.argv[2]))
