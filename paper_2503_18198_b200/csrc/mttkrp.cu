@@ -250,26 +250,40 @@ __global__ void __launch_bounds__(256) k_mttkrp_rows(const MttkrpArgs a) {
       for (int i = 0; i < NI; ++i) my_c[i] = vl ? __ldg(a.in_idx[i] + jl) : 0u;
       const float my_v = vl ? __ldg(a.val + jl) : 0.0f;
       const int cnt = static_cast<int>(e - base < G ? e - base : G);
-      for (int kk = 0; kk < cnt; ++kk) {
-        const float v = __shfl_sync(gmask, my_v, gbase + kk);
-        float t[F];
+      // terms of a batch of SB elements are gathered and multiplied independently (loads in
+      // flight together); only the additions are sequential, in element order
+      constexpr int SB = G < 8 ? G : (F <= 4 ? 8 : (F <= 8 ? 4 : 2));
 #pragma unroll
-        for (int q = 0; q < F; ++q) t[q] = v;
+      for (int sb = 0; sb < G; sb += SB) {
+        if (sb >= cnt) break;
+        float t[SB][F];
 #pragma unroll
-        for (int i = 0; i < NI; ++i) {
-          const uint32_t c = __shfl_sync(gmask, my_c[i], gbase + kk);
-          float y[F];
-          load_row<VEC, G, KREP>(a.in_Y[i], c, a.rank, lane_g, y);
+        for (int k2 = 0; k2 < SB; ++k2) {
+          const int kk = sb + k2 < cnt ? sb + k2 : cnt - 1;
+          const float v = __shfl_sync(gmask, my_v, gbase + kk);
 #pragma unroll
-          for (int q = 0; q < F; ++q) t[q] = __fmul_rn(t[q], y[q]);
+          for (int q = 0; q < F; ++q) t[k2][q] = v;
+#pragma unroll
+          for (int i = 0; i < NI; ++i) {
+            const uint32_t c = __shfl_sync(gmask, my_c[i], gbase + kk);
+            float y[F];
+            load_row<VEC, G, KREP>(a.in_Y[i], c, a.rank, lane_g, y);
+#pragma unroll
+            for (int q = 0; q < F; ++q) t[k2][q] = __fmul_rn(t[k2][q], y[q]);
+          }
         }
-        bool bad = false;
 #pragma unroll
-        for (int q = 0; q < F; ++q) {
-          bad |= !isfinite(t[q]);
-          acc[q] = __fadd_rn(acc[q], t[q]);
+        for (int k2 = 0; k2 < SB; ++k2) {
+          if (sb + k2 < cnt) {
+            bool bad = false;
+#pragma unroll
+            for (int q = 0; q < F; ++q) {
+              bad |= !isfinite(t[k2][q]);
+              acc[q] = __fadd_rn(acc[q], t[k2][q]);
+            }
+            if (bad && first_bad == ~0ull) first_bad = base + sb + k2;
+          }
         }
-        if (bad && first_bad == ~0ull) first_bad = base + kk;
       }
     }
     if (first_bad != ~0ull) atomicMin(a.nonfinite, a.tag | first_bad);

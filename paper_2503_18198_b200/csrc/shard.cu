@@ -16,14 +16,30 @@ namespace {
 
 __global__ void k_segment_split_rows(const uint32_t* __restrict__ cd, uint64_t e0a, uint64_t e0,
                                      uint64_t e1, uint32_t seg, uint32_t tile, uint64_t nseg,
-                                     uint32_t* out) {
+                                     uint32_t* out, uint32_t* flags) {
   const uint64_t s = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
   if (s >= nseg) return;
   const uint32_t per = tile / seg;
   const uint64_t p = e0a + (s / per) * tile + (s % per) * seg;
-  uint32_t row = 0xffffffffu;
-  if (p > e0 && p < e1 && cd[p - 1] == cd[p]) row = cd[p];
+  uint32_t row = 0xffffffffu, flag = 0;
+  // a row continuing across segment start p must be zeroed — once: only at its first split
+  // point (segment starts are exactly seg apart, tiles are contiguous).  The previous
+  // segment start q = p - seg was an earlier split point of the same row iff the row also
+  // continued across q.
+  if (p > e0 && p < e1 && cd[p - 1] == cd[p]) {
+    row = cd[p];
+    const bool earlier = p >= e0 + seg + 1 && cd[p - seg] == row && cd[p - seg - 1] == row;
+    flag = earlier ? 0u : 1u;
+  }
   out[s] = row;
+  flags[s] = flag;
+}
+
+__global__ void k_compact_rows(const uint32_t* __restrict__ rows, const uint32_t* __restrict__ flags,
+                               const uint32_t* __restrict__ pos, uint64_t n,
+                               uint32_t* __restrict__ dst) {
+  const uint64_t s = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+  if (s < n && flags[s]) dst[pos[s]] = rows[s];
 }
 
 // out[i - k0] (row-major R) = src[row_seq[i]] for copy rows i in [k0, k1)
@@ -66,12 +82,24 @@ void ensure_zero_list(Context& c, uint32_t mode, ModeCopy::ZeroList& zl, uint32_
   if (nempty)
     MKB_CUDA(cudaMemcpyAsync(zl.rows.get(), mc.row_seq.get() + mc.distinct,
                              nempty * sizeof(uint32_t), cudaMemcpyDeviceToDevice, st));
+  uint64_t nsplit = 0;
   if (nseg) {
+    // candidate rows + first-occurrence flags, then stream compaction (scan + scatter)
+    DevBuf<uint32_t> rows(nseg), flags(nseg + 1), pos(nseg + 1);
     k_segment_split_rows<<<ceil_div(nseg, 256), 256, 0, st>>>(
-        mc.idx[mode].get(), e0a, e0, e1, seg, tile, nseg, zl.rows.get() + nempty);
+        mc.idx[mode].get(), e0a, e0, e1, seg, tile, nseg, rows.get(), flags.get());
     MKB_LAUNCH();
+    MKB_CUDA(cudaMemsetAsync(flags.get() + nseg, 0, sizeof(uint32_t), st));
+    exclusive_scan_u32(flags.get(), pos.get(), nseg + 1, c.scratch, st);
+    k_compact_rows<<<ceil_div(nseg, 256), 256, 0, st>>>(rows.get(), flags.get(), pos.get(), nseg,
+                                                       zl.rows.get() + nempty);
+    MKB_LAUNCH();
+    uint32_t total = 0;
+    MKB_CUDA(cudaMemcpyAsync(&total, pos.get() + nseg, sizeof total, cudaMemcpyDeviceToHost, st));
+    MKB_CUDA(cudaStreamSynchronize(st));
+    nsplit = total;
   }
-  zl.n = nempty + nseg;
+  zl.n = nempty + nsplit;
   zl.key_seg = seg;
   zl.key_tile = tile;
   zl.key_e0 = e0;
