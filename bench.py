@@ -134,7 +134,8 @@ def ncu_traffic(config_name):
     path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     try:
         with open(path) as fh:
-            return json.load(fh).get(config_name)
+            entry = json.load(fh).get(config_name)
+        return float(entry["dram_bytes_per_sweep"]) if entry else None
     except Exception:
         return None
 
@@ -248,25 +249,41 @@ def our_arm(args, cfg, rank, world, local_rank):
     bytes_mode = algorithmic_bytes(dims, t.nnz, R, distinct)
     b_iter = float(sum(bytes_mode))
 
+    # N > 1: row-range shards per mode + NCCL all-gather of each mode's rows
+    ex = None
+    if world > 1:
+        from paper_2503_18198_b200.distributed import ShardExchange
+        ex = ShardExchange(ctx, R, dims, device=dev)
+
     def sweep_timed(n_steps, flush, record):
         ev = [[torch.cuda.Event(enable_timing=True) for _ in range(n + 1)] for _ in range(n_steps)]
+        evk = [[torch.cuda.Event(enable_timing=True) for _ in range(n)] for _ in range(n_steps)]
         for s in range(n_steps):
             if flush:
                 ctx.flush_l2()
             ev[s][0].record(stream)
             for d in range(n):
                 ctx.mttkrp_mode_async(d, False)
+                evk[s][d].record(stream)
+                if ex is not None:
+                    ex.gather_mode(d)
                 ev[s][d + 1].record(stream)
-        return ev
+        return ev, evk
+
+    def sweep_once():
+        if ex is not None:
+            ex.sweep()
+        else:
+            ctx.sweep_async(False, False)
 
     for _ in range(max(args.warmup, 3)):
-        ctx.sweep_async(False, False)
+        sweep_once()
     ctx.synchronize()
     if args.profile:
         # short, L2-flushed sweeps for ncu (never a bench number)
         for _ in range(args.steps):
             ctx.flush_l2()
-            ctx.sweep_async(False, False)
+            sweep_once()
         ctx.synchronize()
         log(f"profile run done: {args.steps} sweeps of {n} modes")
         return 0
@@ -277,13 +294,13 @@ def our_arm(args, cfg, rank, world, local_rank):
     torch.cuda.synchronize()
     with ClockSampler(local_rank) as clk:
         w0 = time.perf_counter()
-        ev = sweep_timed(args.steps, True, True)
+        ev, evk = sweep_timed(args.steps, True, True)
         torch.cuda.synchronize()
         wall = (time.perf_counter() - w0) * 1e3
     ctx.synchronize()  # non-finite check
     step_ms = [ev[s][0].elapsed_time(ev[s][n]) for s in range(args.steps)]
-    mode_ms = np.array([[ev[s][d].elapsed_time(ev[s][d + 1]) for d in range(n)]
-                        for s in range(args.steps)])
+    mode_ms = np.array([[ev[s][d].elapsed_time(evk[s][d]) for d in range(n)]
+                        for s in range(args.steps)])  # spMTTKRP kernels only
     ms = float(np.mean(step_ms))
     if world > 1:
         import torch.distributed as dist
@@ -292,7 +309,7 @@ def our_arm(args, cfg, rank, world, local_rank):
         ms = float(tt.item())
 
     # warm (no flush) for reference
-    evw = sweep_timed(args.steps, False, True)
+    evw, _ = sweep_timed(args.steps, False, True)
     torch.cuda.synchronize()
     warm_ms = float(np.mean([evw[s][0].elapsed_time(evw[s][n]) for s in range(args.steps)]))
 
@@ -301,14 +318,23 @@ def our_arm(args, cfg, rank, world, local_rank):
     pin_o = [torch.empty((d, R), dtype=torch.float32).pin_memory() for d in dims]
     f_np = [p.numpy() for p in pin_f]
     o_np = [p.numpy() for p in pin_o]
+    def e2e_step():
+        if ex is None:
+            ctx.sweep_host(f_np, o_np)
+        else:  # H2D factors, sharded sweep + all-gathers, D2H outputs
+            ctx.upload_factors(f_np)
+            ex.sweep()
+            for d in range(n):
+                o_np[d][...] = ctx.output(d)
+
     for _ in range(2):
-        ctx.sweep_host(f_np, o_np)
+        e2e_step()
     e2e = []
     for s in range(args.steps):
         ctx.flush_l2()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record(stream)
-        ctx.sweep_host(f_np, o_np)
+        e2e_step()
         b.record(stream)
         b.synchronize()
         e2e.append(a.elapsed_time(b))
@@ -319,12 +345,13 @@ def our_arm(args, cfg, rank, world, local_rank):
     als_ms = None
     if R <= 64:
         ctx.upload_factors(factors)
-        ctx.cpd_als_iter()
+        als_iter = ex.cpd_als_iter if ex is not None else ctx.cpd_als_iter
+        als_iter()
         torch.cuda.synchronize()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record(stream)
         for _ in range(3):
-            ctx.cpd_als_iter()
+            als_iter()
         b.record(stream)
         b.synchronize()
         als_ms = a.elapsed_time(b) / 3
@@ -352,7 +379,8 @@ def our_arm(args, cfg, rank, world, local_rank):
                      "kernel": "k_mttkrp_tiles (all modes)", "kernel_ms_per_sweep": kern_ms},
         "e2e": {"value": e2e_ms, "unit": "ms", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": h2d, "path": "mk_sweep_host (C ABI), pinned host buffers"},
-        "gpu_launches": launches_per_mode * n * args.steps,
+        "gpu_launches": (launches_per_mode + (2 if ex is not None else 0)) * n * args.steps,
+        "allgather_bytes_per_sweep": ex.bytes_per_sweep() if ex is not None else 0,
         "clocks": clk.summary(),
         "per_mode_ms": mode_ms.mean(axis=0).tolist(),
         "warm_ms_per_step": warm_ms,
