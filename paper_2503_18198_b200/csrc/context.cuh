@@ -45,6 +45,9 @@ struct ModeCopy {
   // part B 0/4/8/16 B/element; padded to a multiple of 4 elements
   DevBuf<uint32_t> recA, recB;
   DevBuf<uint32_t> kperm;  // kernel (fiber) order -> reference copy position
+  uint32_t fiber_mode = kMaxModes;  // input mode accumulated per fiber (== n: off)
+  uint32_t rec_modes[kMaxModes] = {};  // record word q -> input mode (extent descending)
+  uint64_t fibers = 0;              // (row, c_fiber) runs in kernel order
   // pre-zero row lists (empty rows + rows split by the kernel's segmentation), cached per
   // (kernel, segment length, shard range)
   struct ZeroList {

@@ -37,18 +37,43 @@ __global__ void k_gather_rank_keys(const uint32_t* __restrict__ cd,
     keys[i] = rank_of_row[cd[perm[i]]];
 }
 
+// Fibers in kernel order: maximal runs of equal (row, c_f).
+__global__ void k_count_fibers(const uint32_t* __restrict__ cd, const uint32_t* __restrict__ cf,
+                               const uint32_t* __restrict__ perm, uint64_t n,
+                               unsigned long long* count) {
+  unsigned long long local = 0;
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint32_t s = perm[i];
+    if (i == 0) {
+      ++local;
+    } else {
+      const uint32_t q = perm[i - 1];
+      local += (cd[s] != cd[q] || cf[s] != cf[q]) ? 1 : 0;
+    }
+  }
+  for (int o = 16; o; o >>= 1) local += __shfl_xor_sync(0xffffffffu, local, o);
+  if ((threadIdx.x & 31) == 0 && local) atomicAdd(count, local);
+}
+
+struct WordModes {
+  uint32_t m[kMaxModes];
+};
+
+// Record words: input coordinates in `order` (extent descending: word 0 is the largest
+// input = the fiber mode; the trailing words are the smallest inputs, which the kernel may
+// stage in shared memory), value bits, c_d.
 __global__ void k_pack_records(const uint32_t* const* idx, const float* __restrict__ val,
                                const uint32_t* __restrict__ perm, uint32_t n, uint32_t mode,
-                               uint64_t nnz, uint64_t padded, uint32_t bw, uint4* recA,
-                               uint32_t* recB) {
+                               WordModes order, uint64_t nnz, uint64_t padded, uint32_t bw,
+                               uint4* recA, uint32_t* recB) {
   for (uint64_t j = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; j < padded;
        j += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
     uint32_t w[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     if (j < nnz) {
       const uint32_t s = perm[j];
       uint32_t k = 0;
-      for (uint32_t m = 0; m < n; ++m)
-        if (m != mode) w[k++] = idx[m][s];
+      for (uint32_t q = 0; q + 1 < n; ++q) w[k++] = idx[order.m[q]][s];
       w[k++] = __float_as_uint(val[s]);
       w[k++] = idx[mode][s];
     }
@@ -90,6 +115,23 @@ void pack_records(Context& c, uint32_t mode, const uint32_t* rank_of_row) {
   radix_sort_pairs(keys.get(), mc.kperm.get(), nnz, bits_for(mc.distinct ? mc.distinct - 1 : 0),
                    c.scratch, st);
 
+  // Two-level (CSF-style) accumulation pays when fibers of the largest input mode are long:
+  // out[i] = Σ_fibers Y_f[c_f] ⊙ Σ_{elements} val · Π_{other inputs} — one gather of Y_f per
+  // fiber instead of per element.  Enabled when the mean fiber length is >= 2.
+  mc.fiber_mode = c.n;  // none
+  {
+    DevBuf<unsigned long long> cnt(1);
+    MKB_CUDA(cudaMemsetAsync(cnt.get(), 0, sizeof(unsigned long long), st));
+    k_count_fibers<<<gblocks, 256, 0, st>>>(mc.idx[mode].get(), mc.idx[inputs[0]].get(),
+                                            mc.kperm.get(), nnz, cnt.get());
+    MKB_LAUNCH();
+    unsigned long long nf = 0;
+    MKB_CUDA(cudaMemcpyAsync(&nf, cnt.get(), sizeof nf, cudaMemcpyDeviceToHost, st));
+    MKB_CUDA(cudaStreamSynchronize(st));
+    mc.fibers = nf;
+    if (nf && nnz >= 2 * nf) mc.fiber_mode = inputs[0];
+  }
+
   const uint32_t words = c.n + 1;  // (n-1) inputs + value + c_d
   const uint32_t bw = words <= 4 ? 0 : (words - 4 <= 2 ? words - 4 : 4);
   const uint64_t padded = (nnz + 3) & ~3ull;
@@ -101,9 +143,14 @@ void pack_records(Context& c, uint32_t mode, const uint32_t* rank_of_row) {
   MKB_CUDA(cudaMemcpyAsync(ptrs.get(), hp, c.n * sizeof(uint32_t*), cudaMemcpyHostToDevice, st));
   const unsigned blocks =
       static_cast<unsigned>(std::min<uint64_t>((padded + 255) / 256, c.num_sms * 16ull));
-  k_pack_records<<<blocks, 256, 0, st>>>(ptrs.get(), mc.val.get(), mc.kperm.get(), c.n, mode, nnz,
-                                         padded, bw, reinterpret_cast<uint4*>(mc.recA.get()),
-                                         mc.recB.get());
+  WordModes order{};
+  for (uint32_t q = 0; q < inputs.size(); ++q) {
+    order.m[q] = inputs[q];
+    mc.rec_modes[q] = inputs[q];
+  }
+  k_pack_records<<<blocks, 256, 0, st>>>(ptrs.get(), mc.val.get(), mc.kperm.get(), c.n, mode,
+                                         order, nnz, padded, bw,
+                                         reinterpret_cast<uint4*>(mc.recA.get()), mc.recB.get());
   MKB_LAUNCH();
   MKB_CUDA(cudaStreamSynchronize(st));  // ptrs / keys are freed on return
 }

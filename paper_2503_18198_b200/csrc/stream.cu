@@ -3,7 +3,7 @@
 // detail::mttkrp_mode_impl, kernel.hpp:75-127, and Algorithm 2).
 //
 // Data path per mode copy (records.cu): element records in fiber order,
-//   part A  16 B : words 0..3 of {c_w (input modes ascending), value bits, c_d}
+//   part A  16 B : words 0..3 of {input coords, value bits, c_d}
 //   part B  4/8/16 B : the remaining words (none when N = 3)
 // so an element's whole record is one LDS.128 (+ one small LDS) instead of N+1 shuffles.
 //
@@ -12,21 +12,27 @@
 // into a 2-stage ring guarded by mbarriers, so the stream never occupies LSU issue slots.
 // Inside a tile each lane group (G = R/4 lanes, 128-bit per lane) owns S consecutive
 // elements (S odd: the groups of a warp read their records from different bank quads).
-// Per element a group gathers the N-1 input factor rows with 128-bit L1-cached loads —
-// issued in batches of B elements before any is consumed (fiber order keeps the large
-// factors in a narrow, L1-resident window) — multiplies with packed FMUL2, and
-// accumulates the output row in registers while
-// c_d is unchanged.  A run that starts and ends inside the group's S elements is owned and
-// stored with a plain 128-bit store (Local_Update); runs crossing an S boundary are added
-// with a vector atomic (Global_Update), combined across the warp first when all its groups
-// end in the same row.  Rows receiving atomics are pre-zeroed from the cached split-row list.
+// Per batch of B elements a group issues all the input-row gathers (128-bit, L1-cached;
+// fiber order keeps the large factors in a narrow L1-resident window) before consuming
+// any, multiplies with packed FMUL2 and accumulates the output row in registers while c_d
+// is unchanged.
+//
+// FIB (two-level / CSF-style accumulation, chosen per mode copy when fibers are long):
+// inside a row, elements sharing the coordinate c_f of the fiber mode f are summed first,
+//   out[i] += Y_f[c_f] ⊙ Σ_fiber val · Π_{w ∉ {d,f}} Y_w[c_w],
+// so Y_f is gathered and multiplied once per fiber instead of once per element.
+//
+// Writes: a run that starts and ends inside the group's S elements is owned and stored with
+// a plain 128-bit store (Local_Update); runs crossing an S boundary are added with a vector
+// atomic (Global_Update), combined across the warp first when all its groups end in the
+// same row.  Rows receiving atomics are pre-zeroed once from the cached split-row list.
 // Non-finite products (kernel.hpp:109-114): row sums are checked at flush; the rare path
-// rescans the run and reports the reference copy position through kperm.
+// rescans the run in the reference's multiplication order and reports the reference copy
+// position through kperm.
 #include <algorithm>
 #include <cstdlib>
 
 #include "context.cuh"
-
 
 namespace mkb {
 namespace {
@@ -65,14 +71,18 @@ struct StreamArgs {
   const uint32_t* recB;     // nnz (padded) x BW words, BW = 0/1/2/4
   const uint32_t* out_idx;  // copy-order c_d (head/tail split tests)
   const uint32_t* kperm;    // kernel position -> reference copy position
-  const float* in_Y[kMaxModes];
+  const float* in_Y[kMaxModes];  // factors in record-word order
   float* out;
   unsigned long long* nonfinite;
   unsigned long long tag;
-  uint32_t nnz;  // total elements of the copy
-  uint32_t e0a;  // tile origin: e0 rounded down to 4 elements (TMA 16-byte alignment)
-  uint32_t e0;   // owned element range [e0, e1) (whole copy unless sharded)
+  uint32_t nnz;   // total elements of the copy
+  uint32_t e0a;   // tile origin: e0 rounded down to 4 elements (TMA 16-byte alignment)
+  uint32_t e0;    // owned element range [e0, e1) (whole copy unless sharded)
   uint32_t e1;
+  uint32_t asc_word;  // nibble p = record word of the p-th input in ascending mode order
+  uint32_t stage_off[4];  // SMEM byte offset of staged record word q (trailing K words)
+  uint32_t stage_bytes[4];
+  uint32_t records_off;   // SMEM byte offset of the record ring (after staged factors)
 };
 
 template <int NI>
@@ -110,24 +120,25 @@ __device__ __forceinline__ void read_record(const uint4* sA, const uint32_t* sB,
   for (int q = 0; q < NI + 2; ++q) w[q] = t[q];
 }
 
-// Cold path: recompute the run's terms and report every offending element's REFERENCE copy
+// Cold path: recompute the run's terms in the reference's order (val, then inputs by
+// ascending mode, kernel.hpp:102-107) and report every offending element's REFERENCE copy
 // position, so the launch minimum equals the reference's first failing position.
 template <int NI, int G>
 __device__ __noinline__ void stream_rescan(const uint4* recA, const uint32_t* recB,
                                            const float* Y0, const float* Y1, const float* Y2,
-                                           const float* Y3, int lane_g, uint32_t s, uint32_t e,
-                                           const uint32_t* kperm, unsigned long long* nf,
-                                           unsigned long long tag) {
+                                           const float* Y3, uint32_t asc_word, int lane_g,
+                                           uint32_t s, uint32_t e, const uint32_t* kperm,
+                                           unsigned long long* nf, unsigned long long tag) {
   const float* Y[4] = {Y0, Y1, Y2, Y3};
   for (uint32_t j = s; j < e; ++j) {
     uint32_t w[NI + 2];
     read_record<NI>(recA, recB, j, w);
     const float v = __uint_as_float(w[Layout<NI>::VAL]);
     float t[4] = {v, v, v, v};
-#pragma unroll
-    for (int i = 0; i < NI; ++i) {
+    for (uint32_t p = 0; p < static_cast<uint32_t>(NI); ++p) {
+      const uint32_t q = (asc_word >> (4 * p)) & 15u;  // record word of ascending input p
       const float4 y =
-          __ldg(reinterpret_cast<const float4*>(Y[i]) + static_cast<size_t>(w[i]) * G + lane_g);
+          __ldg(reinterpret_cast<const float4*>(Y[q]) + static_cast<size_t>(w[q]) * G + lane_g);
       t[0] = __fmul_rn(t[0], y.x);
       t[1] = __fmul_rn(t[1], y.y);
       t[2] = __fmul_rn(t[2], y.z);
@@ -136,6 +147,21 @@ __device__ __noinline__ void stream_rescan(const uint4* recA, const uint32_t* re
     if (!isfinite(t[0]) || !isfinite(t[1]) || !isfinite(t[2]) || !isfinite(t[3]))
       atomicMin(nf, tag | static_cast<unsigned long long>(kperm[j]));
   }
+}
+
+// Row gather of record word i: LDS.128 when that factor is staged in shared memory,
+// otherwise an L1-cached LDG.128.
+template <int NI, int K, int G>
+__device__ __forceinline__ float4 gather_row(const float4* base, int i, uint32_t c) {
+  const float4* p = base + static_cast<size_t>(c) * G;
+  if (i >= NI - K) {
+    float4 v;
+    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+                 : "r"(smem_u32(p)));
+    return v;
+  }
+  return __ldg(p);
 }
 
 __device__ __forceinline__ void flush_row(float4* outv, uint32_t row, float2 a0, float2 a1,
@@ -148,19 +174,24 @@ __device__ __forceinline__ void flush_row(float4* outv, uint32_t row, float2 a0,
     *p = v;
 }
 
-// MINB = minimum resident CTAs per SM the register budget is tuned for (3: <= 85 regs,
-// 4: <= 64 regs); B = elements per gather batch.  Variant picked at run time
-// (MKB_STREAM_VARIANT, stream_variant()).
-template <int NI, int G, int S, int MINB, int B, int PD>
-__global__ void __launch_bounds__(256, MINB) k_mttkrp_stream(const StreamArgs a) {
+// MINB = minimum resident CTAs per SM the register budget is tuned for; B = elements per
+// gather batch; FIB = two-level fiber accumulation (see header); K = number of trailing
+// record words (the smallest inputs) whose whole factor is staged in shared memory for the
+// CTA's lifetime (TMA bulk copy at start; gathers become LDS with no L1/L2 misses);
+// NT = threads per CTA.
+template <int NI, int G, int S, int MINB, int B, bool FIB, int K, int NT>
+__global__ void __launch_bounds__(NT, MINB) k_mttkrp_stream(const StreamArgs a) {
   constexpr int BW = Layout<NI>::BW;
   constexpr int VAL = Layout<NI>::VAL, CD = Layout<NI>::CD;
-  constexpr int GPB = 256 / G;
+  constexpr int GPB = NT / G;
   constexpr int TILE = GPB * S;
+  constexpr int I0 = FIB ? 1 : 0;  // first input gathered per element
   constexpr uint32_t BYTES_A = TILE * 16u;
   constexpr uint32_t BYTES_B = TILE * 4u * BW;
-  extern __shared__ __align__(128) uint8_t smem[];
-  // stage s: part A at smem + s*BYTES_A, part B at smem + 2*BYTES_A + s*BYTES_B
+  extern __shared__ __align__(128) uint8_t smem_raw[];
+  // [staged factors][record ring: stage s part A at rec + s*BYTES_A, part B at
+  //  rec + 2*BYTES_A + s*BYTES_B][mbarriers]
+  uint8_t* smem = smem_raw + a.records_off;
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + 2 * BYTES_A + 2 * BYTES_B);
 
   const int tid = threadIdx.x;
@@ -169,10 +200,33 @@ __global__ void __launch_bounds__(256, MINB) k_mttkrp_stream(const StreamArgs a)
   const uint32_t nnz = a.nnz, e0a = a.e0a, e0 = a.e0, e1 = a.e1;
   const uint32_t ntiles = (e1 - e0a + TILE - 1) / TILE;
 
-  // per-lane base pointers: row c of input i is Yv[i][c * G]
+  // per-lane base pointers: row c of input i is Yv[i][c * G] (global or staged in SMEM)
   const float4* Yv[NI];
 #pragma unroll
-  for (int i = 0; i < NI; ++i) Yv[i] = reinterpret_cast<const float4*>(a.in_Y[i]) + lane_g;
+  for (int i = 0; i < NI; ++i)
+    Yv[i] = (i >= NI - K ? reinterpret_cast<const float4*>(smem_raw + a.stage_off[i])
+                         : reinterpret_cast<const float4*>(a.in_Y[i])) +
+            lane_g;
+  if constexpr (K > 0) {
+    // stage the K smallest input factors once per CTA (TMA bulk copies)
+    if (tid == 0) {
+      mbar_init(&bar[2], 1);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+      uint32_t total = 0;
+#pragma unroll
+      for (int i = NI - K; i < NI; ++i) total += a.stage_bytes[i];
+      mbar_arrive_tx(&bar[2], total);
+#pragma unroll
+      for (int i = NI - K; i < NI; ++i) {
+        // bulk copies are limited to 2^20 - 16 bytes per instruction
+        for (uint32_t off = 0; off < a.stage_bytes[i]; off += 65536u) {
+          const uint32_t sz = a.stage_bytes[i] - off < 65536u ? a.stage_bytes[i] - off : 65536u;
+          tma_load_1d(smem_raw + a.stage_off[i] + off,
+                      reinterpret_cast<const uint8_t*>(a.in_Y[i]) + off, sz, &bar[2]);
+        }
+      }
+    }
+  }
   float4* outv = reinterpret_cast<float4*>(a.out) + lane_g;
   const uint4* gA = a.recA;
   const uint32_t* gB = a.recB;
@@ -200,6 +254,7 @@ __global__ void __launch_bounds__(256, MINB) k_mttkrp_stream(const StreamArgs a)
     if (blockIdx.x < ntiles) issue(blockIdx.x, 0);
     if (blockIdx.x + gridDim.x < ntiles) issue(blockIdx.x + gridDim.x, 1);
   }
+  if constexpr (K > 0) mbar_wait(&bar[2], 0);  // staged factors resident
 
   uint32_t it = 0;
   for (uint32_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
@@ -220,46 +275,23 @@ __global__ void __launch_bounds__(256, MINB) k_mttkrp_stream(const StreamArgs a)
       const bool head_split = p0 > 0 && __ldg(gcd + p0 - 1) == __ldg(gcd + p0);
       const bool tail_split = p1 < nnz && __ldg(gcd + p1) == __ldg(gcd + p1 - 1);
       const uint32_t n = p1 - p0;
+      uint32_t fc = 0;              // FIB: current fiber coordinate
+      float4 yf = make_float4(0.f, 0.f, 0.f, 0.f);  // FIB: its factor row
+      float2 f0 = acc0, f1 = acc0;  // FIB: fiber accumulator
       {
         uint32_t w0[NI + 2];
         read_record<NI>(ra, rb, 0, w0);
         cur = w0[CD];
+        if constexpr (FIB) {
+          fc = w0[0];
+          yf = gather_row<NI, K, G>(Yv[0], 0, fc);
+        }
       }
       uint32_t run_start = p0;
       bool first = true;
-      // Batches of B elements: all B records are read and all B*(N-1) gathers issued before
-      // any of them is consumed (memory-level parallelism without a rotating pipeline).
-      if constexpr (PD > 0) {
-        // prologue of the L1 prefetch stream (elements [0, PD))
-#pragma unroll
-        for (int kp = 0; kp < PD; ++kp) {
-          if (static_cast<uint32_t>(kp) < n) {
-            uint32_t wp[NI + 2];
-            read_record<NI>(ra, rb, kp, wp);
-#pragma unroll
-            for (int i = 0; i < NI; ++i)
-              asm volatile("prefetch.global.L1 [%0];" ::"l"(Yv[i] +
-                                                            static_cast<size_t>(wp[i]) * G));
-          }
-        }
-      }
+      // Batches of B elements: all B records are read and all B*(N-1-FIB) gathers issued
+      // before any of them is consumed (memory-level parallelism without a rotating pipeline).
       for (uint32_t k = 0; k < n; k += B) {
-        if constexpr (PD > 0) {
-          // rows PD elements ahead are pulled into L1 without holding registers, so the
-          // real gathers below mostly hit L1 (latency hiding beyond the register budget)
-#pragma unroll
-          for (int b = 0; b < B; ++b) {
-            const uint32_t kp = k + PD + b;
-            if (kp < n) {
-              uint32_t wp[NI + 2];
-              read_record<NI>(ra, rb, kp, wp);
-#pragma unroll
-              for (int i = 0; i < NI; ++i)
-                asm volatile("prefetch.global.L1 [%0];" ::"l"(Yv[i] +
-                                                              static_cast<size_t>(wp[i]) * G));
-            }
-          }
-        }
         uint32_t w[B][NI + 2];
         float4 y[B][NI];
 #pragma unroll
@@ -270,23 +302,35 @@ __global__ void __launch_bounds__(256, MINB) k_mttkrp_stream(const StreamArgs a)
 #pragma unroll
         for (int b = 0; b < B; ++b)
 #pragma unroll
-          for (int i = 0; i < NI; ++i) y[b][i] = __ldg(Yv[i] + static_cast<size_t>(w[b][i]) * G);
+          for (int i = I0; i < NI; ++i) y[b][i] = gather_row<NI, K, G>(Yv[i], i, w[b][i]);
 #pragma unroll
         for (int b = 0; b < B; ++b) {
           if (B > 1 && k + b >= n) break;
           const float v = __uint_as_float(w[b][VAL]);
           float2 t0 = make_float2(v, v), t1 = t0;
 #pragma unroll
-          for (int i = 0; i < NI; ++i) {
+          for (int i = I0; i < NI; ++i) {
             t0 = __fmul2_rn(t0, make_float2(y[b][i].x, y[b][i].y));
             t1 = __fmul2_rn(t1, make_float2(y[b][i].z, y[b][i].w));
           }
           const uint32_t row = w[b][CD];
+          if constexpr (FIB) {
+            if (row != cur || w[b][0] != fc) {
+              // close the fiber into the row accumulator, open the next one
+              acc0 = __ffma2_rn(f0, make_float2(yf.x, yf.y), acc0);
+              acc1 = __ffma2_rn(f1, make_float2(yf.z, yf.w), acc1);
+              f0 = make_float2(0.f, 0.f);
+              f1 = f0;
+              fc = w[b][0];
+              yf = gather_row<NI, K, G>(Yv[0], 0, fc);
+            }
+          }
           if (row != cur) {
             if (!isfinite(acc0.x + acc0.y + acc1.x + acc1.y))
               stream_rescan<NI, G>(gA, gB, a.in_Y[0], NI > 1 ? a.in_Y[1] : nullptr,
                                    NI > 2 ? a.in_Y[2] : nullptr, NI > 3 ? a.in_Y[3] : nullptr,
-                                   lane_g, run_start, p0 + k + b, a.kperm, a.nonfinite, a.tag);
+                                   a.asc_word, lane_g, run_start, p0 + k + b, a.kperm, a.nonfinite,
+                                   a.tag);
             flush_row(outv, cur, acc0, acc1, first && head_split, G);
             first = false;
             cur = row;
@@ -294,14 +338,23 @@ __global__ void __launch_bounds__(256, MINB) k_mttkrp_stream(const StreamArgs a)
             acc0 = make_float2(0.f, 0.f);
             acc1 = acc0;
           }
-          acc0 = __fadd2_rn(acc0, t0);
-          acc1 = __fadd2_rn(acc1, t1);
+          if constexpr (FIB) {
+            f0 = __fadd2_rn(f0, t0);
+            f1 = __fadd2_rn(f1, t1);
+          } else {
+            acc0 = __fadd2_rn(acc0, t0);
+            acc1 = __fadd2_rn(acc1, t1);
+          }
         }
+      }
+      if constexpr (FIB) {
+        acc0 = __ffma2_rn(f0, make_float2(yf.x, yf.y), acc0);
+        acc1 = __ffma2_rn(f1, make_float2(yf.z, yf.w), acc1);
       }
       if (!isfinite(acc0.x + acc0.y + acc1.x + acc1.y))
         stream_rescan<NI, G>(gA, gB, a.in_Y[0], NI > 1 ? a.in_Y[1] : nullptr,
-                             NI > 2 ? a.in_Y[2] : nullptr, NI > 3 ? a.in_Y[3] : nullptr, lane_g,
-                             run_start, p1, a.kperm, a.nonfinite, a.tag);
+                             NI > 2 ? a.in_Y[2] : nullptr, NI > 3 ? a.in_Y[3] : nullptr, a.asc_word,
+                             lane_g, run_start, p1, a.kperm, a.nonfinite, a.tag);
       have = true;
       last_atomic = tail_split || (first && head_split);
     }
@@ -346,37 +399,64 @@ __global__ void k_stream_zero(float* __restrict__ out, const uint32_t* __restric
 }
 
 template <int NI, int G, int S>
-size_t smem_bytes() {
-  constexpr int TILE = (256 / G) * S;
-  return 2u * TILE * 16u + 2u * TILE * 4u * Layout<NI>::BW + 64;
+size_t record_ring_bytes(int nt) {
+  const int TILE = (nt / G) * S;
+  return 2u * TILE * 16u + 2u * TILE * 4u * Layout<NI>::BW + 64;  // + 3 mbarriers
 }
 
-template <int NI, int G, int S, int MINB, int B, int PD>
-void launch_stream_kernel(Context& c, const StreamArgs& a, uint32_t ntiles, cudaStream_t st) {
-  const size_t smem = smem_bytes<NI, G, S>();
+constexpr uint32_t kMaxDynSmem = 227u * 1024u;
+
+template <int NI, int G, int S, int MINB, int B, bool FIB, int K, int NT>
+void launch_stream_kernel(Context& c, const StreamArgs& a, uint32_t ntiles, size_t smem,
+                          cudaStream_t st) {
   // per-device launch setup, done once (keeps the per-launch host cost to the launch)
   static int per_sm_cache[64] = {};
   int& per_sm = per_sm_cache[c.device & 63];
   if (!per_sm) {
-    MKB_CUDA(cudaFuncSetAttribute(k_mttkrp_stream<NI, G, S, MINB, B, PD>,
+    MKB_CUDA(cudaFuncSetAttribute(k_mttkrp_stream<NI, G, S, MINB, B, FIB, K, NT>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  static_cast<int>(smem)));
+                                  static_cast<int>(kMaxDynSmem)));
     MKB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-        &per_sm, k_mttkrp_stream<NI, G, S, MINB, B, PD>, 256, smem));
+        &per_sm, k_mttkrp_stream<NI, G, S, MINB, B, FIB, K, NT>, NT,
+        K > 0 ? kMaxDynSmem : smem));
     if (per_sm < 1) per_sm = 1;
   }
   const unsigned grid = static_cast<unsigned>(
       std::max<uint64_t>(1, std::min<uint64_t>(ntiles, static_cast<uint64_t>(c.num_sms) * per_sm)));
-  k_mttkrp_stream<NI, G, S, MINB, B, PD><<<grid, 256, smem, st>>>(a);
+  k_mttkrp_stream<NI, G, S, MINB, B, FIB, K, NT><<<grid, NT, smem, st>>>(a);
   MKB_LAUNCH();
 }
 
-int stream_variant() {
+template <int NI, int G, int S, bool FIB>
+void launch_stream_staged(Context& c, const StreamArgs& a, uint32_t k, size_t smem,
+                          uint32_t e1, cudaStream_t st) {
+  constexpr int NT = 512;
+  constexpr int TILE = (NT / G) * S;
+  const uint32_t ntiles = (e1 - a.e0a + TILE - 1) / TILE;
+  if constexpr (NI >= 1)
+    if (k == 1) return launch_stream_kernel<NI, G, S, 1, 2, FIB, 1, NT>(c, a, ntiles, smem, st);
+  if constexpr (NI >= 2)
+    if (k == 2) return launch_stream_kernel<NI, G, S, 1, 2, FIB, 2, NT>(c, a, ntiles, smem, st);
+  if constexpr (NI >= 3)
+    if (k == 3) return launch_stream_kernel<NI, G, S, 1, 2, FIB, 3, NT>(c, a, ntiles, smem, st);
+  if constexpr (NI >= 4)
+    if (k == 4) return launch_stream_kernel<NI, G, S, 1, 2, FIB, 4, NT>(c, a, ntiles, smem, st);
+}
+
+int staging_enabled() {
   static int v = [] {
-    const char* e = std::getenv("MKB_STREAM_VARIANT");
-    return e ? std::atoi(e) : 0;
+    const char* e = std::getenv("MKB_STAGE");  // "0" disables shared-memory factor staging
+    return e && e[0] == '0' ? 0 : 1;
   }();
   return v;
+}
+
+bool fib_enabled() {
+  static int v = [] {
+    const char* e = std::getenv("MKB_FIBER");  // "0" disables the two-level accumulation
+    return e && e[0] == '0' ? 0 : 1;
+  }();
+  return v != 0;
 }
 
 template <int NI, int G, int S>
@@ -395,14 +475,40 @@ void launch_stream_cfg(Context& c, ModeCopy& mc, uint32_t mode, const float* con
     MKB_LAUNCH();
   }
   if (e1 <= e0) return;
+  // record words hold the inputs by extent descending (records.cu): word 0 is the fiber
+  // mode (two-level accumulation when its fibers are long), the trailing words the smallest
+  // factors, staged whole in shared memory when they fit next to the record ring
+  const bool fib = mc.fiber_mode < c.n && fib_enabled();
   StreamArgs a{};
   a.recA = reinterpret_cast<const uint4*>(mc.recA.get());
   a.recB = mc.recB.get();
   a.out_idx = mc.idx[mode].get();
   a.kperm = mc.kperm.get();
-  uint32_t ni = 0;
-  for (uint32_t w = 0; w < c.n; ++w)
-    if (w != mode) a.in_Y[ni++] = in[w];
+  for (uint32_t q = 0; q < static_cast<uint32_t>(NI); ++q) a.in_Y[q] = in[mc.rec_modes[q]];
+  a.asc_word = 0;
+  {
+    uint32_t p = 0;  // ascending mode order -> record word
+    for (uint32_t w = 0; w < c.n; ++w) {
+      if (w == mode) continue;
+      for (uint32_t q = 0; q < static_cast<uint32_t>(NI); ++q)
+        if (mc.rec_modes[q] == w) a.asc_word |= q << (4 * p);
+      ++p;
+    }
+  }
+  uint32_t kstage = 0;
+  size_t staged = 0;
+  const size_t ring512 = record_ring_bytes<NI, G, S>(512);
+  if (staging_enabled()) {
+    for (int q = NI - 1; q >= 0; --q) {
+      const size_t bytes = static_cast<size_t>(c.dims[mc.rec_modes[q]]) * c.rank * 4u;
+      const size_t off = (staged + 127) & ~size_t{127};
+      if (off + bytes + ring512 + 128 > kMaxDynSmem) break;
+      a.stage_off[q] = static_cast<uint32_t>(off);
+      a.stage_bytes[q] = static_cast<uint32_t>(bytes);
+      staged = off + bytes;
+      ++kstage;
+    }
+  }
   a.out = out;
   a.nonfinite = c.nonfinite.get();
   a.tag = static_cast<unsigned long long>(mode) << 32;
@@ -410,13 +516,25 @@ void launch_stream_cfg(Context& c, ModeCopy& mc, uint32_t mode, const float* con
   a.e0a = e0a;
   a.e0 = e0;
   a.e1 = e1;
-  const uint32_t ntiles = (e1 - e0a + TILE - 1) / TILE;
-  switch (stream_variant()) {
-    // measured on B200 (profiles/README.md): B=2 at 3 CTAs/SM is the best of
-    // {B=1,2,4} x {2,3,4 CTAs/SM}; L1 software prefetch (PD>0) lost 2.5x and is off.
-    case 1: launch_stream_kernel<NI, G, S, 4, 1, 0>(c, a, ntiles, st); break;
-    default: launch_stream_kernel<NI, G, S, 3, 2, 0>(c, a, ntiles, st); break;
+  if (kstage > 0) {
+    // one 512-thread CTA per SM holding the staged factors (up to 227 KB of SMEM)
+    a.records_off = static_cast<uint32_t>((staged + 127) & ~size_t{127});
+    const size_t smem = a.records_off + ring512;
+    if (fib)
+      launch_stream_staged<NI, G, S, true>(c, a, kstage, smem, e1, st);
+    else
+      launch_stream_staged<NI, G, S, false>(c, a, kstage, smem, e1, st);
+    return;
   }
+  // no factor fits: 256-thread CTAs, 3 per SM.  B=2 at 3 CTAs/SM measured best of
+  // {B=1,2,4} x {2,3,4 CTAs/SM}; an L1 software prefetch variant lost 2.5x.
+  a.records_off = 0;
+  const size_t smem = record_ring_bytes<NI, G, S>(256);
+  const uint32_t ntiles = (e1 - e0a + TILE - 1) / TILE;
+  if (fib)
+    launch_stream_kernel<NI, G, S, 3, 2, true, 0, 256>(c, a, ntiles, smem, st);
+  else
+    launch_stream_kernel<NI, G, S, 3, 2, false, 0, 256>(c, a, ntiles, smem, st);
 }
 
 template <int NI>
@@ -435,7 +553,6 @@ bool launch_stream_ni(Context& c, ModeCopy& mc, uint32_t mode, const float* cons
 bool launch_stream(Context& c, uint32_t mode, const float* const* in, float* out) {
   ModeCopy& mc = c.copies[mode];
   if (!mc.recA.get()) return false;
-  // 64-bit row offsets are used, but keep factors addressable by 32-bit rows per lane group
   switch (c.n) {
     case 3: return launch_stream_ni<2>(c, mc, mode, in, out);
     case 4: return launch_stream_ni<3>(c, mc, mode, in, out);
