@@ -56,6 +56,29 @@ struct ModeCopy {
     uint64_t key_seg = 0, key_tile = 0, key_e0 = ~0ull, key_e1 = ~0ull;
   };
   ZeroList zl_stream, zl_tiles;
+  // level-ordered, shared-memory-blocked records of the streaming kernel (stream2_plan.cu),
+  // built per (factor rank, shard range) on first use
+  struct Stream2 {
+    bool tried = false, ok = false;
+    uint32_t rank = 0;
+    uint64_t key_e0 = ~0ull, key_e1 = ~0ull;  // shard range the plan was built for
+    uint32_t ni = 0, nout = 0, k = 0, aw = 2;  // input levels, outer levels, staged levels
+    bool os = false;                           // outer factor staged in shared memory
+    uint32_t levels[kMaxModes] = {};           // level -> input mode (outermost first)
+    uint32_t rowbits = 0, b0 = 0, m0 = 0, m1 = 0;
+    uint32_t stage_off[4] = {};
+    uint32_t outer_off = 0, outer_bytes = 0;
+    size_t staged_end = 0;
+    bool blocked = false;
+    uint32_t nblocks = 1;
+    uint64_t outer_runs = 0;                   // distinct (row, level-0 coordinate) pairs
+    std::vector<uint32_t> blk_host;            // s2::Blk table (10 words per block)
+    DevBuf<uint32_t> blk_dev, recA, sk, kperm;
+    // work schedule for a grid size (s2::Item list + per-CTA offsets)
+    unsigned grid = 0;
+    DevBuf<uint32_t> items, cta_items;
+    ZeroList zl;
+  } s2;
   // multi-GPU row-range shard of this copy: copy rows [k0, k1) = elements [e0, e1)
   uint64_t shard_k0 = 0, shard_k1 = 0, shard_e0 = 0, shard_e1 = 0;
   std::vector<uint64_t> shard_cuts;  // world+1 copy-row cut points (all ranks)
@@ -133,6 +156,12 @@ void als_fit(Context& c, double* fit, float* lambda_host);
 // Streaming TMA kernel (stream.cu); false when the shape has no specialisation.
 bool launch_stream(Context& c, uint32_t mode, const float* const* in, float* out);
 void pack_records(Context& c, uint32_t mode, const uint32_t* rank_of_row);
+// v2 level-ordered streaming kernel (stream2_plan.cu): records built per factor rank on first
+// use (or eagerly by prepare_stream2); false when the shape has no specialisation.
+bool prepare_stream2(Context& c, uint32_t mode);
+bool launch_stream2(Context& c, uint32_t mode, const float* const* in, float* out);
+// rank_of_row[row_seq[k]] = k for the copy's non-empty rows
+void rank_of_row_build(Context& c, uint32_t mode, DevBuf<uint32_t>& rank);
 void check_nonfinite(Context& c);  // synchronises; throws MK_ENONFINITE
 
 }  // namespace mkb

@@ -437,8 +437,8 @@ void build_plans(Context& c, uint64_t kappa, int strategy, int policy) {
                                                               c.values.get(), mc.val.get());
       MKB_LAUNCH();
     }
-    // 5b. packed records for the streaming kernel
-    pack_records(c, d, rank_of_row.get());
+    // 5b. the streaming kernels' packed records are built on first use, once the factor
+    //     rank is known (stream2_plan.cu, records.cu)
     // zero-row list: empty rows (row_seq[nv:ext]) + rows split at fast-kernel tile starts
     mc.tile = choose_tile(nnz, c.num_sms);
     const uint32_t ntiles = nnz ? ceil_div(nnz, mc.tile) : 0;

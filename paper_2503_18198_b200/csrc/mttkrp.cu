@@ -361,7 +361,8 @@ void reset_nonfinite(Context& c) {
 }
 
 void launch_mttkrp(Context& c, uint32_t mode, const float* const* in, float* out, int exec) {
-  if (exec == MK_EXEC_FAST && launch_stream(c, mode, in, out)) return;
+  if (exec == MK_EXEC_FAST && (launch_stream2(c, mode, in, out) || launch_stream(c, mode, in, out)))
+    return;
   ModeCopy& mc = c.copies[mode];
   MttkrpArgs a{};
   uint32_t ni = 0;
