@@ -72,12 +72,13 @@ struct ModeCopy {
     bool blocked = false;
     uint32_t nblocks = 1;
     uint64_t outer_runs = 0;                   // distinct (row, level-0 coordinate) pairs
-    std::vector<uint32_t> blk_host;            // s2::Blk table (10 words per block)
-    DevBuf<uint32_t> blk_dev, recA, sk, kperm;
-    // work schedule for a grid size (s2::Item list + per-CTA offsets)
+    DevBuf<uint32_t> blk_dev;                  // s2::Blk table
+    DevBuf<uint32_t> recA, sk, kperm;          // warp-interleaved records, slow keys, kperm
+    DevBuf<uint32_t> wdesc, items, cta_items;  // work schedule (grid = SM count)
+    uint32_t nitems = 0;
     unsigned grid = 0;
-    DevBuf<uint32_t> items, cta_items;
-    ZeroList zl;
+    DevBuf<uint32_t> zero_rows;                // rows to pre-zero (unblocked plans)
+    uint64_t n_zero_rows = 0;
   } s2;
   // multi-GPU row-range shard of this copy: copy rows [k0, k1) = elements [e0, e1)
   uint64_t shard_k0 = 0, shard_k1 = 0, shard_e0 = 0, shard_e1 = 0;
@@ -117,6 +118,7 @@ struct Context {
   // device scalars: [0] = min non-finite copy position (uint64, ~0 = none), [1] = mode
   DevBuf<unsigned long long> nonfinite;
   DevBuf<uint8_t> flush_buf;
+  DevBuf<uint32_t> s2sync;  // streaming kernel: finished-CTA counter + non-finite flag
   SortScratch scratch;
 
   // CPD-ALS state

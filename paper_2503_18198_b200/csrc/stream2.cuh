@@ -2,29 +2,31 @@
 // R = 32 / 64 and N = 3..5 (north-star subsystem 3; reference executor
 // detail::mttkrp_mode_impl, kernel.hpp:75-127, and Algorithm 2).
 //
-// Cost model (measured by tools/ubench_lsu.cu on B200).  Per element the
-// kernel must bring (N-1) factor rows of R*4 bytes into registers.  A 128-B row read by an
-// 8-lane group costs ~0.94 SM-cycles of the shared/L1 data path whether it comes from shared
-// memory or from an L1 hit; from L2 it additionally costs ~1 us of latency, so L2-fed
-// gathers are bound by bytes-in-flight, not bandwidth.  The plan therefore
+// Cost model (tools/ubench_lsu.cu and tools/ubench_chain.cu on B200).  Per
+// element the kernel must bring (N-1) factor rows of R*4 bytes into registers.  A 128-B row
+// read by an 8-lane group costs ~0.94 SM-cycles of the shared/L1 data path whether it comes
+// from shared memory or from an L1 hit; from L2 it additionally costs ~1 us of latency.  The
+// record -> two-gather -> FMA2 chain saturates that path at ~2.27 SM-cycles per element with
+// 16 warps.  The plan (stream2_plan.cu) therefore
 //  * orders the elements of every output row lexicographically by the input coordinates,
 //    smallest extent first ("levels"): the outermost level changes rarely inside a row, so
 //    its factor row stays in a register (`yo`) and is re-read only when it changes;
 //  * stages every inner level's factor in shared memory: whole when it fits, otherwise the
 //    copy is split into BLOCKS by slices of the inner levels' coordinates, each block's
-//    slices fitting shared memory (stream2_plan.cu); CTAs stage one block at a time;
+//    slices fitting shared memory; CTAs stage one block at a time;
 //  * packs an element into 8 bytes (value + inner coordinates relative to the block's
-//    slices + a "slow-key changed" flag), read with one LDS.64 per lane group.  The slow key
-//    (c_d | outer coordinate << rowbits) sits in a side array read only at changes and at
-//    segment edges.
+//    slices + a "slow-key changed" flag), read with one LDS.64 per lane group; the slow key
+//    (c_d | outer coordinate << rowbits) sits in a side stream read only at changes.
 //
-// Work split: persistent CTAs walk a host-built list of work items (block, tile range).  A
-// warp owns a 2-stage TMA ring of warp tiles (GPW groups x S elements), so no CTA-wide
-// barrier sits in the loop.  A lane group of G = R/4 lanes (float4 per lane) owns S
-// consecutive elements, accumulates the current output row in registers and stores it once
-// (Local_Update) or adds it with a vector atomic when the run crosses a segment boundary
-// (Global_Update; such rows are pre-zeroed).  In a blocked plan rows span blocks, so every
-// flush is atomic into a zeroed output.
+// Work split: every lane group (G = R/4 lanes, float4 per lane) owns ONE long contiguous
+// range of the kernel order and keeps its row accumulator, outer row and slow key across the
+// whole range, so rows are flushed only when they end (Local_Update, plain store) and at the
+// two ends of the range (Global_Update, vector atomic into a pre-zeroed row).  The records of
+// a warp's groups are laid out in HBM chunk-interleaved (chunk t of group 0, of group 1, ...),
+// so each tile of a warp's 2-stage ring is ONE TMA bulk copy of records plus one of slow
+// keys, and no barrier wider than the warp sits in the loop.  Persistent CTAs walk a
+// host-built list of work items (block, per-warp stream descriptors).  In a blocked plan rows
+// span blocks, so every flush is atomic into a zeroed output.
 #pragma once
 
 #include <algorithm>
@@ -35,34 +37,46 @@
 namespace mkb {
 namespace s2 {
 
-constexpr int kS = 15;  // elements per group segment (odd: conflict-free record reads)
-constexpr uint32_t kMaxDynSmem = 227u * 1024u;
-constexpr uint32_t kLeadB = 4, kTailPad = 64;  // side-array lead pad, record tail pad
+constexpr uint32_t kMaxDynSmem = 226u * 1024u;  // 227 KB opt-in minus static shared memory
 
-// Element ranges and factor slices of one block (device table).
+// Chunk geometry per record width (AW = record words).  S = elements per group per tile;
+// RS / KS = record / slow-key stride of one group's chunk.  RS * AW * 4 is 32 mod 128 bytes,
+// so the groups of a warp read their records from different banks; all chunk sizes are
+// multiples of 16 B (TMA).
+constexpr int seg_len(int aw) { return aw == 2 ? 36 : 18; }
+constexpr int rec_stride(int aw) { return aw == 2 ? 36 : 18; }
+constexpr int key_stride(int aw) { return aw == 2 ? 36 : 20; }
+
+// Factor slices of one block (device table).
 struct Blk {
-  uint32_t e0, e1;     // record range (e0 % 4 == 0)
   uint32_t lo[4];      // first staged row of each inner slot
   uint32_t bytes[4];   // staged bytes of each inner slot (rows * R * 4)
 };
-// One unit of a CTA's work: tiles [t0, t1) of block blk (tiles start at Blk::e0).
+// One warp's stream inside a work item.
+struct WDesc {
+  uint32_t rec0, key0;  // first record / slow key of the warp's tile 0
+  uint32_t tiles;       // tiles (chunks per group)
+  uint32_t flags;       // bit g: group g's first run continues from before its range;
+                        // bit 4+g: its last run continues after its range
+  uint32_t n[4];        // elements of each group
+};
 struct Item {
-  uint32_t blk, t0, t1, e0;  // e0: first element owned (shard start, else Blk::e0)
+  uint32_t blk, wdesc;  // block; first of the CTA's NW warp descriptors
 };
 
 struct Args {
   const uint2* recA2;       // AW == 2: {value, P0}
   const uint4* recA4;       // AW == 4: {value, P0, P1, P2}
-  const uint32_t* sk;       // slow keys; indices -kLeadB.. are valid (padding)
-  const uint32_t* kperm;    // record -> reference copy position
+  const uint32_t* sk;       // slow keys
+  const uint32_t* kperm;    // record -> reference copy position (~0: padding)
   const float* Yg[4];       // factor of each level (global)
   const Blk* blks;
+  const WDesc* wdesc;
   const Item* items;
   const uint32_t* cta_items;  // CTA c owns items [cta_items[c], cta_items[c+1])
   float* out;
   unsigned long long* nonfinite;
   unsigned long long tag;
-  uint32_t e1;               // end of the owned range (shard end, else nnz) for unblocked
   uint32_t rowmask, rowbits;
   uint32_t asc_level;        // nibble p = level of the p-th input in ascending mode order
   uint32_t b0, m0, m1;       // packed-coordinate shift / masks (see Lay)
@@ -70,11 +84,17 @@ struct Args {
   uint32_t outer_off, outer_bytes;  // staged outer factor (OS)
   uint32_t records_off;      // SMEM byte offset of the per-warp record rings
   uint32_t blocked;          // 1: every flush atomic (output pre-zeroed)
+  uint32_t nitems;
+  const uint32_t* zero_rows; // rows every launch zeroes before its first atomic flush
+  uint32_t n_zero;           // (blocked plans: all rows 0..n_zero-1, zero_rows unused)
+  uint32_t* sync;            // [0] finished CTAs, [1] non-finite row seen, [2] CTAs done
+                             // zeroing (all 0 between launches)
 };
 
 // Record layout.  AW = 2 (NIN <= 2): P0 = c0 | c1 << b0 | flag << 31.
 // AW = 4 (NIN >= 3): P0 = c0 | (NIN == 4 ? c1 << b0 : 0) | flag << 31, then the remaining
-// slots one per word.  flag = this element's slow key differs from the previous record's.
+// slots one per word.  flag = first element of the group range, or its slow key differs from
+// the previous element's.
 template <int NI, int NOUT>
 struct Lay {
   static constexpr int NIN = NI - NOUT;
@@ -116,56 +136,85 @@ __device__ __forceinline__ void read_rec(const uint8_t* ringA, uint32_t i, uint3
   }
 }
 
-// Cold path (kernel.hpp:109-114): recompute the run's products in the reference's order
-// (val, then the inputs by ascending mode) and report every offending element's reference
-// copy position; the launch minimum is the reference's first failing position.
-template <int NI, int NOUT, int G>
-__device__ __noinline__ void rescan(const Args& a, const Blk* blk, int lane_g, uint32_t s,
-                                    uint32_t e) {
+// Cold path (kernel.hpp:109-114), run by the last CTA of a launch in which some row sum was
+// non-finite: recompute every element's product in the reference's order (val, then the
+// inputs by ascending mode, __fmul_rn) and report each offending element's reference copy
+// position; the atomic minimum is the reference's first failing position.
+template <int NI, int NOUT, int G, int NW>
+__device__ __noinline__ void rescan_all(const Args& a) {
   using L = Lay<NI, NOUT>;
-  for (uint32_t j = s; j < e; ++j) {
-    uint32_t r[4];
-    if constexpr (L::AW == 2) {
-      const uint2 v = a.recA2[j];
-      r[0] = v.x;
-      r[1] = v.y;
-      r[2] = r[3] = 0;
-    } else {
-      const uint4 v = a.recA4[j];
-      r[0] = v.x;
-      r[1] = v.y;
-      r[2] = v.z;
-      r[3] = v.w;
+  constexpr int S = seg_len(L::AW), RS = rec_stride(L::AW), KS = key_stride(L::AW);
+  constexpr int GPW = 32 / G;
+  for (uint32_t ii = 0; ii < a.nitems; ++ii) {
+    const Item item = a.items[ii];
+    const Blk* blk = a.blks + item.blk;
+    for (uint32_t w = 0; w < static_cast<uint32_t>(NW); ++w) {
+      const WDesc d = a.wdesc[item.wdesc + w];
+      const uint32_t total = d.tiles * GPW * S;
+      for (uint32_t q = threadIdx.x; q < total; q += blockDim.x) {
+        const uint32_t s = q % S, g = (q / S) % GPW, t = q / (S * GPW);
+        const uint32_t j = d.rec0 + (t * GPW + g) * RS + s;
+        if (a.kperm[j] == 0xffffffffu) continue;
+        uint32_t r[4];
+        if constexpr (L::AW == 2) {
+          const uint2 v = a.recA2[j];
+          r[0] = v.x;
+          r[1] = v.y;
+          r[2] = r[3] = 0;
+        } else {
+          const uint4 v = a.recA4[j];
+          r[0] = v.x;
+          r[1] = v.y;
+          r[2] = v.z;
+          r[3] = v.w;
+        }
+        uint32_t ci[4];
+        unpack<NI, NOUT>(r, a.b0, a.m0, a.m1, ci);
+        const uint32_t key = a.sk[d.key0 + (t * GPW + g) * KS + s];
+        uint32_t c[4];
+        for (int l = 0; l < NI; ++l)
+          c[l] = l < NOUT ? (key >> a.rowbits) : ci[l - NOUT] + blk->lo[l - NOUT];
+        const float v = __uint_as_float(r[0]);
+        bool bad = false;
+        for (int x = 0; x < G * 4; ++x) {
+          float p = v;
+          for (int m = 0; m < NI; ++m) {
+            const uint32_t l = (a.asc_level >> (4 * m)) & 15u;
+            p = __fmul_rn(p, a.Yg[l][static_cast<size_t>(c[l]) * G * 4 + x]);
+          }
+          bad |= !isfinite(p);
+        }
+        if (bad) atomicMin(a.nonfinite, a.tag | static_cast<unsigned long long>(a.kperm[j]));
+      }
     }
-    uint32_t ci[4];
-    unpack<NI, NOUT>(r, a.b0, a.m0, a.m1, ci);
-    uint32_t c[4];
-    for (int l = 0; l < NI; ++l)
-      c[l] = l < NOUT ? (a.sk[j] >> a.rowbits) : ci[l - NOUT] + blk->lo[l - NOUT];
-    const float v = __uint_as_float(r[0]);
-    float t[4] = {v, v, v, v};
-    for (int p = 0; p < NI; ++p) {
-      const uint32_t l = (a.asc_level >> (4 * p)) & 15u;
-      const float4 y = __ldg(reinterpret_cast<const float4*>(a.Yg[l]) +
-                             static_cast<size_t>(c[l]) * G + lane_g);
-      t[0] = __fmul_rn(t[0], y.x);
-      t[1] = __fmul_rn(t[1], y.y);
-      t[2] = __fmul_rn(t[2], y.z);
-      t[3] = __fmul_rn(t[3], y.w);
-    }
-    if (!isfinite(t[0]) || !isfinite(t[1]) || !isfinite(t[2]) || !isfinite(t[3]))
-      atomicMin(a.nonfinite, a.tag | static_cast<unsigned long long>(a.kperm[j]));
   }
 }
 
+// Every CTA zeroes its share of the launch's pre-zero rows first and counts itself in
+// sync[2]; an atomic flush (Global_Update) may add into a zeroed row only once all CTAs have
+// (the grid is co-resident: cooperative launch).  In practice the count is complete long
+// before the first flush.
+__device__ __forceinline__ void wait_zeroed(const uint32_t* cnt, bool& zeroed) {
+  if (zeroed) return;
+  uint32_t v;
+  do {
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(cnt) : "memory");
+    if (v >= gridDim.x) break;
+    __nanosleep(64);
+  } while (true);
+  zeroed = true;
+}
+
 __device__ __forceinline__ void flush(float4* outv, uint32_t row, float2 a0, float2 a1,
-                                      bool atomic, int G) {
+                                      bool atomic, int G, const uint32_t* zcnt, bool& zeroed) {
   float4* p = outv + static_cast<size_t>(row) * G;
   const float4 v = make_float4(a0.x, a0.y, a1.x, a1.y);
-  if (atomic)
+  if (atomic) {
+    wait_zeroed(zcnt, zeroed);
     atomicAdd(p, v);
-  else
+  } else {
     *p = v;
+  }
 }
 
 // Per-lane constants of one launch.
@@ -176,17 +225,18 @@ struct Lane {
   uint32_t so;             // staged outer factor base
   const float4* go;        // global outer factor base
   float4* outv;
+  const uint32_t* zcnt;    // CTAs done zeroing
   uint32_t rowmask, rowbits, b0, m0, m1;
   int lane_g;
-  bool blocked;
 };
 
-// Per-segment state of one lane group.
+// Per-group running state over its range.
 struct Seg {
   float2 acc0, acc1;
   float4 yo;
-  uint32_t cur, row, run_start;
-  bool first, head_split;
+  uint32_t cur, row;
+  bool first, head_atomic, all_atomic, bad;  // all_atomic: blocked plan (rows span blocks)
+  bool zeroed;                                // the launch's pre-zeroing is complete
 };
 
 template <int NI, int NOUT, int K, bool OS, int G>
@@ -217,52 +267,56 @@ struct Body {
     s.acc0 = __ffma2_rn(t0, make_float2(v, v), s.acc0);
     s.acc1 = __ffma2_rn(t1, make_float2(v, v), s.acc1);
   }
-  static __device__ __forceinline__ void check_run(const Args& a, const Blk* blk,
-                                                   const Lane<NIN>& ln, const Seg& s, uint32_t e) {
-    if (!isfinite(s.acc0.x + s.acc0.y + s.acc1.x + s.acc1.y))
-      rescan<NI, NOUT, G>(a, blk, ln.lane_g, s.run_start, e);
-  }
-  // slow-key change at record position pos: flush the row if it changed, reload yo
-  static __device__ __forceinline__ void rekey(const Args& a, const Blk* blk, const Lane<NIN>& ln,
-                                               Seg& s, uint32_t sk, uint32_t pos) {
+  // slow-key change: flush the finished row (if any), reload the outer row
+  static __device__ __forceinline__ void rekey(const Lane<NIN>& ln, Seg& s, uint32_t sk) {
     const uint32_t r = sk & ln.rowmask;
     if (r != s.row) {
-      check_run(a, blk, ln, s, pos);
-      flush(ln.outv, s.row, s.acc0, s.acc1, ln.blocked || (s.first && s.head_split), G);
-      s.first = false;
+      if (s.row != 0xffffffffu) {
+        s.bad |= !isfinite(s.acc0.x + s.acc0.y + s.acc1.x + s.acc1.y);
+        flush(ln.outv, s.row, s.acc0, s.acc1, s.all_atomic || (s.first && s.head_atomic), G,
+              ln.zcnt, s.zeroed);
+        s.first = false;
+      }
       s.row = r;
-      s.run_start = pos;
       s.acc0 = make_float2(0.f, 0.f);
       s.acc1 = s.acc0;
     }
     if constexpr (NOUT > 0) s.yo = outer(ln, sk);
     s.cur = sk;
   }
-  // B elements [k, k+B) of a full segment: all records, all gathers, one warp vote; the
-  // common case (no flagged element in the warp) is straight-line FMUL2/FFMA2.
+  // Full chunks run a software pipeline over batches of B elements: the records of batch
+  // k+2 and the gathers of batch k+1 are in flight while batch k is consumed.  Consuming a
+  // batch is one warp vote; the common case (no flagged element in the warp) is
+  // straight-line FMUL2/FFMA2.
   template <int B>
-  static __device__ __forceinline__ void batch(const Args& a, const Blk* blk, const Lane<NIN>& ln,
-                                               Seg& s, const uint8_t* RA, const uint32_t* RB,
-                                               uint32_t k, uint32_t p0) {
-    uint32_t r[B][4];
-    float4 y[B][NIN];
+  static __device__ __forceinline__ void fetch(const uint8_t* RA, uint32_t k, uint32_t (&r)[B][4]) {
 #pragma unroll
     for (int b = 0; b < B; ++b) read_rec<NI, NOUT>(RA, k + b, r[b]);
-    bool slow = false;
+  }
+  template <int B>
+  static __device__ __forceinline__ void gather_batch(const Lane<NIN>& ln, const uint32_t (&r)[B][4],
+                                                      float4 (&y)[B][NIN]) {
 #pragma unroll
     for (int b = 0; b < B; ++b) {
       uint32_t c[4];
       unpack<NI, NOUT>(r[b], ln.b0, ln.m0, ln.m1, c);
 #pragma unroll
       for (int j = 0; j < NIN; ++j) y[b][j] = gather(ln, j, c[j]);
-      slow |= static_cast<int>(r[b][1]) < 0;
     }
-    if (__any_sync(0xffffffffu, slow)) {
+  }
+  template <int B>
+  static __device__ __forceinline__ void consume(const Lane<NIN>& ln, Seg& s, const uint32_t* RB,
+                                                 uint32_t k, const uint32_t (&r)[B][4],
+                                                 const float4 (&y)[B][NIN]) {
+    uint32_t any = 0;
+#pragma unroll
+    for (int b = 0; b < B; ++b) any |= r[b][1];
+    if (__any_sync(0xffffffffu, static_cast<int>(any) < 0)) {
 #pragma unroll
       for (int b = 0; b < B; ++b) {
         if (static_cast<int>(r[b][1]) < 0) {
           const uint32_t sk = RB[k + b];
-          if (sk != s.cur) rekey(a, blk, ln, s, sk, p0 + k + b);
+          if (sk != s.cur || s.row == 0xffffffffu) rekey(ln, s, sk);
         }
         math(s, __uint_as_float(r[b][0]), y[b]);
       }
@@ -271,24 +325,35 @@ struct Body {
       for (int b = 0; b < B; ++b) math(s, __uint_as_float(r[b][0]), y[b]);
     }
   }
-  // one element of a partial segment (shard / block edges)
-  static __device__ __forceinline__ void single(const Args& a, const Blk* blk, const Lane<NIN>& ln,
-                                                Seg& s, const uint8_t* RA, const uint32_t* RB,
-                                                uint32_t k, uint32_t n, uint32_t p0) {
-    const bool v = k < n;
-    uint32_t r[4];
-    float4 y[NIN];
-    read_rec<NI, NOUT>(RA, v ? k : 0u, r);
-    uint32_t c[4];
-    unpack<NI, NOUT>(r, ln.b0, ln.m0, ln.m1, c);
+  // A chunk is S / B batches (an even number), pipelined as a rolled loop over batch pairs
+  // (ping-pong gather buffers; a small instruction footprint keeps the i-cache warm): while
+  // batch k is consumed the gathers of batch k+1 and the records of batch k+2 are in flight.
+  template <int B, int S>
+  static __device__ __forceinline__ void chunk(const Lane<NIN>& ln, Seg& s, const uint8_t* RA,
+                                               const uint32_t* RB) {
+    constexpr int NB = S / B;
+    static_assert(NB % 2 == 0, "batches are processed in pairs");
+    uint32_t rA[B][4], rB[B][4];
+    float4 yA[B][NIN], yB[B][NIN];
+    fetch<B>(RA, 0, rA);
+    fetch<B>(RA, B, rB);
+    gather_batch<B>(ln, rA, yA);
+#pragma unroll 1
+    for (int k = 0; k < NB; k += 2) {
+      uint32_t rC[B][4];
+      gather_batch<B>(ln, rB, yB);                          // batch k+1
+      if (k + 2 < NB) fetch<B>(RA, (k + 2) * B, rC);        // batch k+2 records
+      consume<B>(ln, s, RB, k * B, rA, yA);                 // batch k
+      if (k + 2 < NB) gather_batch<B>(ln, rC, yA);          // batch k+2
+      consume<B>(ln, s, RB, (k + 1) * B, rB, yB);           // batch k+1
+      if (k + 2 < NB) {
+        fetch<B>(RA, (k + 3) * B, rB);                      // batch k+3 records
 #pragma unroll
-    for (int j = 0; j < NIN; ++j)
-      if (v) y[j] = gather(ln, j, c[j]);
-    if (v && static_cast<int>(r[1]) < 0) {
-      const uint32_t sk = RB[k];
-      if (sk != s.cur) rekey(a, blk, ln, s, sk, p0 + k);
+        for (int b = 0; b < B; ++b)
+#pragma unroll
+          for (int q = 0; q < 4; ++q) rA[b][q] = rC[b][q];
+      }
     }
-    if (v) math(s, __uint_as_float(r[0]), y);
   }
 };
 
@@ -300,17 +365,15 @@ __global__ void __launch_bounds__(NT, MINB) k_stream2(const Args a) {
   using L = Lay<NI, NOUT>;
   using Bd = Body<NI, NOUT, K, OS, G>;
   constexpr int NIN = L::NIN;
-  constexpr int S = kS;
+  constexpr int S = seg_len(L::AW), RS = rec_stride(L::AW), KS = key_stride(L::AW);
   constexpr int GPW = 32 / G;   // lane groups per warp
-  constexpr int WT = GPW * S;   // elements per warp tile
   constexpr int NW = NT / 32;
   constexpr uint32_t RECB = L::AW * 4u;
-  constexpr uint32_t BA = WT * RECB;            // part A slot
-  constexpr uint32_t BB = ((WT + 8u) * 4u + 15u) & ~15u;  // slow-key slot (aligned superset)
+  constexpr uint32_t BA = GPW * RS * RECB;      // records of one tile
+  constexpr uint32_t BB = GPW * KS * 4u;        // slow keys of one tile
   constexpr uint32_t WBYTES = 2u * (BA + BB);
-  static_assert(S % B == 0, "segment must be a whole number of batches");
-  static_assert(WT % 2 == 0, "warp tiles must hold an even number of records");
-  static_assert(BA % 16 == 0, "ring slots must stay 16-B aligned");
+  static_assert(S % B == 0, "a chunk must be a whole number of batches");
+  static_assert(BA % 16 == 0 && BB % 16 == 0, "tiles must be multiples of 16 B");
   extern __shared__ __align__(128) uint8_t smem[];
 
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
@@ -326,7 +389,23 @@ __global__ void __launch_bounds__(NT, MINB) k_stream2(const Args a) {
     mbar_init(&wbar[1], 1);
     mbar_fence_init();
   }
+  // this CTA's share of the pre-zero rows (Global_Update targets), then count it done
+  {
+    const uint32_t z0 = static_cast<uint32_t>(static_cast<uint64_t>(a.n_zero) * blockIdx.x / gridDim.x);
+    const uint32_t z1 =
+        static_cast<uint32_t>(static_cast<uint64_t>(a.n_zero) * (blockIdx.x + 1) / gridDim.x);
+    const float4 zero = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (uint32_t i = z0 + tid / G; i < z1; i += NT / G) {
+      const uint32_t row = a.blocked ? i : a.zero_rows[i];
+      if (row != 0xffffffffu)
+        reinterpret_cast<float4*>(a.out)[static_cast<size_t>(row) * G + tid % G] = zero;
+    }
+  }
   __syncthreads();
+  if (tid == 0) {
+    __threadfence();
+    atomicAdd(a.sync + 2, 1u);
+  }
 
   Lane<NIN> ln;
   ln.lane_g = lane % G;
@@ -338,30 +417,42 @@ __global__ void __launch_bounds__(NT, MINB) k_stream2(const Args a) {
   ln.so = smem_u32(smem + a.outer_off) + ln.lane_g * 16u;
   ln.go = reinterpret_cast<const float4*>(a.Yg[0]) + ln.lane_g;
   ln.outv = reinterpret_cast<float4*>(a.out) + ln.lane_g;
+  ln.zcnt = a.sync + 2;
   ln.rowmask = a.rowmask;
   ln.rowbits = a.rowbits;
   ln.b0 = a.b0;
   ln.m0 = a.m0;
   ln.m1 = a.m1;
-  ln.blocked = a.blocked != 0;
+  const bool blocked = a.blocked != 0;
 
   const uint8_t* gA = L::AW == 2 ? reinterpret_cast<const uint8_t*>(a.recA2)
                                  : reinterpret_cast<const uint8_t*>(a.recA4);
+  bool bad = false;         // this lane flushed a non-finite row sum
+  bool zeroed = false;      // this lane has seen the launch's pre-zeroing complete
   uint32_t it = 0;          // this warp's ring sequence number
   uint32_t sphase = 0;      // staging barrier phase
   uint32_t staged = 0xffffffffu;
   const uint32_t i_end = a.cta_items[blockIdx.x + 1];
   for (uint32_t ii = a.cta_items[blockIdx.x]; ii < i_end; ++ii) {
     const Item item = a.items[ii];
-    const Blk* blk = a.blks + item.blk;
-    const uint32_t be1 = a.blocked ? blk->e1 : a.e1;
-    const uint32_t ee0 = item.e0;
-    const uint32_t tbase = blk->e0;  // tiles of the block start here (multiple of 4)
+    const WDesc d = a.wdesc[ii * NW + wid];
+    auto issue = [&](uint32_t t, int st) {
+      mbar_arrive_tx(&wbar[st], BA + BB);
+      tma_load_1d(ring + st * BA, gA + (static_cast<size_t>(d.rec0) + t * GPW * RS) * RECB, BA,
+                  &wbar[st]);
+      tma_load_1d(ring + 2 * BA + st * BB, a.sk + d.key0 + t * GPW * KS, BB, &wbar[st]);
+    };
+    if (lane == 0) {
+      if (d.tiles > 0) issue(0, it & 1);
+      if (d.tiles > 1) issue(1, (it + 1) & 1);
+    }
+    __syncwarp();
     // (re)stage the block's factor slices (and the outer factor once)
     if constexpr (K > 0 || OS) {
       if (item.blk != staged) {
         __syncthreads();  // every warp is done with the previous slices
         if (tid == 0) {
+          const Blk* blk = a.blks + item.blk;
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
           uint32_t total = 0;
 #pragma unroll
@@ -386,94 +477,79 @@ __global__ void __launch_bounds__(NT, MINB) k_stream2(const Args a) {
         staged = item.blk;
       }
     }
-
-    auto issue = [&](uint32_t t, int st) {
-      const uint32_t base = tbase + t * WT;
-      const uint32_t cnt = min(static_cast<uint32_t>(WT), be1 - base);
-      // part A: an even count (bulk sizes are multiples of 16 B; the array is padded)
-      const uint32_t cnt2 = (cnt + 1u) & ~1u;
-      // slow keys [base-1, base+cnt+1) rounded out to 16-B boundaries (lead/tail padded)
-      const uint32_t b0i = (base - 1u + kLeadB) & ~3u;  // index into the padded array
-      const uint32_t b1i = (base + cnt + 1u + kLeadB + 3u) & ~3u;
-      mbar_arrive_tx(&wbar[st], cnt2 * RECB + (b1i - b0i) * 4u);
-      tma_load_1d(ring + st * BA, gA + static_cast<size_t>(base) * RECB, cnt2 * RECB, &wbar[st]);
-      tma_load_1d(ring + 2 * BA + st * BB, a.sk - kLeadB + b0i, (b1i - b0i) * 4u, &wbar[st]);
-    };
-    const uint32_t t0 = item.t0 + wid, t1 = item.t1;
-    if (lane == 0) {
-      if (t0 < t1) issue(t0, it & 1);
-      if (t0 + NW < t1) issue(t0 + NW, (it + 1) & 1);
-    }
-    __syncwarp();
-    for (uint32_t t = t0; t < t1; t += NW, ++it) {
+    Seg s;
+    s.acc0 = make_float2(0.f, 0.f);
+    s.acc1 = s.acc0;
+    s.yo = make_float4(1.f, 1.f, 1.f, 1.f);
+    s.cur = 0xffffffffu;
+    s.row = 0xffffffffu;
+    s.first = true;
+    s.head_atomic = (d.flags >> gw) & 1u;
+    s.all_atomic = blocked;
+    s.zeroed = zeroed;
+    s.bad = false;
+    for (uint32_t t = 0; t < d.tiles; ++t, ++it) {
       const int st = it & 1;
       mbar_wait(&wbar[st], (it >> 1) & 1);
-      const uint32_t base = tbase + t * WT;
-      const uint32_t b0i = (base - 1u + kLeadB) & ~3u;
-      const uint32_t s0 = base + gw * S;
-      const uint32_t p0 = s0 < ee0 ? ee0 : s0;
-      const uint32_t p1 = s0 >= be1 ? p0 : min(s0 + S, be1);
-      const uint32_t n = p1 - p0;
-      const uint8_t* RA = ring + st * BA + (p0 - base) * RECB;
-      const uint32_t* RB =
-          reinterpret_cast<const uint32_t*>(ring + 2 * BA + st * BB) + (p0 + kLeadB - b0i);
-      Seg s;
-      s.acc0 = make_float2(0.f, 0.f);
-      s.acc1 = s.acc0;
-      s.yo = make_float4(1.f, 1.f, 1.f, 1.f);
-      s.cur = 0xffffffffu;
-      s.row = 0xffffffffu;
-      s.run_start = p0;
-      s.first = true;
-      s.head_split = false;
-      bool tail_split = false;
-      if (n) {
-        s.cur = RB[0];
-        s.row = s.cur & ln.rowmask;
-        s.head_split = p0 > ee0 && (RB[-1] & ln.rowmask) == s.row;
-        tail_split = p1 < be1 && (RB[n] & ln.rowmask) == (RB[n - 1] & ln.rowmask);
-        if constexpr (NOUT > 0) s.yo = Bd::outer(ln, s.cur);
-      }
-      if (__all_sync(0xffffffffu, n == S)) {
-#pragma unroll
-        for (uint32_t k = 0; k < static_cast<uint32_t>(S); k += B)
-          Bd::template batch<B>(a, blk, ln, s, RA, RB, k, p0);
-      } else {
-#pragma unroll 1
-        for (uint32_t k = 0; k < static_cast<uint32_t>(S); ++k)
-          Bd::single(a, blk, ln, s, RA, RB, k, n, p0);
-      }
-      const bool have = n > 0;
-      const bool last_atomic = ln.blocked || tail_split || (s.first && s.head_split);
-      if (have) Bd::check_run(a, blk, ln, s, p1);
-      // When every group of the warp ends inside the same split row (long rows), combine
-      // the partial sums with a butterfly and issue one vector atomic per warp.
-      bool combined = false;
-      if constexpr (G < 32) {
-        const uint32_t key = (have && last_atomic) ? s.row : 0xffffffffu;
-        int same = 0;
-        __match_all_sync(0xffffffffu, key, &same);
-        if (same && key != 0xffffffffu) {
-#pragma unroll
-          for (int off = G; off < 32; off <<= 1) {
-            s.acc0.x += __shfl_xor_sync(0xffffffffu, s.acc0.x, off);
-            s.acc0.y += __shfl_xor_sync(0xffffffffu, s.acc0.y, off);
-            s.acc1.x += __shfl_xor_sync(0xffffffffu, s.acc1.x, off);
-            s.acc1.y += __shfl_xor_sync(0xffffffffu, s.acc1.y, off);
-          }
-          if (lane < G) flush(ln.outv, s.row, s.acc0, s.acc1, true, G);
-          combined = true;
-        }
-      }
-      if (have && !combined) flush(ln.outv, s.row, s.acc0, s.acc1, last_atomic, G);
+      const uint8_t* RA = ring + st * BA + gw * RS * RECB;
+      const uint32_t* RB = reinterpret_cast<const uint32_t*>(ring + 2 * BA + st * BB) + gw * KS;
+      // the last chunk of a group is padded with copies of its last record (value 0, no
+      // flag), so every chunk runs the same pipelined path
+      Bd::template chunk<B, S>(ln, s, RA, RB);
       __syncwarp();  // the whole warp is done with this stage
-      if (lane == 0 && t + 2 * NW < t1) issue(t + 2 * NW, st);
+      if (lane == 0 && t + 2 < d.tiles) issue(t + 2, st);
+    }
+    // the group's last run
+    const bool have = s.row != 0xffffffffu;
+    const bool last_atomic = blocked || ((d.flags >> (4 + gw)) & 1u) || (s.first && s.head_atomic);
+    if (have) s.bad |= !isfinite(s.acc0.x + s.acc0.y + s.acc1.x + s.acc1.y);
+    // When every group of the warp ends inside the same continued row, combine the partial
+    // sums with a butterfly and issue one vector atomic per warp.
+    bool combined = false;
+    if constexpr (G < 32) {
+      const uint32_t key = (have && last_atomic) ? s.row : 0xffffffffu;
+      int same = 0;
+      __match_all_sync(0xffffffffu, key, &same);
+      if (same && key != 0xffffffffu) {
+#pragma unroll
+        for (int off = G; off < 32; off <<= 1) {
+          s.acc0.x += __shfl_xor_sync(0xffffffffu, s.acc0.x, off);
+          s.acc0.y += __shfl_xor_sync(0xffffffffu, s.acc0.y, off);
+          s.acc1.x += __shfl_xor_sync(0xffffffffu, s.acc1.x, off);
+          s.acc1.y += __shfl_xor_sync(0xffffffffu, s.acc1.y, off);
+        }
+        if (lane < G) flush(ln.outv, s.row, s.acc0, s.acc1, true, G, ln.zcnt, zeroed);
+        combined = true;
+      }
+    }
+    if (have && !combined) flush(ln.outv, s.row, s.acc0, s.acc1, last_atomic, G, ln.zcnt, zeroed);
+    bad |= s.bad;
+    zeroed |= s.zeroed;
+  }
+  // Non-finite products are rare: lanes only remember that a row sum was non-finite; the
+  // last CTA to finish rescans the launch's elements in the reference's order.
+  if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(&a.sync[1], 1u);
+  __shared__ uint32_t last;
+  __syncthreads();
+  if (tid == 0) {
+    __threadfence();
+    last = atomicAdd(&a.sync[0], 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (last) {
+    __threadfence();
+    if (*reinterpret_cast<volatile uint32_t*>(&a.sync[1])) rescan_all<NI, NOUT, G, NW>(a);
+    __syncthreads();
+    if (tid == 0) {
+      a.sync[0] = 0;
+      a.sync[1] = 0;
+      a.sync[2] = 0;
     }
   }
 }
 
 constexpr uint32_t ring_bytes_rt(uint32_t aw, uint32_t G, uint32_t NT) {
-  return (NT / 32) * 2u * ((32 / G) * kS * aw * 4u + ((((32 / G) * kS + 8u) * 4u + 15u) & ~15u)) +
+  return (NT / 32) * 2u * ((32 / G) * rec_stride(aw) * aw * 4u + (32 / G) * key_stride(aw) * 4u) +
          (2u * (NT / 32) + 1u) * 8u;
 }
 template <int NI, int NOUT>
@@ -483,7 +559,7 @@ constexpr uint32_t ring_bytes(int G, int NT) {
 
 template <int NI, int NOUT, int K, bool OS, int G, int NT, int MINB>
 void launch_one(const Args& a, unsigned grid, size_t smem, cudaStream_t st) {
-  constexpr int B = Lay<NI, NOUT>::AW == 2 ? 5 : 3;
+  constexpr int B = 3;
   auto kern = k_stream2<NI, NOUT, K, OS, G, B, NT, MINB>;
   static bool attr_set = false;  // the attribute is per function, set before first launch
   if (!attr_set) {
@@ -491,18 +567,17 @@ void launch_one(const Args& a, unsigned grid, size_t smem, cudaStream_t st) {
                                   static_cast<int>(kMaxDynSmem)));
     attr_set = true;
   }
-  kern<<<grid, NT, smem, st>>>(a);
-  MKB_LAUNCH();
+  // cooperative: the pre-zeroing handshake needs every CTA resident
+  void* params[] = {const_cast<Args*>(&a)};
+  MKB_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(kern), dim3(grid), dim3(NT),
+                                       params, smem, st));
 }
 
+// Every plan runs 512-thread CTAs, one per SM (the staged factors take most of the shared
+// memory; without staging the rings still do).
 template <int NI, int NOUT, bool OS, int G>
 void launch_k(const Args& a, uint32_t K, unsigned grid, size_t staged_end, cudaStream_t st) {
   constexpr int NIN = NI - NOUT;
-  if (K == 0 && !OS) {
-    Args b = a;
-    b.records_off = 0;
-    return launch_one<NI, NOUT, 0, false, G, 256, 2>(b, grid, ring_bytes<NI, NOUT>(G, 256), st);
-  }
   const size_t smem = staged_end + ring_bytes<NI, NOUT>(G, 512);
   if (K == 0) return launch_one<NI, NOUT, 0, OS, G, 512, 1>(a, grid, smem, st);
   if constexpr (NIN >= 1)

@@ -18,6 +18,7 @@
 //  5. Records: value + inner coordinates relative to the block's slices + slow-key-changed
 //     flag; slow keys; kperm = reference copy position.  Blocks start 4-aligned.
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <vector>
 
@@ -28,8 +29,10 @@ namespace {
 
 using s2::Blk;
 using s2::Item;
-static_assert(sizeof(Blk) == 10 * sizeof(uint32_t), "Blk layout");
-static_assert(sizeof(Item) == 4 * sizeof(uint32_t), "Item layout");
+using s2::WDesc;
+static_assert(sizeof(Blk) == 8 * sizeof(uint32_t), "Blk layout");
+static_assert(sizeof(Item) == 2 * sizeof(uint32_t), "Item layout");
+static_assert(sizeof(WDesc) == 8 * sizeof(uint32_t), "WDesc layout");
 
 __global__ void k_rank_of_row(const uint32_t* __restrict__ row_seq, uint32_t nv,
                               uint32_t* __restrict__ rank) {
@@ -94,54 +97,83 @@ __global__ void k_count_runs(const uint32_t* __restrict__ cd, const uint32_t* __
   if ((threadIdx.x & 31) == 0 && local) atomicAdd(count, local);
 }
 
-struct PackArgs {
+struct FillArgs {
   Split sp;                       // inner slot coordinates + slicing
   const uint32_t* outer;          // level-0 coordinates (NOUT = 1) or null
   const uint32_t* cd;
   const float* val;
-  const uint32_t* perm;
-  const uint32_t* bstart;         // per block: first sorted position
-  const uint32_t* bdest;          // per block: first record position (4-aligned)
-  uint32_t rowbits, b0, aw, nin, nblocks;
-  uint64_t nnz;
+  const uint32_t* perm;           // kernel order -> copy position
+  const WDesc* wdesc;
+  const uint32_t* gstart;         // per descriptor and group: first kernel-order position
+  const uint32_t* dblk;           // per descriptor: block
+  const Blk* blks;
+  uint32_t rowbits, b0, aw, nin, gpw, S, RS, KS;
   uint32_t* recA;                 // aw words per record
-  uint32_t* sk;                   // slow keys (record index 0)
+  uint32_t* sk;
   uint32_t* kperm;
 };
 
-__global__ void k_pack(const PackArgs p) {
-  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < p.nnz;
-       i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
-    const uint32_t s = p.perm[i];
-    const uint32_t b = p.nblocks > 1 ? block_of(p.sp, s) : 0u;
-    const uint64_t dst = p.bdest[b] + (i - p.bstart[b]);
-    const uint32_t key = p.cd[s] | (p.outer ? p.outer[s] << p.rowbits : 0u);
-    bool flag = i == p.bstart[b];
-    if (!flag) {
-      const uint32_t q = p.perm[i - 1];
-      flag = key != (p.cd[q] | (p.outer ? p.outer[q] << p.rowbits : 0u));
+// One CTA per warp descriptor: writes the warp's chunk-interleaved records, slow keys and
+// kperm (padding slots: zero records, ~0 keys / kperm).
+__global__ void k_fill2(const FillArgs f) {
+  const WDesc d = f.wdesc[blockIdx.x];
+  const Blk bk = f.blks[f.dblk[blockIdx.x]];
+  const uint32_t W = f.RS > f.KS ? f.RS : f.KS;
+  const uint32_t total = d.tiles * f.gpw * W;
+  for (uint32_t q = threadIdx.x; q < total; q += blockDim.x) {
+    const uint32_t s = q % W, g = (q / W) % f.gpw, t = q / (W * f.gpw);
+    const uint32_t off = t * f.S + s;
+    const bool valid = s < f.S && off < d.n[g];
+    const size_t ri = d.rec0 + static_cast<size_t>(t * f.gpw + g) * f.RS + s;
+    const size_t ki = d.key0 + static_cast<size_t>(t * f.gpw + g) * f.KS + s;
+    uint32_t w[4] = {0, 0, 0, 0}, key = 0xffffffffu, kp = 0xffffffffu;
+    // padding of a group's last chunk: a copy of its last element with value 0 and no flag
+    const bool pad = s < f.S && !valid && d.n[g] > 0;
+    if (valid || pad) {
+      const uint32_t kpos = f.gstart[blockIdx.x * 4 + g] + (valid ? off : d.n[g] - 1);
+      const uint32_t e = f.perm[kpos];
+      key = f.cd[e] | (f.outer ? f.outer[e] << f.rowbits : 0u);
+      bool flag = off == 0;
+      if (!flag && valid) {
+        const uint32_t q2 = f.perm[kpos - 1];
+        flag = key != (f.cd[q2] | (f.outer ? f.outer[q2] << f.rowbits : 0u));
+      }
+      uint32_t c[4] = {0, 0, 0, 0};
+      for (uint32_t j = 0; j < f.nin; ++j) c[j] = f.sp.c[j][e] - bk.lo[j];
+      w[0] = __float_as_uint(f.val[e]);
+      if (f.nin == 1) {
+        w[1] = c[0];
+      } else if (f.nin == 2) {
+        w[1] = c[0] | (c[1] << f.b0);
+      } else if (f.nin == 3) {
+        w[1] = c[0];
+        w[2] = c[1];
+        w[3] = c[2];
+      } else {
+        w[1] = c[0] | (c[1] << f.b0);
+        w[2] = c[2];
+        w[3] = c[3];
+      }
+      if (flag && valid) w[1] |= 0x80000000u;
+      if (valid) {
+        kp = e;
+      } else {
+        w[0] = 0;  // +0.0f
+        key = 0xffffffffu;
+      }
     }
-    uint32_t c[4] = {0, 0, 0, 0};
-    for (uint32_t j = 0; j < p.nin; ++j) c[j] = p.sp.c[j][s] % p.sp.rows[j];
-    uint32_t w[4] = {__float_as_uint(p.val[s]), 0, 0, 0};
-    if (p.nin == 1) {
-      w[1] = c[0];
-    } else if (p.nin == 2) {
-      w[1] = c[0] | (c[1] << p.b0);
-    } else if (p.nin == 3) {
-      w[1] = c[0];
-      w[2] = c[1];
-      w[3] = c[2];
-    } else {
-      w[1] = c[0] | (c[1] << p.b0);
-      w[2] = c[2];
-      w[3] = c[3];
+    if (s < f.RS) {
+      for (uint32_t x = 0; x < f.aw; ++x) f.recA[ri * f.aw + x] = w[x];
+      f.kperm[ri] = kp;
     }
-    if (flag) w[1] |= 0x80000000u;
-    for (uint32_t q = 0; q < p.aw; ++q) p.recA[dst * p.aw + q] = w[q];
-    p.sk[dst] = key;
-    p.kperm[dst] = s;
+    if (s < f.KS) f.sk[ki] = key;
   }
+}
+
+__global__ void k_gather_rows(const uint32_t* __restrict__ cd, const uint32_t* __restrict__ pos,
+                              uint32_t n, uint32_t* __restrict__ out) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = cd[pos[i]];
 }
 
 __global__ void k_zero_rows2(float* __restrict__ out, uint32_t G, const uint32_t* __restrict__ rows,
@@ -347,7 +379,7 @@ bool prepare_stream2(Context& c, uint32_t mode) {
       stride *= split[j];
     }
   }
-  std::vector<uint32_t> bstart(p.nblocks + 1, 0), bdest(p.nblocks + 1, 0), bcount(p.nblocks, 0);
+  std::vector<uint32_t> bcount(p.nblocks, 0), bstart(p.nblocks + 1, 0);
   if (p.nblocks > 1) {
     DevBuf<uint32_t> counts(p.nblocks);
     MKB_CUDA(cudaMemsetAsync(counts.get(), 0, p.nblocks * sizeof(uint32_t), st));
@@ -360,49 +392,9 @@ bool prepare_stream2(Context& c, uint32_t mode) {
   } else {
     bcount[0] = static_cast<uint32_t>(nnz);
   }
+  for (uint32_t b = 0; b < p.nblocks; ++b) bstart[b + 1] = bstart[b] + bcount[b];
+  std::vector<Blk> blks(p.nblocks);
   for (uint32_t b = 0; b < p.nblocks; ++b) {
-    bstart[b + 1] = bstart[b] + bcount[b];
-    bdest[b + 1] = bdest[b] + ((bcount[b] + 3u) & ~3u);
-  }
-  const uint64_t nrec = bdest[p.nblocks];
-
-  // 5. records, slow keys, kperm, block table
-  p.recA.resize((nrec + s2::kTailPad) * p.aw);
-  MKB_CUDA(cudaMemsetAsync(p.recA.get(), 0, (nrec + s2::kTailPad) * p.aw * 4, st));
-  p.sk.resize(s2::kLeadB + nrec + s2::kTailPad);
-  MKB_CUDA(cudaMemsetAsync(p.sk.get(), 0xff, (s2::kLeadB + nrec + s2::kTailPad) * 4, st));
-  p.kperm.resize(nrec + s2::kTailPad);
-  MKB_CUDA(cudaMemsetAsync(p.kperm.get(), 0xff, (nrec + s2::kTailPad) * 4, st));
-  DevBuf<uint32_t> dstart(p.nblocks + 1), ddest(p.nblocks + 1);
-  MKB_CUDA(cudaMemcpyAsync(dstart.get(), bstart.data(), (p.nblocks + 1) * 4,
-                           cudaMemcpyHostToDevice, st));
-  MKB_CUDA(cudaMemcpyAsync(ddest.get(), bdest.data(), (p.nblocks + 1) * 4,
-                           cudaMemcpyHostToDevice, st));
-  PackArgs pa{};
-  pa.sp = sp;
-  pa.outer = p.nout ? mc.idx[lv[0]].get() : nullptr;
-  pa.cd = mc.idx[mode].get();
-  pa.val = mc.val.get();
-  pa.perm = perm.get();
-  pa.bstart = dstart.get();
-  pa.bdest = ddest.get();
-  pa.rowbits = p.rowbits;
-  pa.b0 = p.b0;
-  pa.aw = p.aw;
-  pa.nin = nin;
-  pa.nblocks = p.nblocks;
-  pa.nnz = nnz;
-  pa.recA = p.recA.get();
-  pa.sk = p.sk.get() + s2::kLeadB;
-  pa.kperm = p.kperm.get();
-  k_pack<<<gblocks, 256, 0, st>>>(pa);
-  MKB_LAUNCH();
-
-  p.blk_host.assign(static_cast<size_t>(p.nblocks) * 10, 0);
-  for (uint32_t b = 0; b < p.nblocks; ++b) {
-    Blk* bk = reinterpret_cast<Blk*>(p.blk_host.data()) + b;
-    bk->e0 = bdest[b];
-    bk->e1 = bdest[b] + bcount[b];
     uint32_t rem = b;
     for (int j = static_cast<int>(nin) - 1; j >= 0; --j) {
       const uint32_t q = rem % split[j];
@@ -410,60 +402,175 @@ bool prepare_stream2(Context& c, uint32_t mode) {
       const uint32_t ext = c.dims[lv[p.nout + j]];
       const uint32_t lo = q * rows[j];
       const uint32_t hi = std::min(ext, lo + rows[j]);
-      bk->lo[j] = lo;
-      bk->bytes[j] = static_cast<uint32_t>(static_cast<size_t>(hi - lo) * rowbytes);
+      blks[b].lo[j] = lo;
+      blks[b].bytes[j] = static_cast<uint32_t>(static_cast<size_t>(hi - lo) * rowbytes);
     }
   }
-  MKB_CUDA(cudaStreamSynchronize(st));  // temporaries are freed on return
-  p.ok = true;
-  return true;
-}
 
-namespace {
-
-// Per-CTA work items: the blocks' tiles concatenated in block order and cut into `grid`
-// near-equal contiguous ranges (a CTA restages only where its range crosses a block).
-void build_schedule(Context& c, ModeCopy::Stream2& p, const std::vector<uint32_t>& blk,
-                    uint32_t e0, unsigned grid, uint32_t wt) {
-  const uint32_t nb = static_cast<uint32_t>(blk.size() / 10);
-  const Blk* bk = reinterpret_cast<const Blk*>(blk.data());
-  std::vector<uint64_t> tstart(nb + 1, 0);
-  for (uint32_t b = 0; b < nb; ++b)
-    tstart[b + 1] = tstart[b] + (bk[b].e1 > bk[b].e0 ? (bk[b].e1 - bk[b].e0 + wt - 1) / wt : 0);
-  const uint64_t total = tstart[nb];
-  std::vector<uint32_t> items, cta(grid + 1, 0);
+  // 5. work split: CTA c takes an equal slice of the owned kernel-order range, cut at block
+  //    boundaries into items; an item's elements are split evenly over the CTA's lane groups;
+  //    a warp's groups stream chunk-interleaved records.
+  const uint32_t S = s2::seg_len(p.aw), RS = s2::rec_stride(p.aw), KS = s2::key_stride(p.aw);
+  const uint32_t NW = 16, GPW = 32 / G, NG = NW * GPW;
+  const unsigned grid = static_cast<unsigned>(c.num_sms);
+  const uint64_t E0 = p.blocked ? 0 : mc.shard_e0, E1 = p.blocked ? nnz : mc.shard_e1;
+  std::vector<WDesc> wd;
+  std::vector<uint32_t> gstart, dblk, items, cta(grid + 1, 0);
+  uint64_t rec_n = 0, key_n = 0;
   uint32_t b = 0;
-  for (unsigned g = 0; g < grid; ++g) {
-    cta[g] = static_cast<uint32_t>(items.size() / 4);
-    const uint64_t lo = total * g / grid, hi = total * (g + 1) / grid;
-    uint64_t t = lo;
-    while (b < nb && tstart[b + 1] <= t) ++b;
+  for (unsigned cc = 0; cc < grid; ++cc) {
+    cta[cc] = static_cast<uint32_t>(items.size() / 2);
+    const uint64_t lo = E0 + (E1 - E0) * cc / grid, hi = E0 + (E1 - E0) * (cc + 1) / grid;
+    uint64_t x = lo;
+    while (b < p.nblocks && bstart[b + 1] <= x && bstart[b + 1] < E1) ++b;
     uint32_t bb = b;
-    while (t < hi && bb < nb) {
-      const uint64_t end = std::min<uint64_t>(hi, tstart[bb + 1]);
-      if (end > t) {
+    while (x < hi && bb < p.nblocks) {
+      const uint64_t y = std::min<uint64_t>(hi, bstart[bb + 1]);
+      if (y > x) {
         items.push_back(bb);
-        items.push_back(static_cast<uint32_t>(t - tstart[bb]));
-        items.push_back(static_cast<uint32_t>(end - tstart[bb]));
-        items.push_back(std::max(bk[bb].e0, e0));
+        items.push_back(static_cast<uint32_t>(wd.size()));
+        for (uint32_t w = 0; w < NW; ++w) {
+          WDesc d{};
+          d.rec0 = static_cast<uint32_t>(rec_n);
+          d.key0 = static_cast<uint32_t>(key_n);
+          uint32_t tiles = 0;
+          for (uint32_t g = 0; g < 4; ++g) {
+            if (g < GPW) {
+              const uint64_t q = w * GPW + g;
+              const uint64_t g0 = x + (y - x) * q / NG, g1 = x + (y - x) * (q + 1) / NG;
+              d.n[g] = static_cast<uint32_t>(g1 - g0);
+              tiles = std::max<uint32_t>(tiles, (d.n[g] + S - 1) / S);
+              gstart.push_back(static_cast<uint32_t>(g0));
+            } else {
+              gstart.push_back(0);
+            }
+          }
+          d.tiles = tiles;
+          rec_n += static_cast<uint64_t>(tiles) * GPW * RS;
+          key_n += static_cast<uint64_t>(tiles) * GPW * KS;
+          wd.push_back(d);
+          dblk.push_back(bb);
+        }
       }
-      t = end;
+      x = y;
       ++bb;
     }
   }
-  cta[grid] = static_cast<uint32_t>(items.size() / 4);
-  if (items.empty()) items.assign(4, 0);
-  p.items.resize(items.size());
-  p.cta_items.resize(grid + 1);
-  MKB_CUDA(cudaMemcpyAsync(p.items.get(), items.data(), items.size() * 4, cudaMemcpyHostToDevice,
-                           c.stream));
-  MKB_CUDA(cudaMemcpyAsync(p.cta_items.get(), cta.data(), (grid + 1) * 4, cudaMemcpyHostToDevice,
-                           c.stream));
-  MKB_CUDA(cudaStreamSynchronize(c.stream));
+  cta[grid] = static_cast<uint32_t>(items.size() / 2);
+  if (rec_n >= 0xffffffffull || key_n >= 0xffffffffull) return false;
+  p.nitems = cta[grid];
   p.grid = grid;
-}
+  if (items.empty()) items.assign(2, 0);
 
-}  // namespace
+  // split flags (unblocked): a group's first / last run continues beyond its range
+  std::vector<uint32_t> zero_rows;
+  if (!p.blocked && !wd.empty()) {
+    std::vector<uint32_t> pos;
+    for (size_t i = 0; i < wd.size(); ++i)
+      for (uint32_t g = 0; g < GPW; ++g) {
+        const uint64_t g0 = gstart[i * 4 + g], g1 = g0 + wd[i].n[g];
+        pos.push_back(static_cast<uint32_t>(g0 > E0 ? g0 - 1 : g0));
+        pos.push_back(static_cast<uint32_t>(g0 < E1 ? g0 : g0 - 1));
+        pos.push_back(static_cast<uint32_t>(g1 > E0 ? g1 - 1 : g1));
+        pos.push_back(static_cast<uint32_t>(g1 < E1 ? g1 : g1 - 1));
+      }
+    DevBuf<uint32_t> dpos(pos.size()), drow(pos.size());
+    MKB_CUDA(cudaMemcpyAsync(dpos.get(), pos.data(), pos.size() * 4, cudaMemcpyHostToDevice, st));
+    k_gather_rows<<<ceil_div(pos.size(), 256), 256, 0, st>>>(
+        mc.idx[mode].get(), dpos.get(), static_cast<uint32_t>(pos.size()), drow.get());
+    MKB_LAUNCH();
+    std::vector<uint32_t> row(pos.size());
+    MKB_CUDA(cudaMemcpyAsync(row.data(), drow.get(), pos.size() * 4, cudaMemcpyDeviceToHost, st));
+    MKB_CUDA(cudaStreamSynchronize(st));
+    size_t k = 0;
+    for (size_t i = 0; i < wd.size(); ++i)
+      for (uint32_t g = 0; g < GPW; ++g, k += 4) {
+        const uint64_t g0 = gstart[i * 4 + g], g1 = g0 + wd[i].n[g];
+        if (!wd[i].n[g]) continue;
+        if (g0 > E0 && row[k] == row[k + 1]) {
+          wd[i].flags |= 1u << g;
+          zero_rows.push_back(row[k + 1]);
+        }
+        if (g1 < E1 && row[k + 2] == row[k + 3]) wd[i].flags |= 1u << (4 + g);
+      }
+    std::sort(zero_rows.begin(), zero_rows.end());
+    zero_rows.erase(std::unique(zero_rows.begin(), zero_rows.end()), zero_rows.end());
+  }
+
+  // 6. device tables and the chunk-interleaved records
+  p.blk_dev.resize(blks.size() * 8);
+  MKB_CUDA(cudaMemcpyAsync(p.blk_dev.get(), blks.data(), blks.size() * sizeof(Blk),
+                           cudaMemcpyHostToDevice, st));
+  p.wdesc.resize(std::max<size_t>(wd.size(), 1) * 8);
+  if (!wd.empty())
+    MKB_CUDA(cudaMemcpyAsync(p.wdesc.get(), wd.data(), wd.size() * sizeof(WDesc),
+                             cudaMemcpyHostToDevice, st));
+  p.items.resize(items.size());
+  MKB_CUDA(cudaMemcpyAsync(p.items.get(), items.data(), items.size() * 4, cudaMemcpyHostToDevice,
+                           st));
+  p.cta_items.resize(grid + 1);
+  MKB_CUDA(cudaMemcpyAsync(p.cta_items.get(), cta.data(), (grid + 1) * 4, cudaMemcpyHostToDevice,
+                           st));
+  p.recA.resize(std::max<uint64_t>(rec_n, 1) * p.aw);
+  p.kperm.resize(std::max<uint64_t>(rec_n, 1));
+  p.sk.resize(std::max<uint64_t>(key_n, 1));
+  if (!wd.empty()) {
+    DevBuf<uint32_t> dg(gstart.size()), db(dblk.size());
+    MKB_CUDA(cudaMemcpyAsync(dg.get(), gstart.data(), gstart.size() * 4, cudaMemcpyHostToDevice,
+                             st));
+    MKB_CUDA(cudaMemcpyAsync(db.get(), dblk.data(), dblk.size() * 4, cudaMemcpyHostToDevice, st));
+    FillArgs f{};
+    f.sp = sp;
+    f.outer = p.nout ? mc.idx[lv[0]].get() : nullptr;
+    f.cd = mc.idx[mode].get();
+    f.val = mc.val.get();
+    f.perm = perm.get();
+    f.wdesc = reinterpret_cast<const WDesc*>(p.wdesc.get());
+    f.gstart = dg.get();
+    f.dblk = db.get();
+    f.blks = reinterpret_cast<const Blk*>(p.blk_dev.get());
+    f.rowbits = p.rowbits;
+    f.b0 = p.b0;
+    f.aw = p.aw;
+    f.nin = nin;
+    f.gpw = GPW;
+    f.S = S;
+    f.RS = RS;
+    f.KS = KS;
+    f.recA = p.recA.get();
+    f.sk = p.sk.get();
+    f.kperm = p.kperm.get();
+    k_fill2<<<static_cast<unsigned>(wd.size()), 256, 0, st>>>(f);
+    MKB_LAUNCH();
+    MKB_CUDA(cudaStreamSynchronize(st));
+  }
+  // rows to pre-zero: empty rows + rows whose run crosses a group boundary
+  {
+    const uint64_t nempty = c.dims[mode] - mc.distinct;
+    p.n_zero_rows = p.blocked ? 0 : nempty + zero_rows.size();
+    p.zero_rows.resize(std::max<uint64_t>(p.n_zero_rows, 1));
+    if (!p.blocked) {
+      if (nempty)
+        MKB_CUDA(cudaMemcpyAsync(p.zero_rows.get(), mc.row_seq.get() + mc.distinct, nempty * 4,
+                                 cudaMemcpyDeviceToDevice, st));
+      if (!zero_rows.empty())
+        MKB_CUDA(cudaMemcpyAsync(p.zero_rows.get() + nempty, zero_rows.data(),
+                                 zero_rows.size() * 4, cudaMemcpyHostToDevice, st));
+    }
+  }
+  MKB_CUDA(cudaStreamSynchronize(st));  // temporaries are freed on return
+  if (env_int("MKB_DEBUG", 0))
+    std::fprintf(stderr,
+                 "[mkb] mode %u plan: levels %u%s nin %u aw %u %s blocks %u (split %u,%u,%u,%u) "
+                 "staged %u os %d smem %zu items %u records %llu zero_rows %llu\n",
+                 mode, ni, p.nout ? " (outer)" : "", nin, p.aw,
+                 kind == kBlocked ? "blocked" : (kind == kUnblocked ? "unblocked" : "partial"),
+                 p.nblocks, split[0], split[1], split[2], split[3], p.k, p.os ? 1 : 0,
+                 p.staged_end, p.nitems, static_cast<unsigned long long>(rec_n),
+                 static_cast<unsigned long long>(p.n_zero_rows));
+  p.ok = true;
+  return true;
+}
 
 bool launch_stream2(Context& c, uint32_t mode, const float* const* in, float* out) {
   if (!prepare_stream2(c, mode)) return false;
@@ -471,49 +578,31 @@ bool launch_stream2(Context& c, uint32_t mode, const float* const* in, float* ou
   ModeCopy::Stream2& p = mc.s2;
   cudaStream_t st = c.stream;
   const uint32_t G = c.rank / 4;
-  const uint32_t e0 = static_cast<uint32_t>(mc.shard_e0), e1 = static_cast<uint32_t>(mc.shard_e1);
-  const uint32_t e0a = e0 & ~3u;
-  const uint32_t wt = (32 / G) * s2::kS;
-  const bool staged = p.k > 0 || p.os;
-  const unsigned grid = static_cast<unsigned>(c.num_sms) * (staged ? 1u : 2u);
-  if (p.blocked) {
-    MKB_CUDA(cudaMemsetAsync(out, 0, static_cast<size_t>(c.dims[mode]) * c.rank * 4, st));
-  } else {
-    ensure_zero_list(c, mode, p.zl, s2::kS, wt, e0a, e0, e1);
-    if (p.zl.n) {
-      const unsigned blocks =
-          static_cast<unsigned>(std::min<uint64_t>(ceil_div(p.zl.n, 256 / G), c.num_sms * 8ull));
-      k_zero_rows2<<<blocks, 256, 0, st>>>(out, G, p.zl.rows.get(), p.zl.n);
+  if (mc.shard_e1 <= mc.shard_e0 || p.nitems == 0) {
+    // nothing to stream: only the rows the kernel would have zeroed
+    if (p.blocked) {
+      MKB_CUDA(cudaMemsetAsync(out, 0, static_cast<size_t>(c.dims[mode]) * c.rank * 4, st));
+    } else if (p.n_zero_rows) {
+      const unsigned blocks = static_cast<unsigned>(
+          std::min<uint64_t>(ceil_div(p.n_zero_rows, 256 / G), c.num_sms * 8ull));
+      k_zero_rows2<<<blocks, 256, 0, st>>>(out, G, p.zero_rows.get(), p.n_zero_rows);
       MKB_LAUNCH();
     }
-  }
-  if (e1 <= e0) return true;
-  if (p.grid != grid || !p.blk_dev.get()) {
-    // unblocked: one block spanning the owned range, tiles from e0 rounded down to 4
-    std::vector<uint32_t> blk = p.blk_host;
-    if (!p.blocked) {
-      Blk* bk = reinterpret_cast<Blk*>(blk.data());
-      bk->e0 = e0a;
-      bk->e1 = e1;
-    }
-    p.blk_dev.resize(blk.size());
-    MKB_CUDA(cudaMemcpyAsync(p.blk_dev.get(), blk.data(), blk.size() * 4, cudaMemcpyHostToDevice,
-                             st));
-    build_schedule(c, p, blk, p.blocked ? 0u : e0, grid, wt);
+    return true;
   }
   s2::Args a{};
   a.recA2 = reinterpret_cast<const uint2*>(p.recA.get());
   a.recA4 = reinterpret_cast<const uint4*>(p.recA.get());
-  a.sk = p.sk.get() + s2::kLeadB;
+  a.sk = p.sk.get();
   a.kperm = p.kperm.get();
   for (uint32_t l = 0; l < p.ni; ++l) a.Yg[l] = in[p.levels[l]];
   a.blks = reinterpret_cast<const Blk*>(p.blk_dev.get());
+  a.wdesc = reinterpret_cast<const WDesc*>(p.wdesc.get());
   a.items = reinterpret_cast<const Item*>(p.items.get());
   a.cta_items = p.cta_items.get();
   a.out = out;
   a.nonfinite = c.nonfinite.get();
   a.tag = static_cast<unsigned long long>(mode) << 32;
-  a.e1 = e1;
   a.rowbits = p.rowbits;
   a.rowmask = p.rowbits >= 32 ? 0xffffffffu : ((1u << p.rowbits) - 1u);
   a.asc_level = 0;
@@ -534,7 +623,16 @@ bool launch_stream2(Context& c, uint32_t mode, const float* const* in, float* ou
   a.outer_bytes = p.outer_bytes;
   a.records_off = static_cast<uint32_t>(p.staged_end);
   a.blocked = p.blocked ? 1u : 0u;
+  a.nitems = p.nitems;
+  a.zero_rows = p.zero_rows.get();
+  a.n_zero = static_cast<uint32_t>(p.blocked ? c.dims[mode] : p.n_zero_rows);
+  if (!c.s2sync.get()) {
+    c.s2sync.resize(4);
+    MKB_CUDA(cudaMemsetAsync(c.s2sync.get(), 0, 4 * sizeof(uint32_t), st));
+  }
+  a.sync = c.s2sync.get();
   const size_t se = p.staged_end;
+  const unsigned grid = p.grid;
   switch (c.n * 100 + G) {
     case 308: stream2_launch_n3_g8(a, p.nout, p.os, p.k, grid, se, st); break;
     case 316: stream2_launch_n3_g16(a, p.nout, p.os, p.k, grid, se, st); break;
