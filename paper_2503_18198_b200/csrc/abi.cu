@@ -413,10 +413,7 @@ int mk_sweep_host(mk_context* ctx, const float* const* factors, float* const* ou
 int mk_flush_l2(mk_context* ctx) {
   return guarded([&] {
     need_ctx(ctx);
-    Context& c = ctx->c;
-    const size_t bytes = std::max<size_t>(2 * c.l2_bytes, 64u << 20);
-    c.flush_buf.resize(bytes);
-    MKB_CUDA(cudaMemsetAsync(c.flush_buf.get(), 0x5a, bytes, c.stream));
+    flush_l2(ctx->c);
   });
 }
 

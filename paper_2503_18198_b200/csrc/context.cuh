@@ -56,6 +56,12 @@ struct ModeCopy {
     uint64_t key_seg = 0, key_tile = 0, key_e0 = ~0ull, key_e1 = ~0ull;
   };
   ZeroList zl_stream, zl_tiles;
+  // fast-path kernel chosen for this copy by a one-time timing of the candidates
+  // (mttkrp.cu): -1 undecided, 0 level-ordered streaming kernel, 1 fiber-ordered streaming
+  // kernel, 2 generic tile kernel; keyed by factor rank and shard range
+  int fast_kernel = -1;
+  uint32_t fast_rank = 0;
+  uint64_t fast_e0 = ~0ull, fast_e1 = ~0ull;
   // level-ordered, shared-memory-blocked records of the streaming kernel (stream2_plan.cu),
   // built per (factor rank, shard range) on first use
   struct Stream2 {
@@ -157,6 +163,10 @@ void als_update_mode(Context& c, uint32_t d);
 void als_fit(Context& c, double* fit, float* lambda_host);
 // Streaming TMA kernel (stream.cu); false when the shape has no specialisation.
 bool launch_stream(Context& c, uint32_t mode, const float* const* in, float* out);
+bool prepare_stream(Context& c, uint32_t mode);  // builds its records; false: no specialisation
+// Fast-path kernel selection (mttkrp.cu): 0 level-ordered, 1 fiber-ordered, 2 tiles.
+int choose_fast_kernel(Context& c, uint32_t mode, const float* const* in, float* out);
+void flush_l2(Context& c);  // write 2x the L2 size on the context's stream
 void pack_records(Context& c, uint32_t mode, const uint32_t* rank_of_row);
 // v2 level-ordered streaming kernel (stream2_plan.cu): records built per factor rank on first
 // use (or eagerly by prepare_stream2); false when the shape has no specialisation.

@@ -24,6 +24,10 @@
 // order is also element order.
 #include <algorithm>
 
+#include <cstdio>
+#include <cstdlib>
+#include <string>
+
 #include "context.cuh"
 
 namespace mkb {
@@ -360,9 +364,60 @@ void reset_nonfinite(Context& c) {
   MKB_LAUNCH();
 }
 
+void flush_l2(Context& c) {
+  const size_t bytes = std::max<size_t>(2 * c.l2_bytes, 64u << 20);
+  c.flush_buf.resize(bytes);
+  MKB_CUDA(cudaMemsetAsync(c.flush_buf.get(), 0x5a, bytes, c.stream));
+}
+
+// The fast path has two streaming kernels whose relative speed depends on the shape
+// (level-ordered + shared-memory staged vs fiber-ordered + L1/L2 gathers; see DESIGN.md
+// §4.2).  The first fast launch of a mode times each applicable candidate on the actual
+// inputs (after one warm-up launch each, L2 flushed in between) and keeps the fastest;
+// MKB_FAST_KERNEL = s2 | stream | tiles forces one.
+int choose_fast_kernel(Context& c, uint32_t mode, const float* const* in, float* out) {
+  ModeCopy& mc = c.copies[mode];
+  if (mc.fast_kernel >= 0 && mc.fast_rank == c.rank && mc.fast_e0 == mc.shard_e0 &&
+      mc.fast_e1 == mc.shard_e1)
+    return mc.fast_kernel;
+  mc.fast_rank = c.rank;
+  mc.fast_e0 = mc.shard_e0;
+  mc.fast_e1 = mc.shard_e1;
+  const char* e = std::getenv("MKB_FAST_KERNEL");
+  const std::string force = e ? e : "";
+  const bool s2_ok = force != "stream" && force != "tiles" && prepare_stream2(c, mode);
+  const bool st_ok = force != "s2" && force != "tiles" && prepare_stream(c, mode);
+  if (!s2_ok && !st_ok) return mc.fast_kernel = 2;
+  if (!st_ok) return mc.fast_kernel = 0;
+  if (!s2_ok) return mc.fast_kernel = 1;
+  cudaStream_t st = c.stream;
+  cudaEvent_t ev[3];
+  for (auto& x : ev) MKB_CUDA(cudaEventCreate(&x));
+  float ms[2] = {0.f, 0.f};
+  for (int k = 0; k < 2; ++k) {
+    auto run = [&] { k == 0 ? launch_stream2(c, mode, in, out) : launch_stream(c, mode, in, out); };
+    run();  // warm-up: one-time launch setup, L1/L2 state
+    flush_l2(c);
+    MKB_CUDA(cudaEventRecord(ev[0], st));
+    run();
+    MKB_CUDA(cudaEventRecord(ev[1], st));
+    MKB_CUDA(cudaEventSynchronize(ev[1]));
+    MKB_CUDA(cudaEventElapsedTime(&ms[k], ev[0], ev[1]));
+  }
+  for (auto& x : ev) MKB_CUDA(cudaEventDestroy(x));
+  mc.fast_kernel = ms[1] < ms[0] ? 1 : 0;
+  if (std::getenv("MKB_DEBUG"))
+    std::fprintf(stderr, "[mkb] mode %u fast kernel: level-ordered %.1f us, fiber-ordered %.1f us -> %s\n",
+                 mode, ms[0] * 1e3, ms[1] * 1e3, mc.fast_kernel ? "fiber-ordered" : "level-ordered");
+  return mc.fast_kernel;
+}
+
 void launch_mttkrp(Context& c, uint32_t mode, const float* const* in, float* out, int exec) {
-  if (exec == MK_EXEC_FAST && (launch_stream2(c, mode, in, out) || launch_stream(c, mode, in, out)))
-    return;
+  if (exec == MK_EXEC_FAST) {
+    const int k = choose_fast_kernel(c, mode, in, out);
+    if (k == 0 && launch_stream2(c, mode, in, out)) return;
+    if (k == 1 && launch_stream(c, mode, in, out)) return;
+  }
   ModeCopy& mc = c.copies[mode];
   MttkrpArgs a{};
   uint32_t ni = 0;

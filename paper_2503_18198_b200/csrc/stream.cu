@@ -550,7 +550,7 @@ bool launch_stream_ni(Context& c, ModeCopy& mc, uint32_t mode, const float* cons
 
 }  // namespace
 
-bool launch_stream(Context& c, uint32_t mode, const float* const* in, float* out) {
+bool prepare_stream(Context& c, uint32_t mode) {
   ModeCopy& mc = c.copies[mode];
   if (c.n < 3 || c.n > 5 || c.nnz == 0) return false;
   if (c.rank != 16 && c.rank != 32 && c.rank != 64 && c.rank != 128) return false;
@@ -559,7 +559,12 @@ bool launch_stream(Context& c, uint32_t mode, const float* const* in, float* out
     rank_of_row_build(c, mode, rank);
     pack_records(c, mode, rank.get());
   }
-  if (!mc.recA.get()) return false;
+  return mc.recA.get() != nullptr;
+}
+
+bool launch_stream(Context& c, uint32_t mode, const float* const* in, float* out) {
+  ModeCopy& mc = c.copies[mode];
+  if (!prepare_stream(c, mode)) return false;
   switch (c.n) {
     case 3: return launch_stream_ni<2>(c, mc, mode, in, out);
     case 4: return launch_stream_ni<3>(c, mc, mode, in, out);

@@ -310,7 +310,11 @@ bool prepare_stream2(Context& c, uint32_t mode) {
       for (uint32_t j = 0; j < nin; ++j) nb *= split[j];
     }
     // blocks must amortise their staging: <= 32 B of slices per element on average
-    if (slices_bytes() <= budget && nb <= 4096 && nb * slices_bytes() <= 32ull * nnz) {
+    // Blocks must amortise their staging (<= 32 B of slices per element on average), and
+    // the rows they cut must stay long: every (block, row) pair costs one atomic flush, so
+    // blocks x rows must stay below nnz / 16.
+    if (slices_bytes() <= budget && nb <= 4096 && nb * slices_bytes() <= 32ull * nnz &&
+        nb * std::max<uint64_t>(mc.distinct, 1) * 16 <= nnz) {
       kind = kBlocked;
       p.nblocks = static_cast<uint32_t>(nb);
     }
