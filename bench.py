@@ -362,7 +362,8 @@ def our_arm(args, cfg, rank, world, local_rank):
     kern_ms = float(mode_ms.sum(axis=1).mean())
     achieved = b_iter / (kern_ms * 1e-3) / 1e9
     traffic = ncu_traffic(args.config)
-    launches_per_mode = 2  # zero-rows kernel + spMTTKRP kernel
+    fast = [ctx.fast_path_info(d).as_dict() for d in range(n)]
+    launches_per_sweep = sum(f["launches"] for f in fast)
     line = {
         "metric": METRIC, "value": ms, "unit": "ms", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False, "scaling": "strong",
@@ -376,10 +377,11 @@ def our_arm(args, cfg, rank, world, local_rank):
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
                      "algorithmic_bytes_per_sweep": b_iter,
-                     "kernel": "k_mttkrp_tiles (all modes)", "kernel_ms_per_sweep": kern_ms},
+                     "kernel": sorted({f["kernel"] for f in fast}), "kernel_ms_per_sweep": kern_ms,
+                     "per_mode": fast},
         "e2e": {"value": e2e_ms, "unit": "ms", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": h2d, "path": "mk_sweep_host (C ABI), pinned host buffers"},
-        "gpu_launches": (launches_per_mode + (2 if ex is not None else 0)) * n * args.steps,
+        "gpu_launches": (launches_per_sweep + (2 * n if ex is not None else 0)) * args.steps,
         "allgather_bytes_per_sweep": ex.bytes_per_sweep() if ex is not None else 0,
         "clocks": clk.summary(),
         "per_mode_ms": mode_ms.mean(axis=0).tolist(),

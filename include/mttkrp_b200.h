@@ -57,6 +57,19 @@ typedef struct {
   uint64_t device_bytes;   /* bytes of the materialised mode copy on the device */
 } mk_plan_info;
 
+/* How the fast path (MK_EXEC_FAST) runs one mode copy: which streaming kernel the one-time
+ * timing chose and the level-ordered kernel's shared-memory plan. */
+typedef struct {
+  int kernel;               /* 0 level-ordered streaming, 1 fiber-ordered streaming,
+                               2 generic tiles, -1 not chosen yet (no fast launch so far) */
+  int blocked;              /* level-ordered: copy split into shared-memory blocks */
+  uint32_t blocks;          /* level-ordered: blocks (1 when unblocked) */
+  uint32_t staged_levels;   /* level-ordered: inner levels staged in shared memory */
+  int outer_level;          /* level-ordered: outermost input level kept in registers */
+  uint32_t launches;        /* kernel launches per fast call of this mode */
+  uint64_t stream_bytes;    /* bytes streamed from HBM per call (records + slow keys) */
+} mk_fast_info;
+
 /* ---- library / context ------------------------------------------------------------ */
 const char* mk_last_error(void);
 const char* mk_version(void);
@@ -85,6 +98,8 @@ int mk_tensor_norm2(mk_context* ctx, double* norm2);
  * in that mode's order. */
 int mk_build_plans(mk_context* ctx, uint64_t kappa, int strategy, int policy);
 int mk_get_plan_info(mk_context* ctx, uint32_t mode, mk_plan_info* info);
+/* Fast-path kernel choice and plan of a mode copy (valid after a fast launch). */
+int mk_fast_path_info(mk_context* ctx, uint32_t mode, mk_fast_info* info);
 /* ModePlan export (layout.hpp:47-64): order[nnz], partition_offsets[kappa+1],
  * owned_flat[owned_total] (concatenated owned_indices), owned_offsets[kappa+1].
  * Any output pointer may be NULL to skip it. */

@@ -51,7 +51,7 @@ EXEC_FAST, EXEC_DETERMINISTIC = 0, 1
 EXPORTED_SYMBOLS = [
     "mk_last_error", "mk_version", "mk_device_count", "mk_create", "mk_destroy",
     "mk_set_stream", "mk_synchronize", "mk_tensor_upload", "mk_tensor_norm2",
-    "mk_build_plans", "mk_get_plan_info", "mk_plan_export", "mk_mode_degrees",
+    "mk_build_plans", "mk_get_plan_info", "mk_fast_path_info", "mk_plan_export", "mk_mode_degrees",
     "mk_copy_export", "mk_factors_upload", "mk_factor_upload", "mk_factor_download",
     "mk_mttkrp_mode", "mk_mttkrp_all_modes", "mk_sweep_async", "mk_mttkrp_mode_async",
     "mk_output_download",
@@ -92,6 +92,22 @@ class _PlanInfo(C.Structure):
                 ("split_rows", C.c_uint64), ("device_bytes", C.c_uint64)]
 
 
+class _FastInfo(C.Structure):
+    """mk_fast_info: the fast path's kernel choice and plan for one mode copy."""
+    _fields_ = [("kernel", C.c_int), ("blocked", C.c_int), ("blocks", C.c_uint32),
+                ("staged_levels", C.c_uint32), ("outer_level", C.c_int),
+                ("launches", C.c_uint32), ("stream_bytes", C.c_uint64)]
+
+    KERNELS = {-1: "undecided", 0: "k_stream2 (level-ordered)", 1: "k_mttkrp_stream (fiber-ordered)",
+               2: "k_mttkrp_tiles"}
+
+    def as_dict(self):
+        return {"kernel": self.KERNELS.get(self.kernel, str(self.kernel)), "blocked": bool(self.blocked),
+                "blocks": int(self.blocks), "staged_levels": int(self.staged_levels),
+                "outer_level": bool(self.outer_level), "launches": int(self.launches),
+                "stream_bytes": int(self.stream_bytes)}
+
+
 _lib_lock = threading.Lock()
 _lib_handle: Optional[C.CDLL] = None
 
@@ -125,6 +141,7 @@ def load_library() -> C.CDLL:
             "mk_tensor_norm2": (i32, [vp, P(C.c_double)]),
             "mk_build_plans": (i32, [vp, u64, i32, i32]),
             "mk_get_plan_info": (i32, [vp, u32, P(_PlanInfo)]),
+            "mk_fast_path_info": (i32, [vp, u32, P(_FastInfo)]),
             "mk_plan_export": (i32, [vp, u32, vp, vp, vp, vp]),
             "mk_mode_degrees": (i32, [vp, u32, vp]),
             "mk_copy_export": (i32, [vp, u32, vp, vp]),
@@ -339,6 +356,11 @@ class Context:
     def plan_info(self, mode: int) -> _PlanInfo:
         info = _PlanInfo()
         _check(self.lib.mk_get_plan_info(self.h, mode, C.byref(info)))
+        return info
+
+    def fast_path_info(self, mode: int) -> _FastInfo:
+        info = _FastInfo()
+        _check(self.lib.mk_fast_path_info(self.h, mode, C.byref(info)))
         return info
 
     def plan_export(self, mode: int):

@@ -191,6 +191,39 @@ int mk_get_plan_info(mk_context* ctx, uint32_t mode, mk_plan_info* info) {
   });
 }
 
+int mk_fast_path_info(mk_context* ctx, uint32_t mode, mk_fast_info* info) {
+  return guarded([&] {
+    need_ctx(ctx);
+    Context& c = ctx->c;
+    need_plans(c);
+    need_mode(c, mode);
+    if (!info) fail(MK_EINVAL, "null info");
+    const ModeCopy& mc = c.copies[mode];
+    const bool decided = mc.fast_kernel >= 0 && mc.fast_rank == c.rank;
+    *info = mk_fast_info{};
+    info->kernel = decided ? mc.fast_kernel : -1;
+    const ModeCopy::Stream2& p = mc.s2;
+    if (p.ok) {
+      info->blocked = p.blocked ? 1 : 0;
+      info->blocks = p.nblocks;
+      info->staged_levels = p.k;
+      info->outer_level = p.nout ? 1 : 0;
+    }
+    if (info->kernel == 0) {
+      info->launches = 1;  // pre-zeroing runs inside the streaming kernel
+      info->stream_bytes = p.recA.bytes() + p.sk.bytes();
+    } else if (info->kernel == 1) {
+      info->launches = 2;  // split-row pre-zeroing + streaming kernel
+      info->stream_bytes = mc.recA.bytes() + mc.recB.bytes();
+    } else if (info->kernel == 2) {
+      info->launches = 2;
+      uint64_t b = mc.val.bytes();
+      for (uint32_t w = 0; w < c.n; ++w) b += mc.idx[w].bytes();
+      info->stream_bytes = b;
+    }
+  });
+}
+
 int mk_plan_export(mk_context* ctx, uint32_t mode, uint64_t* order, uint64_t* partition_offsets,
                    uint32_t* owned_flat, uint64_t* owned_offsets) {
   return guarded([&] {
