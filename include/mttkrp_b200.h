@@ -100,6 +100,10 @@ int mk_build_plans(mk_context* ctx, uint64_t kappa, int strategy, int policy);
 int mk_get_plan_info(mk_context* ctx, uint32_t mode, mk_plan_info* info);
 /* Fast-path kernel choice and plan of a mode copy (valid after a fast launch). */
 int mk_fast_path_info(mk_context* ctx, uint32_t mode, mk_fast_info* info);
+/* Force the fast path's kernel for every mode (0 level-ordered, 1 fiber-ordered, 2 generic
+ * tiles) or restore the one-time timed choice (-1).  A forced kernel that has no
+ * specialisation for the shape falls back along 0 -> 1 -> 2. */
+int mk_set_fast_kernel(mk_context* ctx, int kernel);
 /* ModePlan export (layout.hpp:47-64): order[nnz], partition_offsets[kappa+1],
  * owned_flat[owned_total] (concatenated owned_indices), owned_offsets[kappa+1].
  * Any output pointer may be NULL to skip it. */

@@ -51,7 +51,7 @@ EXEC_FAST, EXEC_DETERMINISTIC = 0, 1
 EXPORTED_SYMBOLS = [
     "mk_last_error", "mk_version", "mk_device_count", "mk_create", "mk_destroy",
     "mk_set_stream", "mk_synchronize", "mk_tensor_upload", "mk_tensor_norm2",
-    "mk_build_plans", "mk_get_plan_info", "mk_fast_path_info", "mk_plan_export", "mk_mode_degrees",
+    "mk_build_plans", "mk_get_plan_info", "mk_fast_path_info", "mk_set_fast_kernel", "mk_plan_export", "mk_mode_degrees",
     "mk_copy_export", "mk_factors_upload", "mk_factor_upload", "mk_factor_download",
     "mk_mttkrp_mode", "mk_mttkrp_all_modes", "mk_sweep_async", "mk_mttkrp_mode_async",
     "mk_output_download",
@@ -142,6 +142,7 @@ def load_library() -> C.CDLL:
             "mk_build_plans": (i32, [vp, u64, i32, i32]),
             "mk_get_plan_info": (i32, [vp, u32, P(_PlanInfo)]),
             "mk_fast_path_info": (i32, [vp, u32, P(_FastInfo)]),
+            "mk_set_fast_kernel": (i32, [vp, i32]),
             "mk_plan_export": (i32, [vp, u32, vp, vp, vp, vp]),
             "mk_mode_degrees": (i32, [vp, u32, vp]),
             "mk_copy_export": (i32, [vp, u32, vp, vp]),
@@ -362,6 +363,10 @@ class Context:
         info = _FastInfo()
         _check(self.lib.mk_fast_path_info(self.h, mode, C.byref(info)))
         return info
+
+    def set_fast_kernel(self, kernel: int):
+        """Force the fast path's kernel (0 level-ordered, 1 fiber-ordered, 2 tiles; -1 = timed choice)."""
+        _check(self.lib.mk_set_fast_kernel(self.h, int(kernel)))
 
     def plan_export(self, mode: int):
         info = self.plan_info(mode)

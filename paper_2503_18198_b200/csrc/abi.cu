@@ -224,6 +224,16 @@ int mk_fast_path_info(mk_context* ctx, uint32_t mode, mk_fast_info* info) {
   });
 }
 
+int mk_set_fast_kernel(mk_context* ctx, int kernel) {
+  return guarded([&] {
+    need_ctx(ctx);
+    if (kernel < -1 || kernel > 2) fail(MK_EINVAL, "kernel: fast kernel must be -1, 0, 1 or 2");
+    Context& c = ctx->c;
+    c.force_fast_kernel = kernel;
+    for (uint32_t d = 0; d < kMaxModes; ++d) c.copies[d].fast_kernel = -1;  // re-choose
+  });
+}
+
 int mk_plan_export(mk_context* ctx, uint32_t mode, uint64_t* order, uint64_t* partition_offsets,
                    uint32_t* owned_flat, uint64_t* owned_offsets) {
   return guarded([&] {

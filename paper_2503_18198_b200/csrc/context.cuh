@@ -124,6 +124,7 @@ struct Context {
   // device scalars: [0] = min non-finite copy position (uint64, ~0 = none), [1] = mode
   DevBuf<unsigned long long> nonfinite;
   DevBuf<uint8_t> flush_buf;
+  int force_fast_kernel = -1;  // mk_set_fast_kernel: -1 timed choice, else 0 / 1 / 2
   DevBuf<uint32_t> s2sync;  // streaming kernel: finished-CTA counter + non-finite flag
   SortScratch scratch;
 

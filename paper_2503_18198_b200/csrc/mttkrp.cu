@@ -384,12 +384,15 @@ int choose_fast_kernel(Context& c, uint32_t mode, const float* const* in, float*
   mc.fast_e0 = mc.shard_e0;
   mc.fast_e1 = mc.shard_e1;
   const char* e = std::getenv("MKB_FAST_KERNEL");
-  const std::string force = e ? e : "";
+  std::string force = e ? e : "";
+  if (c.force_fast_kernel >= 0) force = c.force_fast_kernel == 0 ? "s2" : (c.force_fast_kernel == 1 ? "stream" : "tiles");
   const bool s2_ok = force != "stream" && force != "tiles" && prepare_stream2(c, mode);
   const bool st_ok = force != "s2" && force != "tiles" && prepare_stream(c, mode);
   if (!s2_ok && !st_ok) return mc.fast_kernel = 2;
   if (!st_ok) return mc.fast_kernel = 0;
   if (!s2_ok) return mc.fast_kernel = 1;
+  if (force == "s2") return mc.fast_kernel = 0;
+  if (force == "stream") return mc.fast_kernel = 1;
   cudaStream_t st = c.stream;
   cudaEvent_t ev[3];
   for (auto& x : ev) MKB_CUDA(cudaEventCreate(&x));

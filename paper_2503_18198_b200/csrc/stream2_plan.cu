@@ -279,71 +279,89 @@ bool prepare_stream2(Context& c, uint32_t mode) {
   const uint32_t nin = ni - p.nout;
   p.aw = nin <= 2 ? 2u : 4u;
 
-  // 3. staging plan
+  // 3. staging plan: enumerate (level order, K innermost levels staged, block split of the
+  //    staged levels) and keep the candidate with the lowest modelled cost per element, in
+  //    SM-cycles (constants measured on B200: tools/ubench_lsu.cu, tools/ubench_chain.cu,
+  //    profiles/r01_ncu_full_cfg5_k_stream2.txt):
+  //      LSU   = 0.94 per 128-B row gathered (shared or L1) + the record read
+  //      L2    = bytes gathered from L2 / 45 B per SM-cycle: L2-fed gathers are latency-bound
+  //              at 16 warps, so they add to the LSU time (L1 hit rate ~ free L1 / factor)
+  //      flush = 32 per atomic row flush: every (block, row) pair of a blocked plan
+  //      stage = per CTA item: staged slice bytes / 85 B per SM-cycle + a ~6000-cycle stall
+  //    cost = LSU + L2 + flush + stage (fitted to the measured cfg2 / cfg3 / cfg5 plans).
   const size_t ring = s2::ring_bytes_rt(p.aw, G, 512);
   size_t budget = s2::kMaxDynSmem - ring - 256;
   const bool stage_on = env_int("MKB_STAGE", 1) != 0;
   const bool block_on = env_int("MKB_BLOCK", 1) != 0 && !sharded;
   p.os = stage_on && p.nout && fbytes(lv[0]) <= std::min<size_t>(32u << 10, budget / 4);
   if (p.os) budget -= align128(fbytes(lv[0]));
-  uint32_t rows[4] = {1, 1, 1, 1}, split[4] = {1, 1, 1, 1};
-  for (uint32_t j = 0; j < nin; ++j) rows[j] = c.dims[lv[p.nout + j]];
-  auto slices_bytes = [&] {
-    size_t b = 0;
-    for (uint32_t j = 0; j < nin; ++j) b += align128(static_cast<size_t>(rows[j]) * rowbytes);
-    return b;
-  };
-  enum { kUnblocked, kBlocked, kPartial } kind = kPartial;
-  if (stage_on && slices_bytes() <= budget) {
-    kind = kUnblocked;
-  } else if (stage_on && block_on) {
-    // greedy: split the slot with the largest slice until every slice fits
+  const double kRow = 0.94 * (rowbytes / 128.0), kRec = (p.aw == 2 ? 1.5 : 2.5) * G / 32.0;
+  const double kL2 = 85.0, kL2Gather = 45.0, kFlush = 32.0;
+  struct Cand {
+    bool swap = false;
+    uint32_t k = 0, rows[4] = {1, 1, 1, 1}, split[4] = {1, 1, 1, 1};
     uint64_t nb = 1;
-    while (slices_bytes() > budget && nb <= 4096) {
-      uint32_t jm = 0;
-      for (uint32_t j = 1; j < nin; ++j)
-        if (rows[j] > rows[jm]) jm = j;
-      const uint32_t ext = c.dims[lv[p.nout + jm]];
-      split[jm] += 1;
-      rows[jm] = (ext + split[jm] - 1) / split[jm];
-      nb = 1;
-      for (uint32_t j = 0; j < nin; ++j) nb *= split[j];
-    }
-    // blocks must amortise their staging: <= 32 B of slices per element on average
-    // Blocks must amortise their staging (<= 32 B of slices per element on average), and
-    // the rows they cut must stay long: every (block, row) pair costs one atomic flush, so
-    // blocks x rows must stay below nnz / 16.
-    if (slices_bytes() <= budget && nb <= 4096 && nb * slices_bytes() <= 32ull * nnz &&
-        nb * std::max<uint64_t>(mc.distinct, 1) * 16 <= nnz) {
-      kind = kBlocked;
-      p.nblocks = static_cast<uint32_t>(nb);
+    double cost = 1e30;
+  } best;
+  for (int sw = 0; sw < (nin >= 2 ? 2 : 1); ++sw) {
+    std::vector<uint32_t> lo = lv;
+    if (sw) std::swap(lo[ni - 1], lo[ni - 2]);
+    for (uint32_t k = stage_on ? nin : 0;; --k) {
+      Cand cd;
+      cd.swap = sw != 0;
+      cd.k = k;
+      for (uint32_t j = 0; j < nin; ++j) cd.rows[j] = c.dims[lo[p.nout + j]];
+      auto staged_bytes = [&] {
+        size_t b = 0;
+        for (uint32_t j = nin - k; j < nin; ++j)
+          b += align128(static_cast<size_t>(cd.rows[j]) * rowbytes);
+        return b;
+      };
+      bool ok = true;
+      while (staged_bytes() > budget) {  // greedy: split the staged slot with the largest slice
+        if (!block_on) { ok = false; break; }
+        uint32_t jm = nin - k;
+        for (uint32_t j = nin - k + 1; j < nin; ++j)
+          if (cd.rows[j] > cd.rows[jm]) jm = j;
+        const uint32_t ext = c.dims[lo[p.nout + jm]];
+        cd.split[jm] += 1;
+        cd.rows[jm] = (ext + cd.split[jm] - 1) / cd.split[jm];
+        cd.nb = 1;
+        for (uint32_t j = 0; j < nin; ++j) cd.nb *= cd.split[j];
+        if (cd.nb > 4096) { ok = false; break; }
+      }
+      if (ok) {
+        const double free_l1 = std::max(32.0 * 1024, 256.0 * 1024 - staged_bytes() - ring);
+        double lsu = nin * kRow + kRec, l2 = 0;
+        for (uint32_t j = 0; j < nin - k; ++j) {
+          const double hit = std::min(0.3, free_l1 / static_cast<double>(fbytes(lo[p.nout + j])));
+          l2 += (1.0 - hit) * rowbytes / kL2Gather;
+        }
+        const double flushes =
+            cd.nb > 1 ? std::min<double>(nnz, static_cast<double>(cd.nb) *
+                                                  std::max<uint64_t>(mc.distinct, 1))
+                      : 0.0;
+        // every CTA item restages: bandwidth + a ~6000-cycle stall (barrier + TMA round trip)
+        const double stage =
+            static_cast<double>(c.num_sms + cd.nb) * (staged_bytes() / kL2 + (k ? 6000.0 : 0.0));
+        cd.cost = lsu + l2 + (kFlush * flushes + stage) / static_cast<double>(nnz);
+        // prefer the simpler plan (fewer blocks, no swap) within 3%
+        if (cd.cost < best.cost * (cd.nb < best.nb ? 1.03 : 0.97)) best = cd;
+      }
+      if (k == 0) break;
     }
   }
-  if (kind != kBlocked) {
-    for (uint32_t j = 0; j < nin; ++j) {
-      rows[j] = c.dims[lv[p.nout + j]];
-      split[j] = 1;
-    }
-    p.nblocks = 1;
+  if (best.swap) std::swap(lv[ni - 1], lv[ni - 2]);
+  uint32_t rows[4], split[4];
+  for (uint32_t j = 0; j < 4; ++j) {
+    rows[j] = best.rows[j];
+    split[j] = best.split[j];
   }
-  p.k = 0;
-  if (kind == kPartial && stage_on) {
-    // the largest inner level may not fit while the second largest does: make the
-    // stageable one innermost
-    if (nin >= 2 && fbytes(lv[ni - 1]) > budget && fbytes(lv[ni - 2]) <= budget)
-      std::swap(lv[ni - 1], lv[ni - 2]);
-    for (uint32_t j = 0; j < nin; ++j) rows[j] = c.dims[lv[p.nout + j]];
-    size_t used = 0;
-    for (int j = static_cast<int>(nin) - 1; j >= 0; --j) {
-      const size_t b = align128(static_cast<size_t>(rows[j]) * rowbytes);
-      if (used + b > budget) break;
-      used += b;
-      ++p.k;
-    }
-  } else if (kind != kPartial) {
-    p.k = nin;
-  }
-  p.blocked = kind == kBlocked;
+  p.k = best.k;
+  p.nblocks = static_cast<uint32_t>(best.nb);
+  p.blocked = best.nb > 1;
+  const char* kind = p.blocked ? "blocked" : (p.k == nin ? "unblocked" : "partial");
+  const double model_cost = best.cost;
   for (uint32_t l = 0; l < ni; ++l) p.levels[l] = lv[l];
   // shared-memory layout: staged inner slots (slot order), outer factor, record rings
   {
@@ -566,12 +584,12 @@ bool prepare_stream2(Context& c, uint32_t mode) {
   if (env_int("MKB_DEBUG", 0))
     std::fprintf(stderr,
                  "[mkb] mode %u plan: levels %u%s nin %u aw %u %s blocks %u (split %u,%u,%u,%u) "
-                 "staged %u os %d smem %zu items %u records %llu zero_rows %llu\n",
+                 "staged %u os %d smem %zu items %u records %llu zero_rows %llu model %.2f cyc/elem\n",
                  mode, ni, p.nout ? " (outer)" : "", nin, p.aw,
-                 kind == kBlocked ? "blocked" : (kind == kUnblocked ? "unblocked" : "partial"),
+                 kind,
                  p.nblocks, split[0], split[1], split[2], split[3], p.k, p.os ? 1 : 0,
                  p.staged_end, p.nitems, static_cast<unsigned long long>(rec_n),
-                 static_cast<unsigned long long>(p.n_zero_rows));
+                 static_cast<unsigned long long>(p.n_zero_rows), model_cost);
   p.ok = true;
   return true;
 }

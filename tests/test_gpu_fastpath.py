@@ -1,0 +1,151 @@
+"""GPU: every fast-path kernel and every staging plan of the level-ordered kernel against the
+oracle (oracle_mttkrp, oracle.hpp:20-43), through the C ABI.
+
+The fast path chooses per mode between the level-ordered streaming kernel (k_stream2: shared
+memory staged whole / in blocks / partially, outer level in registers) and the fiber-ordered
+streaming kernel (k_mttkrp_stream), or falls back to the generic tile kernel.  Each kernel is
+forced here with mk_set_fast_kernel and must match the oracle on shapes chosen so that each
+plan kind occurs.  Tolerance: BASELINE's 1e-4 relative (north star).  These rows hold up to
+~8 K signed values (cancellation, as in support.hpp:31-59), and every kernel sums them in a
+different association than the reference's sequential loop.  The reference's own parallel
+Scheme 2 drifts ~5e-6 on far shorter rows.
+"""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+# (dims, nnz, rank, expected level-ordered plan kinds of some mode)
+SHAPES = [
+    ([183, 24, 1140, 1717], 200_000, 32, {"unblocked", "blocked"}),   # uber-like: outer level
+    ([1000, 1000, 1000], 1_000_000, 32, {"blocked"}),                 # cfg1: two 128 KB factors
+    ([6000, 9000, 30000], 400_000, 32, {"blocked", "partial"}),       # big factors
+    ([300, 400, 500, 600, 700], 100_000, 32, {"unblocked", "blocked", "partial"}),  # N=5: 16-B records
+    ([2482, 2862, 5000, 17], 150_000, 64, {"blocked", "partial"}),    # R=64 (16-lane groups)
+    ([40, 50, 60], 20_000, 64, {"partial"}),  # tiny: staging does not pay (cost model)
+]
+
+
+def plan_kind(info):
+    if info.blocked:
+        return "blocked"
+    return "partial" if info.kernel == 0 and info.staged_levels == 0 else "unblocked"
+
+
+def run(mk, t, f, kernel):
+    c = mk.Context()
+    c.upload_tensor(t)
+    c.build_plans(148)
+    c.upload_factors(f)
+    c.set_fast_kernel(kernel)
+    outs = c.mttkrp_all_modes(False, False)
+    infos = [c.fast_path_info(d) for d in range(t.mode_count())]
+    return outs, infos
+
+
+@pytest.mark.parametrize("shape", range(len(SHAPES)))
+@pytest.mark.parametrize("kernel", [0, 1, 2])
+def test_forced_kernel_matches_oracle(mk, orc, shape, kernel):
+    dims, nnz, R, _ = SHAPES[shape]
+    t = mk.generate_synthetic(dims, nnz, seed=shape + 3)
+    g = np.random.default_rng(shape)
+    sign = np.where(g.integers(0, 2, size=t.nnz) == 1, 1, -1).astype(np.float32)
+    t = mk.SparseTensorCOO(dims, t.coords, t.values * sign)  # cancellation, like support.hpp:31-59
+    f = [m.data for m in mk.random_factors(dims, R, 7)]
+    outs, infos = run(mk, t, f, kernel)
+    for d in range(len(dims)):
+        assert infos[d].kernel == kernel
+        want = orc.mttkrp(dims, t.coords, t.values, f, d)
+        err = mk.verify_against(outs[d], want)[0]
+        assert err <= 1e-4, (dims, R, kernel, d, err, infos[d].as_dict())
+
+
+@pytest.mark.parametrize("shape", range(len(SHAPES)))
+def test_level_ordered_plan_kinds(mk, shape):
+    """The shapes above exercise the plan kinds they are listed with."""
+    dims, nnz, R, kinds = SHAPES[shape]
+    t = mk.generate_synthetic(dims, nnz, seed=shape + 3)
+    f = [m.data for m in mk.random_factors(dims, R, 7)]
+    _, infos = run(mk, t, f, 0)
+    seen = {plan_kind(i) for i in infos}
+    assert seen & kinds, (seen, kinds, [i.as_dict() for i in infos])
+    for i in infos:
+        assert i.launches == 1  # pre-zeroing runs inside the streaming kernel
+        assert i.blocks >= 1 and (i.blocks > 1) == bool(i.blocked)
+
+
+def test_timed_choice_is_one_of_the_kernels_and_stable(mk, orc):
+    dims = [183, 24, 1140, 1717]
+    t = mk.generate_synthetic(dims, 200_000, seed=1)
+    f = [m.data for m in mk.random_factors(dims, 32, 1)]
+    c = mk.Context()
+    c.upload_tensor(t)
+    c.build_plans(148)
+    c.upload_factors(f)
+    a = c.mttkrp_all_modes(False, False)
+    first = [c.fast_path_info(d).kernel for d in range(4)]
+    assert all(k in (0, 1) for k in first)
+    b = c.mttkrp_all_modes(False, False)
+    assert [c.fast_path_info(d).kernel for d in range(4)] == first
+    for d in range(4):
+        want = orc.mttkrp(dims, t.coords, t.values, f, d)
+        assert mk.verify_against(a[d], want)[0] <= 1e-5
+        assert mk.verify_against(b[d], want)[0] <= 1e-5
+
+
+@pytest.mark.parametrize("kernel", [0, 1])
+def test_sharded_ranges_each_kernel(mk, orc, kernel):
+    """Row-range shards: each rank's owned rows match the oracle."""
+    dims = [1000, 24, 3000]
+    t = mk.generate_synthetic(dims, 200_000, seed=5)
+    f = [m.data for m in mk.random_factors(dims, 32, 2)]
+    for world in (2, 3):
+        for r in range(world):
+            c = mk.Context()
+            c.upload_tensor(t)
+            c.build_plans(148)
+            c.upload_factors(f)
+            c.set_fast_kernel(kernel)
+            c.set_shard(r, world)
+            for d in range(3):
+                c.mttkrp_mode_async(d)
+                c.synchronize()
+                k0, k1 = c.shard_rows(d, r)
+                want = orc.mttkrp(dims, t.coords, t.values, f, d)
+                got = c.output(d)
+                seq = orc.build_plan(dims, t.coords, d, 148, 0, 0)
+                order = np.asarray(seq["order"], dtype=np.int64)
+                cd = np.asarray(t.coords)[order, d]
+                runs = cd[np.r_[True, cd[1:] != cd[:-1]]]
+                own = runs[k0:k1]
+                err = np.abs(got[own] - want[own]).max() / max(1.0, np.abs(want[own]).max()) if len(own) else 0.0
+                assert err <= 1e-4, (kernel, world, r, d, err)
+
+
+def test_nonfinite_reported_by_each_kernel(mk):
+    """kernel.hpp:109-114: a non-finite partial product is reported with the reference's
+    copy position, whichever kernel runs (the level-ordered kernel rescans in its last CTA)."""
+    dims = [50, 60, 70]
+    t = mk.generate_synthetic(dims, 5000, seed=9)
+    f = [m.data for m in mk.random_factors(dims, 32, 3)]
+    f[1][7, :] = 3e38
+    f[2][:, :] = 3e38
+    msgs = []
+    for kernel in (0, 1, 2):
+        c = mk.Context()
+        c.upload_tensor(t)
+        c.build_plans(148)
+        c.upload_factors(f)
+        c.set_fast_kernel(kernel)
+        with pytest.raises(mk.MttkrpError) as e:
+            c.mttkrp_mode(0)
+        assert "non-finite" in str(e.value)
+        msgs.append(str(e.value))
+        det = mk.Context()
+        det.upload_tensor(t)
+        det.build_plans(148)
+        det.upload_factors(f)
+        with pytest.raises(mk.MttkrpError) as e2:
+            det.mttkrp_mode(0, True)
+        assert str(e2.value) == msgs[-1]  # same element and copy position as the reference order
+    assert len(set(msgs)) == 1
