@@ -59,6 +59,7 @@ void check_nonfinite(Context& c) {
                            c.stream));
   MKB_CUDA(cudaStreamSynchronize(c.stream));
   if (tagged != ~0ull) {
+    MKB_CUDA(cudaMemsetAsync(c.nonfinite.get(), 0xff, sizeof tagged, c.stream));  // reported once
     const uint64_t mode = tagged >> 32, pos = tagged & 0xffffffffull;
     uint32_t elem = 0;
     MKB_CUDA(cudaMemcpy(&elem, c.copies[mode].order.get() + pos, sizeof elem,
@@ -75,6 +76,11 @@ void check_nonfinite(Context& c) {
 void sweep(Context& c, int chain, int exec) {
   const float* in[kMaxModes];
   for (uint32_t w = 0; w < c.n; ++w) in[w] = c.factors[w].get();
+  if (!chain && exec == MK_EXEC_FAST) {
+    float* outs[kMaxModes];
+    for (uint32_t d = 0; d < c.n; ++d) outs[d] = c.outputs[d].get();
+    if (launch_sweep2(c, in, outs)) return;  // one fused launch (stream2.cuh k_sweep2)
+  }
   for (uint32_t d = 0; d < c.n; ++d) {
     launch_mttkrp(c, d, in, c.outputs[d].get(), exec);
     if (chain) in[d] = c.outputs[d].get();
@@ -403,6 +409,7 @@ int mk_sweep_async(mk_context* ctx, int chain, int exec) {
     Context& c = ctx->c;
     need_plans(c);
     need_factors(c);
+    if (!c.nonfinite.get()) reset_nonfinite(c);  // later checks reset it after reporting
     sweep(c, chain, exec);
   });
 }

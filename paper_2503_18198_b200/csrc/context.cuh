@@ -173,6 +173,9 @@ void pack_records(Context& c, uint32_t mode, const uint32_t* rank_of_row);
 // use (or eagerly by prepare_stream2); false when the shape has no specialisation.
 bool prepare_stream2(Context& c, uint32_t mode);
 bool launch_stream2(Context& c, uint32_t mode, const float* const* in, float* out);
+// One fused launch for an unchained all-mode sweep (when every mode shares the level-ordered
+// kernel's specialisation); false if not applicable (nothing launched).
+bool launch_sweep2(Context& c, const float* const* in, float* const* outs);
 // rank_of_row[row_seq[k]] = k for the copy's non-empty rows
 void rank_of_row_build(Context& c, uint32_t mode, DevBuf<uint32_t>& rank);
 void check_nonfinite(Context& c);  // synchronises; throws MK_ENONFINITE

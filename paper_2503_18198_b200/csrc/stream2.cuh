@@ -30,6 +30,7 @@
 #pragma once
 
 #include <algorithm>
+#include <type_traits>
 
 #include "context.cuh"
 #include "tma.cuh"
@@ -87,8 +88,8 @@ struct Args {
   uint32_t nitems;
   const uint32_t* zero_rows; // rows every launch zeroes before its first atomic flush
   uint32_t n_zero;           // (blocked plans: all rows 0..n_zero-1, zero_rows unused)
-  uint32_t* sync;            // [0] finished CTAs, [1] non-finite row seen, [2] CTAs done
-                             // zeroing (all 0 between launches)
+  uint32_t* sync;            // [0] finished CTAs, [1] non-finite row seen (0 between launches)
+  uint32_t* zcnt;            // CTAs done zeroing this launch's rows (0 between launches)
 };
 
 // Record layout.  AW = 2 (NIN <= 2): P0 = c0 | c1 << b0 | flag << 31.
@@ -357,11 +358,36 @@ struct Body {
   }
 };
 
-// K = number of innermost levels staged in shared memory (all of them in a blocked plan);
-// OS = the outer level's factor is staged too; B = elements per gather batch; NT / MINB =
-// threads per CTA / minimum resident CTAs per SM.
-template <int NI, int NOUT, int K, bool OS, int G, int B, int NT, int MINB>
-__global__ void __launch_bounds__(NT, MINB) k_stream2(const Args a) {
+// Shared memory: [header: mbarriers (fixed, so ring phases persist across the modes of a fused
+// sweep) at 0, the current mode's Args at kArgsOff][staged factor slices][outer factor]
+// [per-warp record rings].
+constexpr uint32_t kHeader = 1024, kArgsOff = 512;
+
+// Per-thread state that persists across the modes of one launch.
+struct Persist {
+  uint32_t it;      // this warp's ring sequence number (mbarrier phase)
+  uint32_t sphase;  // staging barrier phase
+  bool zeroed;      // this lane has seen the launch's pre-zeroing complete
+};
+
+// This CTA's share of a mode's pre-zero rows (Global_Update targets).
+template <int G, int NT>
+__device__ __forceinline__ void zero_share(const Args& a) {
+  const uint32_t z0 = static_cast<uint32_t>(static_cast<uint64_t>(a.n_zero) * blockIdx.x / gridDim.x);
+  const uint32_t z1 =
+      static_cast<uint32_t>(static_cast<uint64_t>(a.n_zero) * (blockIdx.x + 1) / gridDim.x);
+  const float4 zero = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (uint32_t i = z0 + threadIdx.x / G; i < z1; i += NT / G) {
+    const uint32_t row = a.blocked ? i : a.zero_rows[i];
+    if (row != 0xffffffffu)
+      reinterpret_cast<float4*>(a.out)[static_cast<size_t>(row) * G + threadIdx.x % G] = zero;
+  }
+}
+
+// One mode of a launch: the CTA's work items.  Returns whether this lane flushed a
+// non-finite row sum.
+template <int NI, int NOUT, int K, bool OS, int G, int B, int NT>
+__device__ __forceinline__ bool mode_body(const Args& a, uint8_t* smem, Persist& ps) {
   using L = Lay<NI, NOUT>;
   using Bd = Body<NI, NOUT, K, OS, G>;
   constexpr int NIN = L::NIN;
@@ -374,38 +400,12 @@ __global__ void __launch_bounds__(NT, MINB) k_stream2(const Args a) {
   constexpr uint32_t WBYTES = 2u * (BA + BB);
   static_assert(S % B == 0, "a chunk must be a whole number of batches");
   static_assert(BA % 16 == 0 && BB % 16 == 0, "tiles must be multiples of 16 B");
-  extern __shared__ __align__(128) uint8_t smem[];
 
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int gw = lane / G;
   uint8_t* ring = smem + a.records_off + wid * WBYTES;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + a.records_off + NW * WBYTES);
-  uint64_t* wbar = bars + 2 * wid;
-  uint64_t* sbar = bars + 2 * NW;
-
-  if (tid == 0) mbar_init(sbar, 1);
-  if (lane == 0) {
-    mbar_init(&wbar[0], 1);
-    mbar_init(&wbar[1], 1);
-    mbar_fence_init();
-  }
-  // this CTA's share of the pre-zero rows (Global_Update targets), then count it done
-  {
-    const uint32_t z0 = static_cast<uint32_t>(static_cast<uint64_t>(a.n_zero) * blockIdx.x / gridDim.x);
-    const uint32_t z1 =
-        static_cast<uint32_t>(static_cast<uint64_t>(a.n_zero) * (blockIdx.x + 1) / gridDim.x);
-    const float4 zero = make_float4(0.f, 0.f, 0.f, 0.f);
-    for (uint32_t i = z0 + tid / G; i < z1; i += NT / G) {
-      const uint32_t row = a.blocked ? i : a.zero_rows[i];
-      if (row != 0xffffffffu)
-        reinterpret_cast<float4*>(a.out)[static_cast<size_t>(row) * G + tid % G] = zero;
-    }
-  }
-  __syncthreads();
-  if (tid == 0) {
-    __threadfence();
-    atomicAdd(a.sync + 2, 1u);
-  }
+  uint64_t* wbar = reinterpret_cast<uint64_t*>(smem) + 2 * wid;
+  uint64_t* sbar = reinterpret_cast<uint64_t*>(smem) + 2 * NW;
 
   Lane<NIN> ln;
   ln.lane_g = lane % G;
@@ -417,7 +417,7 @@ __global__ void __launch_bounds__(NT, MINB) k_stream2(const Args a) {
   ln.so = smem_u32(smem + a.outer_off) + ln.lane_g * 16u;
   ln.go = reinterpret_cast<const float4*>(a.Yg[0]) + ln.lane_g;
   ln.outv = reinterpret_cast<float4*>(a.out) + ln.lane_g;
-  ln.zcnt = a.sync + 2;
+  ln.zcnt = a.zcnt;
   ln.rowmask = a.rowmask;
   ln.rowbits = a.rowbits;
   ln.b0 = a.b0;
@@ -427,10 +427,9 @@ __global__ void __launch_bounds__(NT, MINB) k_stream2(const Args a) {
 
   const uint8_t* gA = L::AW == 2 ? reinterpret_cast<const uint8_t*>(a.recA2)
                                  : reinterpret_cast<const uint8_t*>(a.recA4);
-  bool bad = false;         // this lane flushed a non-finite row sum
-  bool zeroed = false;      // this lane has seen the launch's pre-zeroing complete
-  uint32_t it = 0;          // this warp's ring sequence number
-  uint32_t sphase = 0;      // staging barrier phase
+  bool bad = false;
+  bool zeroed = ps.zeroed;
+  uint32_t it = ps.it;
   uint32_t staged = 0xffffffffu;
   const uint32_t i_end = a.cta_items[blockIdx.x + 1];
   for (uint32_t ii = a.cta_items[blockIdx.x]; ii < i_end; ++ii) {
@@ -447,7 +446,7 @@ __global__ void __launch_bounds__(NT, MINB) k_stream2(const Args a) {
       if (d.tiles > 1) issue(1, (it + 1) & 1);
     }
     __syncwarp();
-    // (re)stage the block's factor slices (and the outer factor once)
+    // (re)stage the block's factor slices (and the outer factor with the first block)
     if constexpr (K > 0 || OS) {
       if (item.blk != staged) {
         __syncthreads();  // every warp is done with the previous slices
@@ -472,8 +471,8 @@ __global__ void __launch_bounds__(NT, MINB) k_stream2(const Args a) {
           if (OS && staged == 0xffffffffu)
             stage(a.outer_off, reinterpret_cast<const uint8_t*>(a.Yg[0]), a.outer_bytes);
         }
-        mbar_wait(sbar, sphase);
-        sphase ^= 1u;
+        mbar_wait(sbar, ps.sphase);
+        ps.sphase ^= 1u;
         staged = item.blk;
       }
     }
@@ -518,16 +517,25 @@ __global__ void __launch_bounds__(NT, MINB) k_stream2(const Args a) {
           s.acc1.x += __shfl_xor_sync(0xffffffffu, s.acc1.x, off);
           s.acc1.y += __shfl_xor_sync(0xffffffffu, s.acc1.y, off);
         }
-        if (lane < G) flush(ln.outv, s.row, s.acc0, s.acc1, true, G, ln.zcnt, zeroed);
+        if (lane < G) flush(ln.outv, s.row, s.acc0, s.acc1, true, G, ln.zcnt, s.zeroed);
         combined = true;
       }
     }
-    if (have && !combined) flush(ln.outv, s.row, s.acc0, s.acc1, last_atomic, G, ln.zcnt, zeroed);
+    if (have && !combined) flush(ln.outv, s.row, s.acc0, s.acc1, last_atomic, G, ln.zcnt, s.zeroed);
     bad |= s.bad;
     zeroed |= s.zeroed;
   }
-  // Non-finite products are rare: lanes only remember that a row sum was non-finite; the
-  // last CTA to finish rescans the launch's elements in the reference's order.
+  ps.it = it;
+  ps.zeroed = zeroed;
+  return bad;
+}
+
+// End of a mode: non-finite products are rare, so lanes only remember that a row sum was
+// non-finite; the last CTA to finish the mode rescans its elements in the reference's order
+// and resets the mode's counters (and, after the launch's last mode, the zeroing counter).
+template <int NI, int NOUT, int G, int NT>
+__device__ __forceinline__ void mode_epilogue(const Args& a, bool bad, bool last_mode) {
+  const int tid = threadIdx.x, lane = tid & 31;
   if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(&a.sync[1], 1u);
   __shared__ uint32_t last;
   __syncthreads();
@@ -538,13 +546,86 @@ __global__ void __launch_bounds__(NT, MINB) k_stream2(const Args a) {
   __syncthreads();
   if (last) {
     __threadfence();
-    if (*reinterpret_cast<volatile uint32_t*>(&a.sync[1])) rescan_all<NI, NOUT, G, NW>(a);
+    if (*reinterpret_cast<volatile uint32_t*>(&a.sync[1])) rescan_all<NI, NOUT, G, NT / 32>(a);
     __syncthreads();
     if (tid == 0) {
       a.sync[0] = 0;
       a.sync[1] = 0;
-      a.sync[2] = 0;
+      if (last_mode) *a.zcnt = 0;
     }
+  }
+  __syncthreads();  // the next mode may reuse this mode's shared memory
+}
+
+template <int NT>
+__device__ __forceinline__ void init_barriers(uint8_t* smem) {
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem);
+  if (tid == 0) mbar_init(bars + 2 * (NT / 32), 1);
+  if (lane == 0) {
+    mbar_init(&bars[2 * wid], 1);
+    mbar_init(&bars[2 * wid + 1], 1);
+    mbar_fence_init();
+  }
+}
+
+// K = number of innermost levels staged in shared memory (all of them in a blocked plan);
+// OS = the outer level's factor is staged too; B = elements per gather batch; NT / MINB =
+// threads per CTA / minimum resident CTAs per SM.
+template <int NI, int NOUT, int K, bool OS, int G, int B, int NT, int MINB>
+__global__ void __launch_bounds__(NT, MINB) k_stream2(const Args a) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  init_barriers<NT>(smem);
+  zero_share<G, NT>(a);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    atomicAdd(a.zcnt, 1u);
+  }
+  Persist ps{0u, 0u, false};
+  const bool bad = mode_body<NI, NOUT, K, OS, G, B, NT>(a, smem, ps);
+  mode_epilogue<NI, NOUT, G, NT>(a, bad, true);
+}
+
+// A whole unchained sweep (Algorithm 1 without chaining, the unit run_timed measures) in one
+// launch, for modes sharing one specialisation: all modes' rows are zeroed up front, then
+// every CTA walks its items of mode 0, 1, ... with no grid barrier in between, so a CTA that
+// finishes a mode early stages the next one while others are still busy.
+struct SweepArgs {
+  Args m[kMaxModes];
+  uint32_t nmodes;
+};
+
+template <int NI, int NOUT, int K, bool OS, int G, int B, int NT, int MINB>
+__global__ void __launch_bounds__(NT, MINB) k_sweep2(const SweepArgs sa) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  init_barriers<NT>(smem);
+#pragma unroll
+  for (uint32_t m = 0; m < 5; ++m)
+    if (m < sa.nmodes) zero_share<G, NT>(sa.m[m]);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    atomicAdd(sa.m[0].zcnt, 1u);
+  }
+  Persist ps{0u, 0u, false};
+  // The mode's Args go to shared memory (static-index copies): indexing the kernel-parameter
+  // array with a runtime mode would put all of it on the local-memory stack.
+  Args* as = reinterpret_cast<Args*>(smem + kArgsOff);
+  static_assert(kArgsOff + sizeof(Args) <= kHeader, "header too small");
+  for (uint32_t m = 0; m < sa.nmodes; ++m) {
+    if (threadIdx.x == 0) {
+      switch (m) {
+        case 0: *as = sa.m[0]; break;
+        case 1: *as = sa.m[1]; break;
+        case 2: *as = sa.m[2]; break;
+        case 3: *as = sa.m[3]; break;
+        default: *as = sa.m[4]; break;
+      }
+    }
+    __syncthreads();
+    const bool bad = mode_body<NI, NOUT, K, OS, G, B, NT>(*as, smem, ps);
+    mode_epilogue<NI, NOUT, G, NT>(*as, bad, m + 1 == sa.nmodes);
   }
 }
 
@@ -573,38 +654,61 @@ void launch_one(const Args& a, unsigned grid, size_t smem, cudaStream_t st) {
                                        params, smem, st));
 }
 
+template <int NI, int NOUT, int K, bool OS, int G, int NT, int MINB>
+void launch_sweep_one(const SweepArgs& a, unsigned grid, size_t smem, cudaStream_t st) {
+  constexpr int B = 3;
+  auto kern = k_sweep2<NI, NOUT, K, OS, G, B, NT, MINB>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    MKB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(kMaxDynSmem)));
+    attr_set = true;
+  }
+  void* params[] = {const_cast<SweepArgs*>(&a)};
+  MKB_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(kern), dim3(grid), dim3(NT),
+                                       params, smem, st));
+}
+
 // Every plan runs 512-thread CTAs, one per SM (the staged factors take most of the shared
-// memory; without staging the rings still do).
-template <int NI, int NOUT, bool OS, int G>
-void launch_k(const Args& a, uint32_t K, unsigned grid, size_t staged_end, cudaStream_t st) {
+// memory; without staging the rings still do).  `smem` is the dynamic shared memory size.
+template <int NI, int NOUT, bool OS, int G, typename A>
+void launch_k(const A& a, uint32_t K, unsigned grid, size_t smem, cudaStream_t st) {
   constexpr int NIN = NI - NOUT;
-  const size_t smem = staged_end + ring_bytes<NI, NOUT>(G, 512);
-  if (K == 0) return launch_one<NI, NOUT, 0, OS, G, 512, 1>(a, grid, smem, st);
+  auto go = [&](auto kc) {
+    constexpr int KK = decltype(kc)::value;
+    if constexpr (std::is_same_v<A, SweepArgs>)
+      launch_sweep_one<NI, NOUT, KK, OS, G, 512, 1>(a, grid, smem, st);
+    else
+      launch_one<NI, NOUT, KK, OS, G, 512, 1>(a, grid, smem, st);
+  };
+  if (K == 0) return go(std::integral_constant<int, 0>{});
   if constexpr (NIN >= 1)
-    if (K == 1) return launch_one<NI, NOUT, 1, OS, G, 512, 1>(a, grid, smem, st);
+    if (K == 1) return go(std::integral_constant<int, 1>{});
   if constexpr (NIN >= 2)
-    if (K == 2) return launch_one<NI, NOUT, 2, OS, G, 512, 1>(a, grid, smem, st);
+    if (K == 2) return go(std::integral_constant<int, 2>{});
   if constexpr (NIN >= 3)
-    if (K == 3) return launch_one<NI, NOUT, 3, OS, G, 512, 1>(a, grid, smem, st);
+    if (K == 3) return go(std::integral_constant<int, 3>{});
   if constexpr (NIN >= 4)
-    if (K == 4) return launch_one<NI, NOUT, 4, OS, G, 512, 1>(a, grid, smem, st);
+    if (K == 4) return go(std::integral_constant<int, 4>{});
   fail(MK_EINVAL, "stream2: bad staging count");
 }
 
-template <int NI, int G>
-void launch_ni_g(const Args& a, uint32_t nout, bool os, uint32_t K, unsigned grid,
-                 size_t staged_end, cudaStream_t st) {
-  if (nout == 0) return launch_k<NI, 0, false, G>(a, K, grid, staged_end, st);
-  if (os) return launch_k<NI, 1, true, G>(a, K, grid, staged_end, st);
-  return launch_k<NI, 1, false, G>(a, K, grid, staged_end, st);
+template <int NI, int G, typename A>
+void launch_ni_g(const A& a, uint32_t nout, bool os, uint32_t K, unsigned grid, size_t smem,
+                 cudaStream_t st) {
+  if (nout == 0) return launch_k<NI, 0, false, G>(a, K, grid, smem, st);
+  if (os) return launch_k<NI, 1, true, G>(a, K, grid, smem, st);
+  return launch_k<NI, 1, false, G>(a, K, grid, smem, st);
 }
 
 }  // namespace s2
 
-// per-(N, G) dispatch (stream2_n<N>_g<G>.cu)
+// per-(N, G) dispatch (stream2_n<N>_g<G>.cu); `smem` = dynamic shared memory bytes
 #define MKB_S2_DECL(N, G)                                                                  \
   void stream2_launch_n##N##_g##G(const s2::Args& a, uint32_t nout, bool os, uint32_t K,   \
-                                  unsigned grid, size_t staged_end, cudaStream_t st);
+                                  unsigned grid, size_t smem, cudaStream_t st);            \
+  void stream2_sweep_n##N##_g##G(const s2::SweepArgs& a, uint32_t nout, bool os, uint32_t K, \
+                                 unsigned grid, size_t smem, cudaStream_t st);
 MKB_S2_DECL(3, 8)
 MKB_S2_DECL(3, 16)
 MKB_S2_DECL(4, 8)

@@ -1,10 +1,14 @@
-// Instantiations of the streaming kernel for N = 3, G = 8 lanes per row (one file per
-// shape so the instantiations compile in parallel).
+// Instantiations of the streaming kernels for N = 3, G = 8 lanes per row (one file per shape
+// so the instantiations compile in parallel).
 #include "stream2.cuh"
 
 namespace mkb {
 void stream2_launch_n3_g8(const s2::Args& a, uint32_t nout, bool os, uint32_t K,
-                          unsigned grid, size_t staged_end, cudaStream_t st) {
-  s2::launch_ni_g<2, 8>(a, nout, os, K, grid, staged_end, st);
+                          unsigned grid, size_t smem, cudaStream_t st) {
+  s2::launch_ni_g<2, 8>(a, nout, os, K, grid, smem, st);
+}
+void stream2_sweep_n3_g8(const s2::SweepArgs& a, uint32_t nout, bool os, uint32_t K,
+                         unsigned grid, size_t smem, cudaStream_t st) {
+  s2::launch_ni_g<2, 8>(a, nout, os, K, grid, smem, st);
 }
 }  // namespace mkb

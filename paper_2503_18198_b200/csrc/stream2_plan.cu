@@ -290,7 +290,7 @@ bool prepare_stream2(Context& c, uint32_t mode) {
   //      stage = per CTA item: staged slice bytes / 85 B per SM-cycle + a ~6000-cycle stall
   //    cost = LSU + L2 + flush + stage (fitted to the measured cfg2 / cfg3 / cfg5 plans).
   const size_t ring = s2::ring_bytes_rt(p.aw, G, 512);
-  size_t budget = s2::kMaxDynSmem - ring - 256;
+  size_t budget = s2::kMaxDynSmem - ring - s2::kHeader;
   const bool stage_on = env_int("MKB_STAGE", 1) != 0;
   const bool block_on = env_int("MKB_BLOCK", 1) != 0 && !sharded;
   p.os = stage_on && p.nout && fbytes(lv[0]) <= std::min<size_t>(32u << 10, budget / 4);
@@ -365,7 +365,7 @@ bool prepare_stream2(Context& c, uint32_t mode) {
   for (uint32_t l = 0; l < ni; ++l) p.levels[l] = lv[l];
   // shared-memory layout: staged inner slots (slot order), outer factor, record rings
   {
-    size_t off = 0;
+    size_t off = s2::kHeader;  // mbarriers first (stream2.cuh)
     for (uint32_t j = nin - p.k; j < nin; ++j) {
       p.stage_off[j] = static_cast<uint32_t>(off);
       off += align128(static_cast<size_t>(rows[j]) * rowbytes);
@@ -594,6 +594,62 @@ bool prepare_stream2(Context& c, uint32_t mode) {
   return true;
 }
 
+namespace {
+
+// Kernel arguments of one mode (the plan must be prepared); false if nothing to stream.
+void fill_args(Context& c, uint32_t mode, const float* const* in, float* out, s2::Args& a,
+               uint32_t* sync, uint32_t* zcnt) {
+  ModeCopy& mc = c.copies[mode];
+  ModeCopy::Stream2& p = mc.s2;
+  a = s2::Args{};
+  a.recA2 = reinterpret_cast<const uint2*>(p.recA.get());
+  a.recA4 = reinterpret_cast<const uint4*>(p.recA.get());
+  a.sk = p.sk.get();
+  a.kperm = p.kperm.get();
+  for (uint32_t l = 0; l < p.ni; ++l) a.Yg[l] = in[p.levels[l]];
+  a.blks = reinterpret_cast<const Blk*>(p.blk_dev.get());
+  a.wdesc = reinterpret_cast<const WDesc*>(p.wdesc.get());
+  a.items = reinterpret_cast<const Item*>(p.items.get());
+  a.cta_items = p.cta_items.get();
+  a.out = out;
+  a.nonfinite = c.nonfinite.get();
+  a.tag = static_cast<unsigned long long>(mode) << 32;
+  a.rowbits = p.rowbits;
+  a.rowmask = p.rowbits >= 32 ? 0xffffffffu : ((1u << p.rowbits) - 1u);
+  a.asc_level = 0;
+  uint32_t q = 0;  // ascending mode order -> level
+  for (uint32_t w = 0; w < c.n; ++w) {
+    if (w == mode) continue;
+    for (uint32_t l = 0; l < p.ni; ++l)
+      if (p.levels[l] == w) a.asc_level |= l << (4 * q);
+    ++q;
+  }
+  a.b0 = p.b0;
+  a.m0 = p.m0;
+  a.m1 = p.m1;
+  for (uint32_t j = 0; j < 4; ++j) a.stage_off[j] = p.stage_off[j];
+  a.outer_off = p.outer_off;
+  a.outer_bytes = p.outer_bytes;
+  a.records_off = static_cast<uint32_t>(p.staged_end);
+  a.blocked = p.blocked ? 1u : 0u;
+  a.nitems = p.nitems;
+  a.zero_rows = p.zero_rows.get();
+  a.n_zero = static_cast<uint32_t>(p.blocked ? c.dims[mode] : p.n_zero_rows);
+  a.sync = sync;
+  a.zcnt = zcnt;
+}
+
+// counters: [0..1] single-mode launches, [2] zeroing, [4 + 2m ..] per mode of a fused sweep
+uint32_t* sync_words(Context& c) {
+  if (!c.s2sync.get()) {
+    c.s2sync.resize(4 + 2 * kMaxModes);
+    MKB_CUDA(cudaMemsetAsync(c.s2sync.get(), 0, (4 + 2 * kMaxModes) * sizeof(uint32_t), c.stream));
+  }
+  return c.s2sync.get();
+}
+
+}  // namespace
+
 bool launch_stream2(Context& c, uint32_t mode, const float* const* in, float* out) {
   if (!prepare_stream2(c, mode)) return false;
   ModeCopy& mc = c.copies[mode];
@@ -612,56 +668,54 @@ bool launch_stream2(Context& c, uint32_t mode, const float* const* in, float* ou
     }
     return true;
   }
-  s2::Args a{};
-  a.recA2 = reinterpret_cast<const uint2*>(p.recA.get());
-  a.recA4 = reinterpret_cast<const uint4*>(p.recA.get());
-  a.sk = p.sk.get();
-  a.kperm = p.kperm.get();
-  for (uint32_t l = 0; l < p.ni; ++l) a.Yg[l] = in[p.levels[l]];
-  a.blks = reinterpret_cast<const Blk*>(p.blk_dev.get());
-  a.wdesc = reinterpret_cast<const WDesc*>(p.wdesc.get());
-  a.items = reinterpret_cast<const Item*>(p.items.get());
-  a.cta_items = p.cta_items.get();
-  a.out = out;
-  a.nonfinite = c.nonfinite.get();
-  a.tag = static_cast<unsigned long long>(mode) << 32;
-  a.rowbits = p.rowbits;
-  a.rowmask = p.rowbits >= 32 ? 0xffffffffu : ((1u << p.rowbits) - 1u);
-  a.asc_level = 0;
-  {
-    uint32_t q = 0;  // ascending mode order -> level
-    for (uint32_t w = 0; w < c.n; ++w) {
-      if (w == mode) continue;
-      for (uint32_t l = 0; l < p.ni; ++l)
-        if (p.levels[l] == w) a.asc_level |= l << (4 * q);
-      ++q;
-    }
-  }
-  a.b0 = p.b0;
-  a.m0 = p.m0;
-  a.m1 = p.m1;
-  for (uint32_t j = 0; j < 4; ++j) a.stage_off[j] = p.stage_off[j];
-  a.outer_off = p.outer_off;
-  a.outer_bytes = p.outer_bytes;
-  a.records_off = static_cast<uint32_t>(p.staged_end);
-  a.blocked = p.blocked ? 1u : 0u;
-  a.nitems = p.nitems;
-  a.zero_rows = p.zero_rows.get();
-  a.n_zero = static_cast<uint32_t>(p.blocked ? c.dims[mode] : p.n_zero_rows);
-  if (!c.s2sync.get()) {
-    c.s2sync.resize(4);
-    MKB_CUDA(cudaMemsetAsync(c.s2sync.get(), 0, 4 * sizeof(uint32_t), st));
-  }
-  a.sync = c.s2sync.get();
-  const size_t se = p.staged_end;
+  uint32_t* sw = sync_words(c);
+  s2::Args a;
+  fill_args(c, mode, in, out, a, sw, sw + 2);
+  const size_t smem = p.staged_end + s2::ring_bytes_rt(p.aw, G, 512);
   const unsigned grid = p.grid;
   switch (c.n * 100 + G) {
-    case 308: stream2_launch_n3_g8(a, p.nout, p.os, p.k, grid, se, st); break;
-    case 316: stream2_launch_n3_g16(a, p.nout, p.os, p.k, grid, se, st); break;
-    case 408: stream2_launch_n4_g8(a, p.nout, p.os, p.k, grid, se, st); break;
-    case 416: stream2_launch_n4_g16(a, p.nout, p.os, p.k, grid, se, st); break;
-    case 508: stream2_launch_n5_g8(a, p.nout, p.os, p.k, grid, se, st); break;
-    case 516: stream2_launch_n5_g16(a, p.nout, p.os, p.k, grid, se, st); break;
+    case 308: stream2_launch_n3_g8(a, p.nout, p.os, p.k, grid, smem, st); break;
+    case 316: stream2_launch_n3_g16(a, p.nout, p.os, p.k, grid, smem, st); break;
+    case 408: stream2_launch_n4_g8(a, p.nout, p.os, p.k, grid, smem, st); break;
+    case 416: stream2_launch_n4_g16(a, p.nout, p.os, p.k, grid, smem, st); break;
+    case 508: stream2_launch_n5_g8(a, p.nout, p.os, p.k, grid, smem, st); break;
+    case 516: stream2_launch_n5_g16(a, p.nout, p.os, p.k, grid, smem, st); break;
+    default: return false;
+  }
+  return true;
+}
+
+// One launch for an unchained all-mode sweep when every mode runs the level-ordered kernel
+// with the same specialisation; false (nothing launched) otherwise.
+bool launch_sweep2(Context& c, const float* const* in, float* const* outs) {
+  if (std::getenv("MKB_FUSE") && std::getenv("MKB_FUSE")[0] == '0') return false;
+  const uint32_t G = c.rank / 4;
+  size_t smem = 0;
+  const ModeCopy::Stream2& p0 = c.copies[0].s2;
+  for (uint32_t d = 0; d < c.n; ++d) {
+    if (choose_fast_kernel(c, d, in, outs[d]) != 0) return false;
+    if (!prepare_stream2(c, d)) return false;
+    const ModeCopy& mc = c.copies[d];
+    const ModeCopy::Stream2& p = mc.s2;
+    if (p.nitems == 0 || mc.shard_e1 <= mc.shard_e0) return false;
+    if (p.nout != p0.nout || p.os != p0.os || p.k != p0.k || p.aw != p0.aw || p.grid != p0.grid)
+      return false;
+    smem = std::max(smem, p.staged_end + s2::ring_bytes_rt(p.aw, G, 512));
+  }
+  uint32_t* sw = sync_words(c);
+  static_assert(sizeof(s2::SweepArgs) <= 32000, "kernel parameter space");
+  s2::SweepArgs sa{};
+  sa.nmodes = c.n;
+  for (uint32_t d = 0; d < c.n; ++d) fill_args(c, d, in, outs[d], sa.m[d], sw + 4 + 2 * d, sw + 2);
+  cudaStream_t st = c.stream;
+  const unsigned grid = p0.grid;
+  switch (c.n * 100 + G) {
+    case 308: stream2_sweep_n3_g8(sa, p0.nout, p0.os, p0.k, grid, smem, st); break;
+    case 316: stream2_sweep_n3_g16(sa, p0.nout, p0.os, p0.k, grid, smem, st); break;
+    case 408: stream2_sweep_n4_g8(sa, p0.nout, p0.os, p0.k, grid, smem, st); break;
+    case 416: stream2_sweep_n4_g16(sa, p0.nout, p0.os, p0.k, grid, smem, st); break;
+    case 508: stream2_sweep_n5_g8(sa, p0.nout, p0.os, p0.k, grid, smem, st); break;
+    case 516: stream2_sweep_n5_g16(sa, p0.nout, p0.os, p0.k, grid, smem, st); break;
     default: return false;
   }
   return true;

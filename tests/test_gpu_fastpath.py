@@ -149,3 +149,49 @@ def test_nonfinite_reported_by_each_kernel(mk):
             det.mttkrp_mode(0, True)
         assert str(e2.value) == msgs[-1]  # same element and copy position as the reference order
     assert len(set(msgs)) == 1
+
+
+@pytest.mark.parametrize("dims,nnz", [([183, 24, 1140, 1717], 300_000), ([1000, 1000, 1000], 400_000),
+                                      ([6000, 9000, 30000], 600_000)])
+def test_fused_sweep_matches_oracle(mk, orc, dims, nnz):
+    """An unchained sweep runs as ONE launch (k_sweep2) when every mode shares the level-ordered
+    kernel's specialisation; it must equal the per-mode results and the oracle, repeatedly and
+    interleaved with single-mode launches (shared zeroing / completion counters)."""
+    t = mk.generate_synthetic(dims, nnz, seed=4)
+    f = [m.data for m in mk.random_factors(dims, 32, 5)]
+    c = mk.Context()
+    c.upload_tensor(t)
+    c.build_plans(148)
+    c.upload_factors(f)
+    c.set_fast_kernel(0)
+    want = [orc.mttkrp(dims, t.coords, t.values, f, d) for d in range(len(dims))]
+    for rep in range(3):
+        c.sweep_async(False, False)
+        c.synchronize()
+        for d in range(len(dims)):
+            assert mk.verify_against(c.output(d), want[d])[0] <= 1e-4, (rep, d)
+        single = c.mttkrp_mode(rep % len(dims))
+        assert mk.verify_against(single, want[rep % len(dims)])[0] <= 1e-4
+
+
+def test_fused_sweep_nonfinite_reports_first_mode(mk):
+    dims = [50, 60, 70]
+    t = mk.generate_synthetic(dims, 5000, seed=9)
+    f = [m.data for m in mk.random_factors(dims, 32, 3)]
+    f[1][:, :] = 3e38  # mode 0 (Y_1 * Y_2) overflows; modes 1 and 2 stay finite
+    f[2][:, :] = 3e38
+    c = mk.Context()
+    c.upload_tensor(t)
+    c.build_plans(148)
+    c.upload_factors(f)
+    c.set_fast_kernel(0)
+    c.mttkrp_mode(1)  # a finite mode
+    c.sweep_async(False, False)  # one fused launch; the first failing mode is reported
+    with pytest.raises(mk.MttkrpError) as e:
+        c.synchronize()
+    assert "non-finite" in str(e.value) and "(mode 0," in str(e.value)
+    # the counters are reset: a clean run afterwards succeeds
+    f2 = [m.data for m in mk.random_factors(dims, 32, 3)]
+    c.upload_factors(f2)
+    c.sweep_async(False, False)
+    c.synchronize()
