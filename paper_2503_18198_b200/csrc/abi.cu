@@ -217,7 +217,7 @@ int mk_fast_path_info(mk_context* ctx, uint32_t mode, mk_fast_info* info) {
     }
     if (info->kernel == 0) {
       info->launches = 1;  // pre-zeroing runs inside the streaming kernel
-      info->stream_bytes = p.recA.bytes() + p.sk.bytes();
+      info->stream_bytes = p.tiles.bytes();
     } else if (info->kernel == 1) {
       info->launches = 2;  // split-row pre-zeroing + streaming kernel
       info->stream_bytes = mc.recA.bytes() + mc.recB.bytes();

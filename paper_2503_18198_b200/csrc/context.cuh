@@ -71,7 +71,7 @@ struct ModeCopy {
     uint32_t ni = 0, nout = 0, k = 0, aw = 2;  // input levels, outer levels, staged levels
     bool os = false;                           // outer factor staged in shared memory
     uint32_t levels[kMaxModes] = {};           // level -> input mode (outermost first)
-    uint32_t rowbits = 0, b0 = 0, m0 = 0, m1 = 0;
+    uint32_t rowbits = 0, b0 = 0, m0 = 0, m1 = 0, ob = 0, om = 0;
     uint32_t stage_off[4] = {};
     uint32_t outer_off = 0, outer_bytes = 0;
     size_t staged_end = 0;
@@ -79,7 +79,7 @@ struct ModeCopy {
     uint32_t nblocks = 1;
     uint64_t outer_runs = 0;                   // distinct (row, level-0 coordinate) pairs
     DevBuf<uint32_t> blk_dev;                  // s2::Blk table
-    DevBuf<uint32_t> recA, sk, kperm;          // warp-interleaved records, slow keys, kperm
+    DevBuf<uint32_t> tiles, kperm;             // tile stream (records + slow keys), kperm
     DevBuf<uint32_t> wdesc, items, cta_items;  // work schedule (grid = SM count)
     uint32_t nitems = 0;
     unsigned grid = 0;

@@ -55,7 +55,7 @@ struct Blk {
 };
 // One warp's stream inside a work item.
 struct WDesc {
-  uint32_t rec0, key0;  // first record / slow key of the warp's tile 0
+  uint32_t tile0, pad;  // the warp's first tile in the tile stream
   uint32_t tiles;       // tiles (chunks per group)
   uint32_t flags;       // bit g: group g's first run continues from before its range;
                         // bit 4+g: its last run continues after its range
@@ -66,10 +66,9 @@ struct Item {
 };
 
 struct Args {
-  const uint2* recA2;       // AW == 2: {value, P0}
-  const uint4* recA4;       // AW == 4: {value, P0, P1, P2}
-  const uint32_t* sk;       // slow keys
-  const uint32_t* kperm;    // record -> reference copy position (~0: padding)
+  const uint32_t* tiles;    // tile stream: per warp tile [records (GPW x RS x AW words)]
+                            // [slow keys (GPW x KS words)] (stream2_plan.cu)
+  const uint32_t* kperm;    // record slot -> reference copy position (~0: padding)
   const float* Yg[4];       // factor of each level (global)
   const Blk* blks;
   const WDesc* wdesc;
@@ -81,6 +80,7 @@ struct Args {
   uint32_t rowmask, rowbits;
   uint32_t asc_level;        // nibble p = level of the p-th input in ascending mode order
   uint32_t b0, m0, m1;       // packed-coordinate shift / masks (see Lay)
+  uint32_t ob, om;           // outer coordinate in P0: shift / mask (om == 0: read the slow key)
   uint32_t stage_off[4];     // SMEM byte offset of each inner slot's staged slice
   uint32_t outer_off, outer_bytes;  // staged outer factor (OS)
   uint32_t records_off;      // SMEM byte offset of the per-warp record rings
@@ -92,10 +92,11 @@ struct Args {
   uint32_t* zcnt;            // CTAs done zeroing this launch's rows (0 between launches)
 };
 
-// Record layout.  AW = 2 (NIN <= 2): P0 = c0 | c1 << b0 | flag << 31.
-// AW = 4 (NIN >= 3): P0 = c0 | (NIN == 4 ? c1 << b0 : 0) | flag << 31, then the remaining
-// slots one per word.  flag = first element of the group range, or its slow key differs from
-// the previous element's.
+// Record layout.  AW = 2 (NIN <= 2): P0 = c0 | c1 << b0 | outer << ob | row << 30 | flag << 31.
+// AW = 4 (NIN >= 3): P0 = c0 | (NIN == 4 ? c1 << b0 : 0) | outer << ob | row | flag, then the
+// remaining slots one per word.  flag = first element of the group range, or its slow key
+// (row, outer coordinate) differs from the previous element's; row = its row differs.  The
+// outer coordinate sits in P0 when it fits (om != 0), so an outer change needs no slow key.
 template <int NI, int NOUT>
 struct Lay {
   static constexpr int NIN = NI - NOUT;
@@ -146,32 +147,24 @@ __device__ __noinline__ void rescan_all(const Args& a) {
   using L = Lay<NI, NOUT>;
   constexpr int S = seg_len(L::AW), RS = rec_stride(L::AW), KS = key_stride(L::AW);
   constexpr int GPW = 32 / G;
+  constexpr int TW = GPW * (RS * L::AW + KS);  // words per warp tile
   for (uint32_t ii = 0; ii < a.nitems; ++ii) {
     const Item item = a.items[ii];
     const Blk* blk = a.blks + item.blk;
     for (uint32_t w = 0; w < static_cast<uint32_t>(NW); ++w) {
-      const WDesc d = a.wdesc[item.wdesc + w];
+      const WDesc d = a.wdesc[ii * NW + w];
       const uint32_t total = d.tiles * GPW * S;
       for (uint32_t q = threadIdx.x; q < total; q += blockDim.x) {
         const uint32_t s = q % S, g = (q / S) % GPW, t = q / (S * GPW);
-        const uint32_t j = d.rec0 + (t * GPW + g) * RS + s;
-        if (a.kperm[j] == 0xffffffffu) continue;
-        uint32_t r[4];
-        if constexpr (L::AW == 2) {
-          const uint2 v = a.recA2[j];
-          r[0] = v.x;
-          r[1] = v.y;
-          r[2] = r[3] = 0;
-        } else {
-          const uint4 v = a.recA4[j];
-          r[0] = v.x;
-          r[1] = v.y;
-          r[2] = v.z;
-          r[3] = v.w;
-        }
+        const size_t tile = static_cast<size_t>(d.tile0) + t;
+        const size_t slot = (tile * GPW + g) * RS + s;
+        if (a.kperm[slot] == 0xffffffffu) continue;
+        const uint32_t* tw = a.tiles + tile * TW;
+        uint32_t r[4] = {0, 0, 0, 0};
+        for (int x = 0; x < L::AW; ++x) r[x] = tw[(g * RS + s) * L::AW + x];
         uint32_t ci[4];
         unpack<NI, NOUT>(r, a.b0, a.m0, a.m1, ci);
-        const uint32_t key = a.sk[d.key0 + (t * GPW + g) * KS + s];
+        const uint32_t key = tw[GPW * RS * L::AW + g * KS + s];
         uint32_t c[4];
         for (int l = 0; l < NI; ++l)
           c[l] = l < NOUT ? (key >> a.rowbits) : ci[l - NOUT] + blk->lo[l - NOUT];
@@ -185,7 +178,7 @@ __device__ __noinline__ void rescan_all(const Args& a) {
           }
           bad |= !isfinite(p);
         }
-        if (bad) atomicMin(a.nonfinite, a.tag | static_cast<unsigned long long>(a.kperm[j]));
+        if (bad) atomicMin(a.nonfinite, a.tag | static_cast<unsigned long long>(a.kperm[slot]));
       }
     }
   }
@@ -227,7 +220,7 @@ struct Lane {
   const float4* go;        // global outer factor base
   float4* outv;
   const uint32_t* zcnt;    // CTAs done zeroing
-  uint32_t rowmask, rowbits, b0, m0, m1;
+  uint32_t rowmask, rowbits, b0, m0, m1, ob, om;
   int lane_g;
 };
 
@@ -235,7 +228,7 @@ struct Lane {
 struct Seg {
   float2 acc0, acc1;
   float4 yo;
-  uint32_t cur, row;
+  uint32_t row;
   bool first, head_atomic, all_atomic, bad;  // all_atomic: blocked plan (rows span blocks)
   bool zeroed;                                // the launch's pre-zeroing is complete
 };
@@ -249,10 +242,12 @@ struct Body {
     if (j >= NIN - K) return lds128(ln.sb[j] + c * (G * 16u));
     return __ldg(ln.gb[j] + static_cast<size_t>(c) * G);
   }
-  static __device__ __forceinline__ float4 outer(const Lane<NIN>& ln, uint32_t sk) {
-    const uint32_t c = sk >> ln.rowbits;
+  static __device__ __forceinline__ float4 outer_row(const Lane<NIN>& ln, uint32_t c) {
     if constexpr (OS) return lds128(ln.so + c * (G * 16u));
     return __ldg(ln.go + static_cast<size_t>(c) * G);
+  }
+  static __device__ __forceinline__ float4 outer(const Lane<NIN>& ln, uint32_t sk) {
+    return outer_row(ln, sk >> ln.rowbits);
   }
   static __device__ __forceinline__ void math(Seg& s, float v, const float4 (&y)[NIN]) {
     float2 t0 = make_float2(y[0].x, y[0].y), t1 = make_float2(y[0].z, y[0].w);
@@ -268,10 +263,15 @@ struct Body {
     s.acc0 = __ffma2_rn(t0, make_float2(v, v), s.acc0);
     s.acc1 = __ffma2_rn(t1, make_float2(v, v), s.acc1);
   }
-  // slow-key change: flush the finished row (if any), reload the outer row
-  static __device__ __forceinline__ void rekey(const Lane<NIN>& ln, Seg& s, uint32_t sk) {
-    const uint32_t r = sk & ln.rowmask;
-    if (r != s.row) {
+  // A flagged element: on a row change (P0 bit 30) read its slow key, flush the finished row
+  // (if any) and start the next; reload the outer row from the record's outer field (or the
+  // slow key when the field did not fit).
+  static __device__ __forceinline__ void flagged(const Lane<NIN>& ln, Seg& s, uint32_t p,
+                                                 const uint32_t* key) {
+    uint32_t sk = 0;
+    if (p & 0x40000000u) {
+      sk = *key;
+      const uint32_t r = sk & ln.rowmask;
       if (s.row != 0xffffffffu) {
         s.bad |= !isfinite(s.acc0.x + s.acc0.y + s.acc1.x + s.acc1.y);
         flush(ln.outv, s.row, s.acc0, s.acc1, s.all_atomic || (s.first && s.head_atomic), G,
@@ -282,8 +282,14 @@ struct Body {
       s.acc0 = make_float2(0.f, 0.f);
       s.acc1 = s.acc0;
     }
-    if constexpr (NOUT > 0) s.yo = outer(ln, sk);
-    s.cur = sk;
+    if constexpr (NOUT > 0) {
+      if (ln.om) {
+        s.yo = outer_row(ln, (p >> ln.ob) & ln.om);
+      } else {
+        if (!(p & 0x40000000u)) sk = *key;
+        s.yo = outer(ln, sk);
+      }
+    }
   }
   // Full chunks run a software pipeline over batches of B elements: the records of batch
   // k+2 and the gathers of batch k+1 are in flight while batch k is consumed.  Consuming a
@@ -315,10 +321,7 @@ struct Body {
     if (__any_sync(0xffffffffu, static_cast<int>(any) < 0)) {
 #pragma unroll
       for (int b = 0; b < B; ++b) {
-        if (static_cast<int>(r[b][1]) < 0) {
-          const uint32_t sk = RB[k + b];
-          if (sk != s.cur || s.row == 0xffffffffu) rekey(ln, s, sk);
-        }
+        if (static_cast<int>(r[b][1]) < 0) flagged(ln, s, r[b][1], RB + k + b);
         math(s, __uint_as_float(r[b][0]), y[b]);
       }
     } else {
@@ -402,6 +405,8 @@ __device__ __forceinline__ bool mode_body(const Args& a, uint8_t* smem, Persist&
   static_assert(BA % 16 == 0 && BB % 16 == 0, "tiles must be multiples of 16 B");
 
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  (void)RS;
+  (void)KS;
   const int gw = lane / G;
   uint8_t* ring = smem + a.records_off + wid * WBYTES;
   uint64_t* wbar = reinterpret_cast<uint64_t*>(smem) + 2 * wid;
@@ -423,10 +428,11 @@ __device__ __forceinline__ bool mode_body(const Args& a, uint8_t* smem, Persist&
   ln.b0 = a.b0;
   ln.m0 = a.m0;
   ln.m1 = a.m1;
+  ln.ob = a.ob;
+  ln.om = a.om;
   const bool blocked = a.blocked != 0;
 
-  const uint8_t* gA = L::AW == 2 ? reinterpret_cast<const uint8_t*>(a.recA2)
-                                 : reinterpret_cast<const uint8_t*>(a.recA4);
+  const uint8_t* gT = reinterpret_cast<const uint8_t*>(a.tiles);
   bool bad = false;
   bool zeroed = ps.zeroed;
   uint32_t it = ps.it;
@@ -435,11 +441,10 @@ __device__ __forceinline__ bool mode_body(const Args& a, uint8_t* smem, Persist&
   for (uint32_t ii = a.cta_items[blockIdx.x]; ii < i_end; ++ii) {
     const Item item = a.items[ii];
     const WDesc d = a.wdesc[ii * NW + wid];
-    auto issue = [&](uint32_t t, int st) {
+    auto issue = [&](uint32_t t, int st) {  // one bulk copy: the tile's records + slow keys
       mbar_arrive_tx(&wbar[st], BA + BB);
-      tma_load_1d(ring + st * BA, gA + (static_cast<size_t>(d.rec0) + t * GPW * RS) * RECB, BA,
-                  &wbar[st]);
-      tma_load_1d(ring + 2 * BA + st * BB, a.sk + d.key0 + t * GPW * KS, BB, &wbar[st]);
+      tma_load_1d(ring + st * (BA + BB), gT + (static_cast<size_t>(d.tile0) + t) * (BA + BB),
+                  BA + BB, &wbar[st]);
     };
     if (lane == 0) {
       if (d.tiles > 0) issue(0, it & 1);
@@ -480,7 +485,6 @@ __device__ __forceinline__ bool mode_body(const Args& a, uint8_t* smem, Persist&
     s.acc0 = make_float2(0.f, 0.f);
     s.acc1 = s.acc0;
     s.yo = make_float4(1.f, 1.f, 1.f, 1.f);
-    s.cur = 0xffffffffu;
     s.row = 0xffffffffu;
     s.first = true;
     s.head_atomic = (d.flags >> gw) & 1u;
@@ -490,8 +494,8 @@ __device__ __forceinline__ bool mode_body(const Args& a, uint8_t* smem, Persist&
     for (uint32_t t = 0; t < d.tiles; ++t, ++it) {
       const int st = it & 1;
       mbar_wait(&wbar[st], (it >> 1) & 1);
-      const uint8_t* RA = ring + st * BA + gw * RS * RECB;
-      const uint32_t* RB = reinterpret_cast<const uint32_t*>(ring + 2 * BA + st * BB) + gw * KS;
+      const uint8_t* RA = ring + st * (BA + BB) + gw * RS * RECB;
+      const uint32_t* RB = reinterpret_cast<const uint32_t*>(ring + st * (BA + BB) + BA) + gw * KS;
       // the last chunk of a group is padded with copies of its last record (value 0, no
       // flag), so every chunk runs the same pipelined path
       Bd::template chunk<B, S>(ln, s, RA, RB);

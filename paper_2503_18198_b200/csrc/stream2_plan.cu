@@ -107,36 +107,36 @@ struct FillArgs {
   const uint32_t* gstart;         // per descriptor and group: first kernel-order position
   const uint32_t* dblk;           // per descriptor: block
   const Blk* blks;
-  uint32_t rowbits, b0, aw, nin, gpw, S, RS, KS;
-  uint32_t* recA;                 // aw words per record
-  uint32_t* sk;
+  uint32_t rowbits, b0, ob, om, aw, nin, gpw, S, RS, KS;
+  uint32_t* tiles;                // tile stream (records + slow keys per warp tile)
   uint32_t* kperm;
 };
 
-// One CTA per warp descriptor: writes the warp's chunk-interleaved records, slow keys and
-// kperm (padding slots: zero records, ~0 keys / kperm).
+// One CTA per warp descriptor: writes the warp's tiles (chunk-interleaved records, then the
+// slow keys) and kperm.  Padding of a group's last chunk: a copy of its last record with
+// value 0 and no flags; slots past the padding: zero records, ~0 keys / kperm.
 __global__ void k_fill2(const FillArgs f) {
   const WDesc d = f.wdesc[blockIdx.x];
   const Blk bk = f.blks[f.dblk[blockIdx.x]];
   const uint32_t W = f.RS > f.KS ? f.RS : f.KS;
+  const uint32_t TW = f.gpw * (f.RS * f.aw + f.KS);
   const uint32_t total = d.tiles * f.gpw * W;
   for (uint32_t q = threadIdx.x; q < total; q += blockDim.x) {
     const uint32_t s = q % W, g = (q / W) % f.gpw, t = q / (W * f.gpw);
     const uint32_t off = t * f.S + s;
     const bool valid = s < f.S && off < d.n[g];
-    const size_t ri = d.rec0 + static_cast<size_t>(t * f.gpw + g) * f.RS + s;
-    const size_t ki = d.key0 + static_cast<size_t>(t * f.gpw + g) * f.KS + s;
+    const size_t tile = static_cast<size_t>(d.tile0) + t;
     uint32_t w[4] = {0, 0, 0, 0}, key = 0xffffffffu, kp = 0xffffffffu;
-    // padding of a group's last chunk: a copy of its last element with value 0 and no flag
     const bool pad = s < f.S && !valid && d.n[g] > 0;
     if (valid || pad) {
       const uint32_t kpos = f.gstart[blockIdx.x * 4 + g] + (valid ? off : d.n[g] - 1);
       const uint32_t e = f.perm[kpos];
       key = f.cd[e] | (f.outer ? f.outer[e] << f.rowbits : 0u);
-      bool flag = off == 0;
-      if (!flag && valid) {
+      bool flag = true, rowflag = true;
+      if (off != 0 && valid) {
         const uint32_t q2 = f.perm[kpos - 1];
         flag = key != (f.cd[q2] | (f.outer ? f.outer[q2] << f.rowbits : 0u));
+        rowflag = f.cd[e] != f.cd[q2];
       }
       uint32_t c[4] = {0, 0, 0, 0};
       for (uint32_t j = 0; j < f.nin; ++j) c[j] = f.sp.c[j][e] - bk.lo[j];
@@ -154,7 +154,9 @@ __global__ void k_fill2(const FillArgs f) {
         w[2] = c[2];
         w[3] = c[3];
       }
-      if (flag && valid) w[1] |= 0x80000000u;
+      if (f.om && f.outer) w[1] |= f.outer[e] << f.ob;
+      if (valid && flag) w[1] |= 0x80000000u;
+      if (valid && rowflag) w[1] |= 0x40000000u;
       if (valid) {
         kp = e;
       } else {
@@ -162,11 +164,12 @@ __global__ void k_fill2(const FillArgs f) {
         key = 0xffffffffu;
       }
     }
+    uint32_t* tw = f.tiles + tile * TW;
     if (s < f.RS) {
-      for (uint32_t x = 0; x < f.aw; ++x) f.recA[ri * f.aw + x] = w[x];
-      f.kperm[ri] = kp;
+      for (uint32_t x = 0; x < f.aw; ++x) tw[(g * f.RS + s) * f.aw + x] = w[x];
+      f.kperm[(tile * f.gpw + g) * f.RS + s] = kp;
     }
-    if (s < f.KS) f.sk[ki] = key;
+    if (s < f.KS) tw[f.gpw * f.RS * f.aw + g * f.KS + s] = key;
   }
 }
 
@@ -378,12 +381,21 @@ bool prepare_stream2(Context& c, uint32_t mode) {
     p.staged_end = off;
   }
   // packed coordinate widths (relative to the slices)
+  // P0 bits 30 / 31 are the row / slow-key flags: coordinates get at most 30 bits
   const int bw0 = bits_for(rows[0] - 1), bw1 = nin >= 2 ? bits_for(rows[1] - 1) : 0;
   const bool pair0 = nin == 2 || nin == 4;
-  if ((pair0 && bw0 + bw1 > 31) || bw0 > 31) return false;
+  const int used = pair0 ? bw0 + bw1 : bw0;
+  if (used > 30) return false;
   p.b0 = static_cast<uint32_t>(bw0);
   p.m0 = (1u << bw0) - 1u;
   p.m1 = bw1 >= 32 ? 0xffffffffu : ((1u << bw1) - 1u);
+  p.ob = static_cast<uint32_t>(used);
+  p.om = 0;
+  if (p.nout) {
+    const int bwo = bits_for(c.dims[lv[0]] - 1);
+    if (used + bwo <= 30) p.om = bwo ? (1u << bwo) - 1u : 0u;
+    if (bwo == 0) p.om = 0;  // a 1-row outer factor: read the slow key (never changes)
+  }
 
   // 4. kernel order: levels (innermost first), row rank, block
   iota_u32(perm.get(), nnz, st);
@@ -438,7 +450,7 @@ bool prepare_stream2(Context& c, uint32_t mode) {
   const uint64_t E0 = p.blocked ? 0 : mc.shard_e0, E1 = p.blocked ? nnz : mc.shard_e1;
   std::vector<WDesc> wd;
   std::vector<uint32_t> gstart, dblk, items, cta(grid + 1, 0);
-  uint64_t rec_n = 0, key_n = 0;
+  uint64_t tile_n = 0;
   uint32_t b = 0;
   for (unsigned cc = 0; cc < grid; ++cc) {
     cta[cc] = static_cast<uint32_t>(items.size() / 2);
@@ -453,8 +465,7 @@ bool prepare_stream2(Context& c, uint32_t mode) {
         items.push_back(static_cast<uint32_t>(wd.size()));
         for (uint32_t w = 0; w < NW; ++w) {
           WDesc d{};
-          d.rec0 = static_cast<uint32_t>(rec_n);
-          d.key0 = static_cast<uint32_t>(key_n);
+          d.tile0 = static_cast<uint32_t>(tile_n);
           uint32_t tiles = 0;
           for (uint32_t g = 0; g < 4; ++g) {
             if (g < GPW) {
@@ -468,8 +479,7 @@ bool prepare_stream2(Context& c, uint32_t mode) {
             }
           }
           d.tiles = tiles;
-          rec_n += static_cast<uint64_t>(tiles) * GPW * RS;
-          key_n += static_cast<uint64_t>(tiles) * GPW * KS;
+          tile_n += tiles;
           wd.push_back(d);
           dblk.push_back(bb);
         }
@@ -479,7 +489,9 @@ bool prepare_stream2(Context& c, uint32_t mode) {
     }
   }
   cta[grid] = static_cast<uint32_t>(items.size() / 2);
-  if (rec_n >= 0xffffffffull || key_n >= 0xffffffffull) return false;
+  const uint64_t rec_n = tile_n * GPW * RS;            // record slots (kperm entries)
+  const uint64_t tile_words = GPW * (RS * p.aw + KS);  // words per warp tile
+  if (tile_n >= 0xffffffffull || rec_n >= 0xffffffffull) return false;
   p.nitems = cta[grid];
   p.grid = grid;
   if (items.empty()) items.assign(2, 0);
@@ -533,9 +545,8 @@ bool prepare_stream2(Context& c, uint32_t mode) {
   p.cta_items.resize(grid + 1);
   MKB_CUDA(cudaMemcpyAsync(p.cta_items.get(), cta.data(), (grid + 1) * 4, cudaMemcpyHostToDevice,
                            st));
-  p.recA.resize(std::max<uint64_t>(rec_n, 1) * p.aw);
+  p.tiles.resize(std::max<uint64_t>(tile_n * tile_words, 1));
   p.kperm.resize(std::max<uint64_t>(rec_n, 1));
-  p.sk.resize(std::max<uint64_t>(key_n, 1));
   if (!wd.empty()) {
     DevBuf<uint32_t> dg(gstart.size()), db(dblk.size());
     MKB_CUDA(cudaMemcpyAsync(dg.get(), gstart.data(), gstart.size() * 4, cudaMemcpyHostToDevice,
@@ -553,14 +564,15 @@ bool prepare_stream2(Context& c, uint32_t mode) {
     f.blks = reinterpret_cast<const Blk*>(p.blk_dev.get());
     f.rowbits = p.rowbits;
     f.b0 = p.b0;
+    f.ob = p.ob;
+    f.om = p.om;
     f.aw = p.aw;
     f.nin = nin;
     f.gpw = GPW;
     f.S = S;
     f.RS = RS;
     f.KS = KS;
-    f.recA = p.recA.get();
-    f.sk = p.sk.get();
+    f.tiles = p.tiles.get();
     f.kperm = p.kperm.get();
     k_fill2<<<static_cast<unsigned>(wd.size()), 256, 0, st>>>(f);
     MKB_LAUNCH();
@@ -584,10 +596,10 @@ bool prepare_stream2(Context& c, uint32_t mode) {
   if (env_int("MKB_DEBUG", 0))
     std::fprintf(stderr,
                  "[mkb] mode %u plan: levels %u%s nin %u aw %u %s blocks %u (split %u,%u,%u,%u) "
-                 "staged %u os %d smem %zu items %u records %llu zero_rows %llu model %.2f cyc/elem\n",
+                 "staged %u os %d outer-in-record %d smem %zu items %u record slots %llu zero_rows %llu model %.2f cyc/elem\n",
                  mode, ni, p.nout ? " (outer)" : "", nin, p.aw,
                  kind,
-                 p.nblocks, split[0], split[1], split[2], split[3], p.k, p.os ? 1 : 0,
+                 p.nblocks, split[0], split[1], split[2], split[3], p.k, p.os ? 1 : 0, p.om ? 1 : 0,
                  p.staged_end, p.nitems, static_cast<unsigned long long>(rec_n),
                  static_cast<unsigned long long>(p.n_zero_rows), model_cost);
   p.ok = true;
@@ -602,9 +614,7 @@ void fill_args(Context& c, uint32_t mode, const float* const* in, float* out, s2
   ModeCopy& mc = c.copies[mode];
   ModeCopy::Stream2& p = mc.s2;
   a = s2::Args{};
-  a.recA2 = reinterpret_cast<const uint2*>(p.recA.get());
-  a.recA4 = reinterpret_cast<const uint4*>(p.recA.get());
-  a.sk = p.sk.get();
+  a.tiles = p.tiles.get();
   a.kperm = p.kperm.get();
   for (uint32_t l = 0; l < p.ni; ++l) a.Yg[l] = in[p.levels[l]];
   a.blks = reinterpret_cast<const Blk*>(p.blk_dev.get());
@@ -627,6 +637,8 @@ void fill_args(Context& c, uint32_t mode, const float* const* in, float* out, s2
   a.b0 = p.b0;
   a.m0 = p.m0;
   a.m1 = p.m1;
+  a.ob = p.ob;
+  a.om = p.om;
   for (uint32_t j = 0; j < 4; ++j) a.stage_off[j] = p.stage_off[j];
   a.outer_off = p.outer_off;
   a.outer_bytes = p.outer_bytes;

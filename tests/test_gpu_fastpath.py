@@ -23,6 +23,7 @@ SHAPES = [
     ([300, 400, 500, 600, 700], 100_000, 32, {"unblocked", "blocked", "partial"}),  # N=5: 16-B records
     ([2482, 2862, 5000, 17], 150_000, 64, {"blocked", "partial"}),    # R=64 (16-lane groups)
     ([40, 50, 60], 20_000, 64, {"partial"}),  # tiny: staging does not pay (cost model)
+    ([17, 300, 2862, 5000], 200_000, 64, {"blocked", "partial"}),  # outer level not staged
 ]
 
 

@@ -34,8 +34,10 @@ print("# ncu --metrics gpu__time_duration.sum --clock-control none (cold-cache, 
 print("# kernel, launches, mean us, total us")
 for k, (cnt, tot) in agg.items():
     print(f"{k}, {cnt}, {tot / cnt:.2f}, {tot:.1f}")
-hot = ("k_stream2", "k_mttkrp_stream", "k_mttkrp_tiles")
+hot = ("k_stream2", "k_sweep2", "k_mttkrp_stream", "k_mttkrp_tiles")
 idx = [i for i, (k, _) in enumerate(launches) if k.startswith(hot)]
+if any(launches[i][0].startswith("k_sweep2") for i in idx[-1:]):
+    nmodes = 1  # the last sweep is one fused launch
 if len(idx) >= nmodes:
     first = idx[-nmodes]
     # include the zeroing launches that precede the first hot launch of the sweep
