@@ -113,7 +113,8 @@ _lib_handle: Optional[C.CDLL] = None
 
 
 def library_path() -> str:
-    return os.path.join(HERE, _LIB_NAME)
+    # MKB_LIB: an alternative build of the same library (kernel-variant experiments)
+    return os.environ.get("MKB_LIB") or os.path.join(HERE, _LIB_NAME)
 
 
 def load_library() -> C.CDLL:

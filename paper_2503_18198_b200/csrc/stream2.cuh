@@ -365,6 +365,9 @@ struct Body {
 // sweep) at 0, the current mode's Args at kArgsOff][staged factor slices][outer factor]
 // [per-warp record rings].
 constexpr uint32_t kHeader = 1024, kArgsOff = 512;
+#ifndef MKB_S2_B
+#define MKB_S2_B 3  // elements per gather batch (8-B records)
+#endif
 
 // Per-thread state that persists across the modes of one launch.
 struct Persist {
@@ -644,7 +647,7 @@ constexpr uint32_t ring_bytes(int G, int NT) {
 
 template <int NI, int NOUT, int K, bool OS, int G, int NT, int MINB>
 void launch_one(const Args& a, unsigned grid, size_t smem, cudaStream_t st) {
-  constexpr int B = 3;
+  constexpr int B = Lay<NI, NOUT>::AW == 2 ? MKB_S2_B : 3;
   auto kern = k_stream2<NI, NOUT, K, OS, G, B, NT, MINB>;
   static bool attr_set = false;  // the attribute is per function, set before first launch
   if (!attr_set) {
@@ -660,7 +663,7 @@ void launch_one(const Args& a, unsigned grid, size_t smem, cudaStream_t st) {
 
 template <int NI, int NOUT, int K, bool OS, int G, int NT, int MINB>
 void launch_sweep_one(const SweepArgs& a, unsigned grid, size_t smem, cudaStream_t st) {
-  constexpr int B = 3;
+  constexpr int B = Lay<NI, NOUT>::AW == 2 ? MKB_S2_B : 3;
   auto kern = k_sweep2<NI, NOUT, K, OS, G, B, NT, MINB>;
   static bool attr_set = false;
   if (!attr_set) {
