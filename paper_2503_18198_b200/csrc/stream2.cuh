@@ -342,22 +342,24 @@ struct Body {
     fetch<B>(RA, 0, rA);
     fetch<B>(RA, B, rB);
     gather_batch<B>(ln, rA, yA);
+    // steady state: no conditions in the body (the last pair is peeled below)
 #pragma unroll 1
-    for (int k = 0; k < NB; k += 2) {
+    for (int k = 0; k < NB - 2; k += 2) {
       uint32_t rC[B][4];
-      gather_batch<B>(ln, rB, yB);                          // batch k+1
-      if (k + 2 < NB) fetch<B>(RA, (k + 2) * B, rC);        // batch k+2 records
-      consume<B>(ln, s, RB, k * B, rA, yA);                 // batch k
-      if (k + 2 < NB) gather_batch<B>(ln, rC, yA);          // batch k+2
-      consume<B>(ln, s, RB, (k + 1) * B, rB, yB);           // batch k+1
-      if (k + 2 < NB) {
-        fetch<B>(RA, (k + 3) * B, rB);                      // batch k+3 records
+      gather_batch<B>(ln, rB, yB);                    // batch k+1
+      fetch<B>(RA, (k + 2) * B, rC);                  // batch k+2 records
+      consume<B>(ln, s, RB, k * B, rA, yA);           // batch k
+      gather_batch<B>(ln, rC, yA);                    // batch k+2
+      consume<B>(ln, s, RB, (k + 1) * B, rB, yB);     // batch k+1
+      fetch<B>(RA, (k + 3) * B, rB);                  // batch k+3 records
 #pragma unroll
-        for (int b = 0; b < B; ++b)
+      for (int b = 0; b < B; ++b)
 #pragma unroll
-          for (int q = 0; q < 4; ++q) rA[b][q] = rC[b][q];
-      }
+        for (int q = 0; q < 4; ++q) rA[b][q] = rC[b][q];
     }
+    gather_batch<B>(ln, rB, yB);                      // batch NB-1
+    consume<B>(ln, s, RB, (NB - 2) * B, rA, yA);
+    consume<B>(ln, s, RB, (NB - 1) * B, rB, yB);
   }
 };
 
