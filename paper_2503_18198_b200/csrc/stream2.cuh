@@ -226,7 +226,8 @@ struct Lane {
 
 // Per-group running state over its range.
 struct Seg {
-  float2 acc0, acc1;
+  float2 acc0, acc1;  // the current row's sum
+  float2 in0, in1;    // outer level: sum over the current outer run, folded in with yo
   float4 yo;
   uint32_t row;
   bool first, head_atomic, all_atomic, bad;  // all_atomic: blocked plan (rows span blocks)
@@ -249,6 +250,8 @@ struct Body {
   static __device__ __forceinline__ float4 outer(const Lane<NIN>& ln, uint32_t sk) {
     return outer_row(ln, sk >> ln.rowbits);
   }
+  // val * Π inner rows, accumulated into the row sum, or (outer level) into the outer run's
+  // sum, which is multiplied by yo once per run (CSF-style: no per-element yo multiply)
   static __device__ __forceinline__ void math(Seg& s, float v, const float4 (&y)[NIN]) {
     float2 t0 = make_float2(y[0].x, y[0].y), t1 = make_float2(y[0].z, y[0].w);
 #pragma unroll
@@ -257,17 +260,28 @@ struct Body {
       t1 = __fmul2_rn(t1, make_float2(y[j].z, y[j].w));
     }
     if constexpr (NOUT > 0) {
-      t0 = __fmul2_rn(t0, make_float2(s.yo.x, s.yo.y));
-      t1 = __fmul2_rn(t1, make_float2(s.yo.z, s.yo.w));
+      s.in0 = __ffma2_rn(t0, make_float2(v, v), s.in0);
+      s.in1 = __ffma2_rn(t1, make_float2(v, v), s.in1);
+    } else {
+      s.acc0 = __ffma2_rn(t0, make_float2(v, v), s.acc0);
+      s.acc1 = __ffma2_rn(t1, make_float2(v, v), s.acc1);
     }
-    s.acc0 = __ffma2_rn(t0, make_float2(v, v), s.acc0);
-    s.acc1 = __ffma2_rn(t1, make_float2(v, v), s.acc1);
+  }
+  // close the outer run: row sum += run sum (.) yo
+  static __device__ __forceinline__ void fold(Seg& s) {
+    if constexpr (NOUT > 0) {
+      s.acc0 = __ffma2_rn(s.in0, make_float2(s.yo.x, s.yo.y), s.acc0);
+      s.acc1 = __ffma2_rn(s.in1, make_float2(s.yo.z, s.yo.w), s.acc1);
+      s.in0 = make_float2(0.f, 0.f);
+      s.in1 = s.in0;
+    }
   }
   // A flagged element: on a row change (P0 bit 30) read its slow key, flush the finished row
   // (if any) and start the next; reload the outer row from the record's outer field (or the
   // slow key when the field did not fit).
   static __device__ __forceinline__ void flagged(const Lane<NIN>& ln, Seg& s, uint32_t p,
                                                  const uint32_t* key) {
+    fold(s);  // the outer run (if any) ends here
     uint32_t sk = 0;
     if (p & 0x40000000u) {
       sk = *key;
@@ -282,7 +296,7 @@ struct Body {
       s.acc0 = make_float2(0.f, 0.f);
       s.acc1 = s.acc0;
     }
-    if constexpr (NOUT > 0) {
+    if constexpr (NOUT > 0) {  // the next run's outer row: needed only at its fold
       if (ln.om) {
         s.yo = outer_row(ln, (p >> ln.ob) & ln.om);
       } else {
@@ -489,6 +503,8 @@ __device__ __forceinline__ bool mode_body(const Args& a, uint8_t* smem, Persist&
     Seg s;
     s.acc0 = make_float2(0.f, 0.f);
     s.acc1 = s.acc0;
+    s.in0 = s.acc0;
+    s.in1 = s.acc0;
     s.yo = make_float4(1.f, 1.f, 1.f, 1.f);
     s.row = 0xffffffffu;
     s.first = true;
@@ -508,6 +524,7 @@ __device__ __forceinline__ bool mode_body(const Args& a, uint8_t* smem, Persist&
       if (lane == 0 && t + 2 < d.tiles) issue(t + 2, st);
     }
     // the group's last run
+    Bd::fold(s);
     const bool have = s.row != 0xffffffffu;
     const bool last_atomic = blocked || ((d.flags >> (4 + gw)) & 1u) || (s.first && s.head_atomic);
     if (have) s.bad |= !isfinite(s.acc0.x + s.acc0.y + s.acc1.x + s.acc1.y);
