@@ -3,15 +3,20 @@
 // (Kolda & Bader) and is pinned against our own fp64 restatement
 // (oracle/als.py) — parity for this subsystem is "unpinned" against the reference.
 //
-// Per mode d of an iteration:
-//   M      = MTTKRP_d(Y_0..Y_{N-1})             (spMTTKRP kernel, chained factors)
+// Per mode d of an iteration: the spMTTKRP, then ONE cooperative launch (k_als_update):
+//   P      = Mᵀ M                               (phase 1: per-CTA partials, fp64 atomics)
+//   -- grid barrier --
 //   V      = ⊛_{w≠d} G_w,  G_w = Y_wᵀ Y_w      (R×R, fp64, Grams kept resident)
-//   Y_d    = M V⁻¹                              (Cholesky in SMEM; Jacobi pseudo-inverse
-//                                                 fallback when V is not positive definite)
-//   λ_r    = ||Y_d[:,r]||₂ (1 when zero);  Y_d[:,r] /= λ_r;  G_d rescaled
+//   V⁻¹                                         (phase 2, every CTA redundantly: Gauss-Jordan
+//                                                 in SMEM; Jacobi pseudo-inverse fallback when a
+//                                                 pivot shows V is not positive definite)
+//   Gram of M V⁻¹ = V⁻ᵀ P V⁻¹ (algebraically, no pass over the rows)
+//   λ_r    = its diagonal's square root (1 when zero);  G_d = that Gram / λλᵀ (CTA 0)
+//   Y_d    = M (V⁻¹ diag(1/λ))                  (phase 3, each CTA its rows)
 // After the last mode:
 //   fit    = 1 - sqrt(max(0, ||X||² - 2⟨X, X̂⟩ + ||X̂||²)) / ||X||
-//   ⟨X,X̂⟩ = Σ_r λ_r Σ_i M_{N-1}[i,r] Y_{N-1}[i,r];   ||X̂||² = λᵀ (⊛_w G_w) λ
+//   ⟨X,X̂⟩ = Σ_r λ_r Σ_i M_{N-1}[i,r] Y_{N-1}[i,r] = trace(P V⁻¹),
+//   ||X̂||² = λᵀ (⊛_w G_w) λ — both written by the last mode's update.
 #include <algorithm>
 #include <cmath>
 #include <vector>
@@ -54,85 +59,83 @@ __global__ void __launch_bounds__(256) k_gram(const float* __restrict__ Y, uint3
   }
 }
 
-// One CTA: V = ⊛_{w≠d} G_w; Cholesky V = L Lᵀ; Vinv = L⁻ᵀ L⁻¹ (fp64 in SMEM), written as
-// fp32 for the row apply.  Falls back to a Jacobi eigen pseudo-inverse when a pivot is
-// not positive.  status[0] = 1 when the fallback ran.
-__global__ void __launch_bounds__(256) k_solve(const double* __restrict__ grams, uint32_t n,
-                                               uint32_t d, uint32_t R, float* __restrict__ vinv,
-                                               int* status) {
-  extern __shared__ double dsm[];
-  double* V = dsm;            // R x R
-  double* L = dsm + R * R;    // R x R
-  double* W = dsm + 2 * R * R;  // R x R (inverse of L / eigenvectors)
+// ---- fused per-mode update: one cooperative launch --------------------------------------
+struct UpdArgs {
+  const float* M;      // MTTKRP output, rows x R
+  float* Y;            // updated factor, rows x R
+  uint32_t rows, R, n, d;
+  double* grams;       // N x R x R
+  double* P;           // this mode's MᵀM accumulator (zero on entry)
+  double* P_next;      // the next mode's accumulator (zeroed here)
+  float* lambda;
+  double* scalars;     // [⟨X,X̂⟩, ||X̂||²] (last mode)
+  int last;
+  int* status;
+  unsigned int* bar;   // grid barrier counter (monotonic)
+  unsigned int target; // barrier target for this launch
+};
+
+// Block-level V⁻¹ of the symmetric positive definite V = ⊛_{w≠d} G_w by Gauss-Jordan on
+// [V | I] (fp64, SMEM); Jacobi pseudo-inverse when a pivot <= 1e-12 max diag(V).  On return
+// A[:, R:] holds the (pseudo-)inverse.  Returns whether the fallback ran.
+__device__ bool block_inverse(const double* __restrict__ grams, uint32_t n, uint32_t d, uint32_t R,
+                              double* A, double* T, double* fac, double* scratch) {
+  const uint32_t RR = R * R, W2 = 2 * R;
   __shared__ int bad;
-  const uint32_t RR = R * R;
+  __shared__ double vmax;
+  for (uint32_t p = threadIdx.x; p < RR; p += blockDim.x) {
+    double v = 1.0;
+    for (uint32_t w = 0; w < n; ++w)
+      if (w != d) v *= grams[static_cast<size_t>(w) * RR + p];
+    const uint32_t r = p / R, c = p % R;
+    A[r * W2 + c] = v;
+    A[r * W2 + R + c] = r == c ? 1.0 : 0.0;
+  }
+  if (threadIdx.x == 0) bad = 0;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    double m = 0.0;
+    for (uint32_t j = threadIdx.x; j < R; j += 32) m = fmax(m, A[j * W2 + j]);
+    for (int o = 16; o; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if (threadIdx.x == 0) vmax = m;
+  }
+  __syncthreads();
+  for (uint32_t j = 0; j < R; ++j) {
+    const double piv = A[j * W2 + j];
+    if (!(piv > 1e-12 * vmax)) {
+      if (threadIdx.x == 0) bad = 1;
+      break;
+    }
+    const double inv = 1.0 / piv;
+    double* prow = scratch;  // the normalised pivot row (2R <= R*R)
+    for (uint32_t c = threadIdx.x; c < W2; c += blockDim.x) prow[c] = A[j * W2 + c] * inv;
+    for (uint32_t i = threadIdx.x; i < R; i += blockDim.x) fac[i] = A[i * W2 + j];
+    __syncthreads();
+    for (uint32_t q = threadIdx.x; q < R * W2; q += blockDim.x) {
+      const uint32_t i = q / W2, c = q % W2;
+      A[q] = i == j ? prow[c] : A[q] - fac[i] * prow[c];
+    }
+    __syncthreads();
+  }
+  __syncthreads();
+  if (!bad) return false;
+  // cyclic Jacobi eigen-decomposition of V: T = V (diagonalised in place), Wv = eigenvectors
+  double* V = T;
+  double* Wv = scratch;
   for (uint32_t p = threadIdx.x; p < RR; p += blockDim.x) {
     double v = 1.0;
     for (uint32_t w = 0; w < n; ++w)
       if (w != d) v *= grams[static_cast<size_t>(w) * RR + p];
     V[p] = v;
-    L[p] = 0.0;
-    W[p] = 0.0;
-  }
-  __shared__ double vmax;
-  if (threadIdx.x == 0) {
-    bad = 0;
-    vmax = 0.0;
-    for (uint32_t j = 0; j < R; ++j) vmax = fmax(vmax, V[j * R + j]);
-  }
-  __syncthreads();
-  // right-looking Cholesky, column by column; a pivot <= 1e-12 max diag(V) = not SPD
-  for (uint32_t j = 0; j < R; ++j) {
-    if (threadIdx.x == 0) {
-      double s = V[j * R + j];
-      for (uint32_t k = 0; k < j; ++k) s -= L[j * R + k] * L[j * R + k];
-      if (!(s > 1e-12 * vmax)) bad = 1;
-      L[j * R + j] = s > 0.0 ? sqrt(s) : 1.0;
-    }
-    __syncthreads();
-    for (uint32_t i = j + 1 + threadIdx.x; i < R; i += blockDim.x) {
-      double s = V[i * R + j];
-      for (uint32_t k = 0; k < j; ++k) s -= L[i * R + k] * L[j * R + k];
-      L[i * R + j] = s / L[j * R + j];
-    }
-    __syncthreads();
-  }
-  if (!bad) {
-    // W = L⁻¹ (lower), column c solved by one thread
-    for (uint32_t c = threadIdx.x; c < R; c += blockDim.x) {
-      for (uint32_t i = 0; i < R; ++i) {
-        double s = (i == c) ? 1.0 : 0.0;
-        for (uint32_t k = c; k < i; ++k) s -= L[i * R + k] * W[k * R + c];
-        W[i * R + c] = i < c ? 0.0 : s / L[i * R + i];
-      }
-    }
-    __syncthreads();
-    // Vinv = Wᵀ W
-    for (uint32_t p = threadIdx.x; p < RR; p += blockDim.x) {
-      const uint32_t r = p / R, s = p % R;
-      double a = 0.0;
-      for (uint32_t k = max(r, s); k < R; ++k) a += W[k * R + r] * W[k * R + s];
-      vinv[p] = static_cast<float>(a);
-    }
-    if (threadIdx.x == 0) status[0] = 0;
-    return;
-  }
-  // Fallback: cyclic Jacobi eigen-decomposition of V (in place), W = eigenvectors,
-  // pinv = W diag(1/λ, λ > 1e-12 λ_max) Wᵀ.
-  __syncthreads();
-  for (uint32_t p = threadIdx.x; p < RR; p += blockDim.x) {
-    V[p] = 1.0;
-    for (uint32_t w = 0; w < n; ++w)
-      if (w != d) V[p] *= grams[static_cast<size_t>(w) * RR + p];
-    W[p] = (p / R == p % R) ? 1.0 : 0.0;
+    Wv[p] = (p / R == p % R) ? 1.0 : 0.0;
   }
   __syncthreads();
   __shared__ double cs[2];
   for (int sweep = 0; sweep < 30; ++sweep) {
-    for (uint32_t pidx = 0; pidx + 1 < R; ++pidx) {
-      for (uint32_t q = pidx + 1; q < R; ++q) {
+    for (uint32_t pi = 0; pi + 1 < R; ++pi) {
+      for (uint32_t q = pi + 1; q < R; ++q) {
         if (threadIdx.x == 0) {
-          const double app = V[pidx * R + pidx], aqq = V[q * R + q], apq = V[pidx * R + q];
+          const double app = V[pi * R + pi], aqq = V[q * R + q], apq = V[pi * R + q];
           double c = 1.0, s = 0.0;
           if (fabs(apq) > 1e-300) {
             const double tau = (aqq - app) / (2.0 * apq);
@@ -146,19 +149,19 @@ __global__ void __launch_bounds__(256) k_solve(const double* __restrict__ grams,
         __syncthreads();
         const double c = cs[0], s = cs[1];
         if (s != 0.0) {
-          for (uint32_t k = threadIdx.x; k < R; k += blockDim.x) {  // rows p, q
-            const double vp = V[pidx * R + k], vq = V[q * R + k];
-            V[pidx * R + k] = c * vp - s * vq;
+          for (uint32_t k = threadIdx.x; k < R; k += blockDim.x) {
+            const double vp = V[pi * R + k], vq = V[q * R + k];
+            V[pi * R + k] = c * vp - s * vq;
             V[q * R + k] = s * vp + c * vq;
           }
           __syncthreads();
-          for (uint32_t k = threadIdx.x; k < R; k += blockDim.x) {  // columns p, q
-            const double vp = V[k * R + pidx], vq = V[k * R + q];
-            V[k * R + pidx] = c * vp - s * vq;
+          for (uint32_t k = threadIdx.x; k < R; k += blockDim.x) {
+            const double vp = V[k * R + pi], vq = V[k * R + q];
+            V[k * R + pi] = c * vp - s * vq;
             V[k * R + q] = s * vp + c * vq;
-            const double wp = W[k * R + pidx], wq = W[k * R + q];
-            W[k * R + pidx] = c * wp - s * wq;
-            W[k * R + q] = s * wp + c * wq;
+            const double wp = Wv[k * R + pi], wq = Wv[k * R + q];
+            Wv[k * R + pi] = c * wp - s * wq;
+            Wv[k * R + q] = s * wp + c * wq;
           }
         }
         __syncthreads();
@@ -168,81 +171,150 @@ __global__ void __launch_bounds__(256) k_solve(const double* __restrict__ grams,
   double lmax = 0.0;
   for (uint32_t k = 0; k < R; ++k) lmax = fmax(lmax, fabs(V[k * R + k]));
   for (uint32_t p = threadIdx.x; p < RR; p += blockDim.x) {
-    const uint32_t r = p / R, s = p % R;
+    const uint32_t r = p / R, c = p % R;
     double a = 0.0;
     for (uint32_t k = 0; k < R; ++k) {
-      const double lam = V[k * R + k];
-      if (fabs(lam) > 1e-12 * lmax) a += W[r * R + k] * W[s * R + k] / lam;
+      const double l = V[k * R + k];
+      if (fabs(l) > 1e-12 * lmax) a += Wv[r * R + k] * Wv[c * R + k] / l;
     }
-    vinv[p] = static_cast<float>(a);
+    A[r * W2 + R + c] = a;
   }
-  if (threadIdx.x == 0) status[0] = 1;
+  __syncthreads();
+  return true;
 }
 
-// Y[i,:] = M[i,:] · Vinv  (rows staged in SMEM, Vinv in SMEM)
-__global__ void __launch_bounds__(256) k_apply(const float* __restrict__ M, uint32_t rows,
-                                               uint32_t R, const float* __restrict__ vinv,
-                                               float* __restrict__ Y) {
-  extern __shared__ float sm[];
-  float* Vs = sm;          // R x R
-  float* Ms = sm + R * R;  // kGramRows x R
-  for (uint32_t p = threadIdx.x; p < R * R; p += blockDim.x) Vs[p] = vinv[p];
-  for (uint32_t r0 = blockIdx.x * kGramRows; r0 < rows; r0 += gridDim.x * kGramRows) {
-    const uint32_t nr = rows - r0 < kGramRows ? rows - r0 : kGramRows;
+// Phase 1: P += MᵀM over this CTA's rows; grid barrier; phase 2 (every CTA, redundantly):
+// V⁻¹, the Gram of M V⁻¹ = V⁻ᵀ P V⁻¹, λ, S = V⁻¹ diag(1/λ) (CTA 0 also writes G_d, λ and
+// the fit terms); phase 3: Y = M S over this CTA's rows.
+template <int RT>  // RT > 0: the rank at compile time (16 / 32 / 64); 0: runtime u.R <= 64
+__global__ void __launch_bounds__(256) k_als_update(const UpdArgs u) {
+  extern __shared__ double dsm[];
+  constexpr int RMAX = RT ? RT : 64;
+  const uint32_t R = RT ? RT : u.R, RR = R * R, W2 = 2 * R;
+  double* A = dsm;             // R x 2R
+  double* T = A + 2 * RR;      // R x R
+  double* Pm = T + RR;         // R x R
+  double* scratch = Pm + RR;   // R x R (Jacobi eigenvectors)
+  double* lam = scratch + RR;  // R
+  double* fac = lam + R;       // R
+  float* S = reinterpret_cast<float*>(fac + R);  // R x R
+  float* tile = S + RR;                          // kGramRows x R
+  const uint32_t r0 = static_cast<uint32_t>(static_cast<uint64_t>(u.rows) * blockIdx.x / gridDim.x);
+  const uint32_t r1 = static_cast<uint32_t>(static_cast<uint64_t>(u.rows) * (blockIdx.x + 1) / gridDim.x);
+  // phase 1
+  {
+    constexpr int PER = (RMAX * RMAX + 255) / 256;
+    double acc[PER];
+#pragma unroll
+    for (int k = 0; k < PER; ++k) acc[k] = 0.0;
+    for (uint32_t b = r0; b < r1; b += kGramRows) {
+      const uint32_t nr = min(r1 - b, static_cast<uint32_t>(kGramRows));
+      __syncthreads();
+      for (uint32_t i = threadIdx.x; i < nr * R; i += blockDim.x)
+        tile[i] = u.M[static_cast<size_t>(b) * R + i];
+      __syncthreads();
+#pragma unroll
+      for (int k = 0; k < PER; ++k) {
+        const uint32_t p = threadIdx.x + k * 256;
+        if (p < RR) {
+          const uint32_t r = p / R, s = p % R;
+          double a = 0.0;
+          for (uint32_t i = 0; i < nr; ++i)
+            a += static_cast<double>(tile[i * R + r]) * static_cast<double>(tile[i * R + s]);
+          acc[k] += a;
+        }
+      }
+    }
+    if (r1 > r0) {
+#pragma unroll
+      for (int k = 0; k < PER; ++k) {
+        const uint32_t p = threadIdx.x + k * 256;
+        if (p < RR) atomicAdd(&u.P[p], acc[k]);
+      }
+    }
+  }
+  // grid barrier (cooperative launch: every CTA is resident)
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    atomicAdd(u.bar, 1u);
+    unsigned int v;
+    do {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(u.bar) : "memory");
+    } while (static_cast<int>(v - u.target) < 0);
+  }
+  __syncthreads();
+  // phase 2
+  for (uint32_t p = threadIdx.x; p < RR; p += blockDim.x) Pm[p] = __ldcg(&u.P[p]);
+  const bool fell_back = block_inverse(u.grams, u.n, u.d, R, A, T, fac, scratch);
+  for (uint32_t p = threadIdx.x; p < RR; p += blockDim.x) {  // T = P V⁻¹
+    const uint32_t r = p / R, c = p % R;
+    double a = 0.0;
+#pragma unroll 8
+    for (uint32_t k = 0; k < R; ++k) a += Pm[r * R + k] * A[k * W2 + R + c];
+    T[p] = a;
+  }
+  __syncthreads();
+  for (uint32_t r = threadIdx.x; r < R; r += blockDim.x) {
+    double a = 0.0;
+    for (uint32_t k = 0; k < R; ++k) a += A[k * W2 + R + r] * T[k * R + r];
+    const double l = sqrt(fmax(a, 0.0));
+    lam[r] = l > 0.0 ? l : 1.0;
+  }
+  __syncthreads();
+  for (uint32_t p = threadIdx.x; p < RR; p += blockDim.x)
+    S[p] = static_cast<float>(A[(p / R) * W2 + R + p % R] / lam[p % R]);
+  if (blockIdx.x == 0) {
+    double* G = u.grams + static_cast<size_t>(u.d) * RR;
+    for (uint32_t p = threadIdx.x; p < RR; p += blockDim.x) {
+      const uint32_t r = p / R, c = p % R;
+      double a = 0.0;
+      for (uint32_t k = 0; k < R; ++k) a += A[k * W2 + R + r] * T[k * R + c];
+      G[p] = a / (lam[r] * lam[c]);
+      u.P_next[p] = 0.0;
+    }
+    for (uint32_t r = threadIdx.x; r < R; r += blockDim.x) u.lambda[r] = static_cast<float>(lam[r]);
+    __syncthreads();
+    if (u.last && threadIdx.x < 32) {
+      // ⟨X, X̂⟩ = Σ_r λ_r (P S)_rr = trace(P V⁻¹);  ||X̂||² = λᵀ (⊛_w G_w) λ
+      double inner = 0.0, model = 0.0;
+      for (uint32_t r = threadIdx.x; r < R; r += 32) inner += T[r * R + r];
+      for (uint32_t p = threadIdx.x; p < RR; p += 32) {
+        double v = lam[p / R] * lam[p % R];
+        for (uint32_t w = 0; w < u.n; ++w) v *= u.grams[static_cast<size_t>(w) * RR + p];
+        model += v;
+      }
+      for (int o = 16; o; o >>= 1) {
+        inner += __shfl_xor_sync(0xffffffffu, inner, o);
+        model += __shfl_xor_sync(0xffffffffu, model, o);
+      }
+      if (threadIdx.x == 0) {
+        u.scalars[0] = inner;
+        u.scalars[1] = model;
+      }
+    }
+    if (threadIdx.x == 0) u.status[0] = fell_back ? 1 : 0;
+  }
+  __syncthreads();
+  // phase 3: Y = M S
+  for (uint32_t b = r0; b < r1; b += kGramRows) {
+    const uint32_t nr = min(r1 - b, static_cast<uint32_t>(kGramRows));
     __syncthreads();
     for (uint32_t i = threadIdx.x; i < nr * R; i += blockDim.x)
-      Ms[i] = M[static_cast<size_t>(r0) * R + i];
+      tile[i] = u.M[static_cast<size_t>(b) * R + i];
     __syncthreads();
     for (uint32_t p = threadIdx.x; p < nr * R; p += blockDim.x) {
       const uint32_t i = p / R, r = p % R;
       float a = 0.f;
-      for (uint32_t s = 0; s < R; ++s) a = fmaf(Ms[i * R + s], Vs[s * R + r], a);
-      Y[static_cast<size_t>(r0) * R + p] = a;
+#pragma unroll 8
+      for (uint32_t s2 = 0; s2 < R; ++s2) a = fmaf(tile[i * R + s2], S[s2 * R + r], a);
+      u.Y[static_cast<size_t>(b) * R + p] = a;
     }
   }
 }
 
-// λ_r = sqrt(G[r][r]) (1 when zero); G[r][s] /= λ_r λ_s
-__global__ void k_lambda(double* __restrict__ G, uint32_t R, float* __restrict__ lambda) {
-  __shared__ double lam[256];
-  for (uint32_t r = threadIdx.x; r < R; r += blockDim.x) {
-    const double v = sqrt(fmax(G[r * R + r], 0.0));
-    lam[r] = v > 0.0 ? v : 1.0;
-    lambda[r] = static_cast<float>(lam[r]);
-  }
-  __syncthreads();
-  for (uint32_t p = threadIdx.x; p < R * R; p += blockDim.x) G[p] /= lam[p / R] * lam[p % R];
-}
-
-__global__ void k_scale_cols(float* __restrict__ Y, size_t count, uint32_t R,
-                             const float* __restrict__ lambda) {
-  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < count;
-       i += static_cast<size_t>(gridDim.x) * blockDim.x)
-    Y[i] = Y[i] / lambda[i % R];
-}
-
-// out[0] += Σ_i Σ_r λ_r M[i,r] Y[i,r]  (fp64)
-__global__ void k_inner(const float* __restrict__ M, const float* __restrict__ Y, size_t count,
-                        uint32_t R, const float* __restrict__ lambda, double* out) {
-  double a = 0.0;
-  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < count;
-       i += static_cast<size_t>(gridDim.x) * blockDim.x)
-    a += static_cast<double>(M[i]) * static_cast<double>(Y[i]) * lambda[i % R];
-  for (int o = 16; o; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
-  if ((threadIdx.x & 31) == 0) atomicAdd(out, a);
-}
-
-// out[1] = λᵀ (⊛_w G_w) λ
-__global__ void k_model_norm(const double* __restrict__ grams, uint32_t n, uint32_t R,
-                             const float* __restrict__ lambda, double* out) {
-  double a = 0.0;
-  for (uint32_t p = threadIdx.x; p < R * R; p += blockDim.x) {
-    double v = static_cast<double>(lambda[p / R]) * static_cast<double>(lambda[p % R]);
-    for (uint32_t w = 0; w < n; ++w) v *= grams[static_cast<size_t>(w) * R * R + p];
-    a += v;
-  }
-  for (int o = 16; o; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
-  if ((threadIdx.x & 31) == 0) atomicAdd(out + 1, a);
+size_t upd_smem(uint32_t R) {
+  return sizeof(double) * (5 * R * R + 2 * R) + sizeof(float) * (R * R + kGramRows * R);
 }
 
 int blocks_for(uint64_t rows, int sms) {
@@ -274,49 +346,59 @@ void als_prepare(Context& c) {
   c.lambda.resize(R);
   c.als_scalars.resize(2);
   c.als_status.resize(1);
+  if (c.mtm.size() < 2 * static_cast<size_t>(R) * R) {  // two MᵀM accumulators (ping-pong)
+    c.mtm.resize(2 * static_cast<size_t>(R) * R);
+    MKB_CUDA(cudaMemsetAsync(c.mtm.get(), 0, 2 * sizeof(double) * R * R, c.stream));
+  }
+  if (!c.als_bar.get()) {
+    c.als_bar.resize(1);
+    MKB_CUDA(cudaMemsetAsync(c.als_bar.get(), 0, sizeof(unsigned int), c.stream));
+    c.als_bar_count = 0;
+  }
 }
 
-// Y_d = M_d V⁻¹ with V = ⊛_{w≠d} G_w, then G_d and the column normalisation.  M_d is the
-// (possibly all-gathered) MTTKRP output in c.outputs[d].
+// Y_d = M_d V⁻¹ diag(1/λ) with V = ⊛_{w≠d} G_w; G_d, λ and (last mode) the fit terms.
+// M_d is the (possibly all-gathered) MTTKRP output in c.outputs[d].
 void als_update_mode(Context& c, uint32_t d) {
   als_prepare(c);
   const uint32_t R = c.rank, n = c.n;
   cudaStream_t st = c.stream;
-  const size_t solve_smem = 3 * sizeof(double) * R * R;
-  const size_t apply_smem = sizeof(float) * (R * R + kGramRows * R);
-  static int smem_set[64] = {};
-  if (!smem_set[c.device & 63]) {  // up to 3 x 64 x 64 doubles = 96 KB
-    MKB_CUDA(cudaFuncSetAttribute(k_solve, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  3 * 64 * 64 * static_cast<int>(sizeof(double))));
-    smem_set[c.device & 63] = 1;
-  }
-  k_solve<<<1, 256, solve_smem, st>>>(c.gram.get(), n, d, R, c.solve.get(), c.als_status.get());
-  MKB_LAUNCH();
-  k_apply<<<blocks_for(c.dims[d], c.num_sms), 256, apply_smem, st>>>(
-      c.outputs[d].get(), c.dims[d], R, c.solve.get(), c.factors[d].get());
-  MKB_LAUNCH();
-  gram_of(c, d);
-  double* G = c.gram.get() + static_cast<size_t>(d) * R * R;
-  k_lambda<<<1, 256, 0, st>>>(G, R, c.lambda.get());
-  MKB_LAUNCH();
-  const size_t cnt = static_cast<size_t>(c.dims[d]) * R;
-  k_scale_cols<<<std::max(1, std::min<int>(static_cast<int>((cnt + 255) / 256), c.num_sms * 8)),
-                 256, 0, st>>>(c.factors[d].get(), cnt, R, c.lambda.get());
-  MKB_LAUNCH();
+  UpdArgs u{};
+  u.M = c.outputs[d].get();
+  u.Y = c.factors[d].get();
+  u.rows = c.dims[d];
+  u.R = R;
+  u.n = n;
+  u.d = d;
+  u.grams = c.gram.get();
+  u.P = c.mtm.get() + static_cast<size_t>(c.als_epoch & 1) * R * R;
+  u.P_next = c.mtm.get() + static_cast<size_t>((c.als_epoch + 1) & 1) * R * R;
+  u.lambda = c.lambda.get();
+  u.scalars = c.als_scalars.get();
+  u.last = d + 1 == n ? 1 : 0;
+  u.status = c.als_status.get();
+  u.bar = c.als_bar.get();
+  const unsigned grid = static_cast<unsigned>(std::min<uint64_t>(
+      c.num_sms, std::max<uint64_t>(1, (u.rows + kGramRows - 1) / kGramRows)));
+  u.target = (c.als_bar_count += grid);
+  ++c.als_epoch;
+  auto go = [&](auto kern, size_t smem) {
+    MKB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(smem)));
+    void* params[] = {&u};
+    MKB_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(kern), dim3(grid),
+                                         dim3(256), params, smem, st));
+  };
+  if (R == 16) go(k_als_update<16>, upd_smem(R));
+  else if (R == 32) go(k_als_update<32>, upd_smem(R));
+  else if (R == 64) go(k_als_update<64>, upd_smem(R));
+  else go(k_als_update<0>, upd_smem(R));
 }
 
-// fit after the last mode (its MTTKRP output is still in c.outputs[N-1])
+// fit after the last mode: the last update wrote [⟨X,X̂⟩, ||X̂||²]
 void als_fit(Context& c, double* fit, float* lambda_host) {
-  const uint32_t R = c.rank, n = c.n, last = n - 1;
+  const uint32_t R = c.rank;
   cudaStream_t st = c.stream;
-  MKB_CUDA(cudaMemsetAsync(c.als_scalars.get(), 0, 2 * sizeof(double), st));
-  const size_t cnt = static_cast<size_t>(c.dims[last]) * R;
-  k_inner<<<std::max(1, std::min<int>(static_cast<int>((cnt + 255) / 256), c.num_sms * 4)), 256, 0,
-            st>>>(c.outputs[last].get(), c.factors[last].get(), cnt, R, c.lambda.get(),
-                  c.als_scalars.get());
-  MKB_LAUNCH();
-  k_model_norm<<<1, 256, 0, st>>>(c.gram.get(), n, R, c.lambda.get(), c.als_scalars.get());
-  MKB_LAUNCH();
   double sc[2];
   MKB_CUDA(cudaMemcpyAsync(sc, c.als_scalars.get(), sizeof sc, cudaMemcpyDeviceToHost, st));
   if (lambda_host)

@@ -130,6 +130,10 @@ struct Context {
 
   // CPD-ALS state
   DevBuf<double> gram;    // N x R x R (fp64)
+  DevBuf<double> mtm;     // 2 x R x R: MᵀM accumulators (fp64, ping-pong, zero between uses)
+  DevBuf<unsigned int> als_bar;  // grid barrier counter of the fused update (monotonic)
+  unsigned int als_bar_count = 0;
+  uint64_t als_epoch = 0;
   DevBuf<float> solve;    // R x R inverse of V (fp32 for the row apply)
   DevBuf<float> lambda;   // R
   DevBuf<double> als_scalars;

@@ -384,6 +384,10 @@ constexpr uint32_t kHeader = 1024, kArgsOff = 512;
 #ifndef MKB_S2_B
 #define MKB_S2_B 3  // elements per gather batch (8-B records)
 #endif
+#ifndef MKB_S2_NT
+#define MKB_S2_NT 512  // threads per CTA (one CTA per SM)
+#endif
+constexpr int kNT = MKB_S2_NT;
 
 // Per-thread state that persists across the modes of one launch.
 struct Persist {
@@ -703,9 +707,9 @@ void launch_k(const A& a, uint32_t K, unsigned grid, size_t smem, cudaStream_t s
   auto go = [&](auto kc) {
     constexpr int KK = decltype(kc)::value;
     if constexpr (std::is_same_v<A, SweepArgs>)
-      launch_sweep_one<NI, NOUT, KK, OS, G, 512, 1>(a, grid, smem, st);
+      launch_sweep_one<NI, NOUT, KK, OS, G, kNT, 1>(a, grid, smem, st);
     else
-      launch_one<NI, NOUT, KK, OS, G, 512, 1>(a, grid, smem, st);
+      launch_one<NI, NOUT, KK, OS, G, kNT, 1>(a, grid, smem, st);
   };
   if (K == 0) return go(std::integral_constant<int, 0>{});
   if constexpr (NIN >= 1)

@@ -292,7 +292,7 @@ bool prepare_stream2(Context& c, uint32_t mode) {
   //      flush = 32 per atomic row flush: every (block, row) pair of a blocked plan
   //      stage = per CTA item: staged slice bytes / 85 B per SM-cycle + a ~6000-cycle stall
   //    cost = LSU + L2 + flush + stage (fitted to the measured cfg2 / cfg3 / cfg5 plans).
-  const size_t ring = s2::ring_bytes_rt(p.aw, G, 512);
+  const size_t ring = s2::ring_bytes_rt(p.aw, G, s2::kNT);
   size_t budget = s2::kMaxDynSmem - ring - s2::kHeader;
   const bool stage_on = env_int("MKB_STAGE", 1) != 0;
   const bool block_on = env_int("MKB_BLOCK", 1) != 0 && !sharded;
@@ -445,7 +445,7 @@ bool prepare_stream2(Context& c, uint32_t mode) {
   //    boundaries into items; an item's elements are split evenly over the CTA's lane groups;
   //    a warp's groups stream chunk-interleaved records.
   const uint32_t S = s2::seg_len(p.aw), RS = s2::rec_stride(p.aw), KS = s2::key_stride(p.aw);
-  const uint32_t NW = 16, GPW = 32 / G, NG = NW * GPW;
+  const uint32_t NW = s2::kNT / 32, GPW = 32 / G, NG = NW * GPW;
   const unsigned grid = static_cast<unsigned>(c.num_sms);
   const uint64_t E0 = p.blocked ? 0 : mc.shard_e0, E1 = p.blocked ? nnz : mc.shard_e1;
   std::vector<WDesc> wd;
@@ -683,7 +683,7 @@ bool launch_stream2(Context& c, uint32_t mode, const float* const* in, float* ou
   uint32_t* sw = sync_words(c);
   s2::Args a;
   fill_args(c, mode, in, out, a, sw, sw + 2);
-  const size_t smem = p.staged_end + s2::ring_bytes_rt(p.aw, G, 512);
+  const size_t smem = p.staged_end + s2::ring_bytes_rt(p.aw, G, s2::kNT);
   const unsigned grid = p.grid;
   switch (c.n * 100 + G) {
     case 308: stream2_launch_n3_g8(a, p.nout, p.os, p.k, grid, smem, st); break;
@@ -712,7 +712,7 @@ bool launch_sweep2(Context& c, const float* const* in, float* const* outs) {
     if (p.nitems == 0 || mc.shard_e1 <= mc.shard_e0) return false;
     if (p.nout != p0.nout || p.os != p0.os || p.k != p0.k || p.aw != p0.aw || p.grid != p0.grid)
       return false;
-    smem = std::max(smem, p.staged_end + s2::ring_bytes_rt(p.aw, G, 512));
+    smem = std::max(smem, p.staged_end + s2::ring_bytes_rt(p.aw, G, s2::kNT));
   }
   uint32_t* sw = sync_words(c);
   static_assert(sizeof(s2::SweepArgs) <= 32000, "kernel parameter space");
