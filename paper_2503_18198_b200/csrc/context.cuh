@@ -61,11 +61,16 @@ struct ModeCopy {
   // kernel, 2 generic tile kernel; keyed by factor rank and shard range
   int fast_kernel = -1;
   uint32_t fast_rank = 0;
+  // level-ordered plan autotune: staged-level count to plan for (-1: cost model), and the
+  // timed milliseconds of the best plan per staged-level count (< 0: none)
+  int s2_force_k = -1;
+  float s2_ms[5] = {-1.f, -1.f, -1.f, -1.f, -1.f};
   uint64_t fast_e0 = ~0ull, fast_e1 = ~0ull;
   // level-ordered, shared-memory-blocked records of the streaming kernel (stream2_plan.cu),
   // built per (factor rank, shard range) on first use
   struct Stream2 {
     bool tried = false, ok = false;
+    int k_req = -1;                            // requested staged-level count (-1: model)
     uint32_t rank = 0;
     uint64_t key_e0 = ~0ull, key_e1 = ~0ull;  // shard range the plan was built for
     uint32_t ni = 0, nout = 0, k = 0, aw = 2;  // input levels, outer levels, staged levels

@@ -375,6 +375,59 @@ void flush_l2(Context& c) {
 // §4.2).  The first fast launch of a mode times each applicable candidate on the actual
 // inputs (after one warm-up launch each, L2 flushed in between) and keeps the fastest;
 // MKB_FAST_KERNEL = s2 | stream | tiles forces one.
+// Device time of one launch, L2 flushed first (min of two runs after a warm-up launch).
+template <class F>
+static float time_launch(Context& c, F&& run) {
+  cudaStream_t st = c.stream;
+  cudaEvent_t ev[2];
+  for (auto& x : ev) MKB_CUDA(cudaEventCreate(&x));
+  run();  // warm-up: one-time launch setup
+  float best = 1e30f;
+  for (int r = 0; r < 2; ++r) {
+    flush_l2(c);
+    MKB_CUDA(cudaEventRecord(ev[0], st));
+    run();
+    MKB_CUDA(cudaEventRecord(ev[1], st));
+    MKB_CUDA(cudaEventSynchronize(ev[1]));
+    float ms = 0.f;
+    MKB_CUDA(cudaEventElapsedTime(&ms, ev[0], ev[1]));
+    best = std::min(best, ms);
+  }
+  for (auto& x : ev) MKB_CUDA(cudaEventDestroy(x));
+  return best;
+}
+
+// Level-ordered plan autotune: the cost model's plan, then the best plan of every other
+// staged-level count, each timed once; the fastest is kept (mc.s2) and every count's time is
+// recorded (mc.s2_ms) for the fused sweep's common choice (launch_sweep2).
+static float tune_stream2(Context& c, uint32_t mode, const float* const* in, float* out) {
+  ModeCopy& mc = c.copies[mode];
+  const bool dbg = std::getenv("MKB_DEBUG") != nullptr;
+  for (float& x : mc.s2_ms) x = -1.f;
+  float best_ms = time_launch(c, [&] { launch_stream2(c, mode, in, out); });
+  const uint32_t k_model = mc.s2.k, nin = mc.s2.ni - mc.s2.nout;
+  if (k_model < 5) mc.s2_ms[k_model] = best_ms;
+  if (dbg) std::fprintf(stderr, "[mkb] mode %u level-ordered plan k=%u (model): %.1f us\n", mode, k_model, best_ms * 1e3);
+  if (std::getenv("MKB_FORCE_K")) return best_ms;
+  ModeCopy::Stream2 best = std::move(mc.s2);
+  for (uint32_t k = 0; k <= nin && k < 5; ++k) {
+    if (k == k_model) continue;
+    mc.s2 = ModeCopy::Stream2();
+    mc.s2_force_k = static_cast<int>(k);
+    if (!prepare_stream2(c, mode)) continue;
+    const float ms = time_launch(c, [&] { launch_stream2(c, mode, in, out); });
+    mc.s2_ms[k] = ms;
+    if (dbg) std::fprintf(stderr, "[mkb] mode %u level-ordered plan k=%u: %.1f us\n", mode, k, ms * 1e3);
+    if (ms < best_ms * 0.98f) {  // a clear win over the model's (simpler) choice
+      best_ms = ms;
+      best = std::move(mc.s2);
+    }
+  }
+  mc.s2 = std::move(best);
+  mc.s2_force_k = mc.s2.k_req;
+  return best_ms;
+}
+
 int choose_fast_kernel(Context& c, uint32_t mode, const float* const* in, float* out) {
   ModeCopy& mc = c.copies[mode];
   if (mc.fast_kernel >= 0 && mc.fast_rank == c.rank && mc.fast_e0 == mc.shard_e0 &&
@@ -386,6 +439,7 @@ int choose_fast_kernel(Context& c, uint32_t mode, const float* const* in, float*
   const char* e = std::getenv("MKB_FAST_KERNEL");
   std::string force = e ? e : "";
   if (c.force_fast_kernel >= 0) force = c.force_fast_kernel == 0 ? "s2" : (c.force_fast_kernel == 1 ? "stream" : "tiles");
+  if (!force.empty()) mc.s2_force_k = -1;  // a forced kernel runs the cost model's plan
   const bool s2_ok = force != "stream" && force != "tiles" && prepare_stream2(c, mode);
   const bool st_ok = force != "s2" && force != "tiles" && prepare_stream(c, mode);
   if (!s2_ok && !st_ok) return mc.fast_kernel = 2;
@@ -393,25 +447,12 @@ int choose_fast_kernel(Context& c, uint32_t mode, const float* const* in, float*
   if (!s2_ok) return mc.fast_kernel = 1;
   if (force == "s2") return mc.fast_kernel = 0;
   if (force == "stream") return mc.fast_kernel = 1;
-  cudaStream_t st = c.stream;
-  cudaEvent_t ev[3];
-  for (auto& x : ev) MKB_CUDA(cudaEventCreate(&x));
-  float ms[2] = {0.f, 0.f};
-  for (int k = 0; k < 2; ++k) {
-    auto run = [&] { k == 0 ? launch_stream2(c, mode, in, out) : launch_stream(c, mode, in, out); };
-    run();  // warm-up: one-time launch setup, L1/L2 state
-    flush_l2(c);
-    MKB_CUDA(cudaEventRecord(ev[0], st));
-    run();
-    MKB_CUDA(cudaEventRecord(ev[1], st));
-    MKB_CUDA(cudaEventSynchronize(ev[1]));
-    MKB_CUDA(cudaEventElapsedTime(&ms[k], ev[0], ev[1]));
-  }
-  for (auto& x : ev) MKB_CUDA(cudaEventDestroy(x));
-  mc.fast_kernel = ms[1] < ms[0] ? 1 : 0;
+  const float ms0 = tune_stream2(c, mode, in, out);
+  const float ms1 = time_launch(c, [&] { launch_stream(c, mode, in, out); });
+  mc.fast_kernel = ms1 < ms0 ? 1 : 0;
   if (std::getenv("MKB_DEBUG"))
-    std::fprintf(stderr, "[mkb] mode %u fast kernel: level-ordered %.1f us, fiber-ordered %.1f us -> %s\n",
-                 mode, ms[0] * 1e3, ms[1] * 1e3, mc.fast_kernel ? "fiber-ordered" : "level-ordered");
+    std::fprintf(stderr, "[mkb] mode %u fast kernel: level-ordered %.1f us (k=%u), fiber-ordered %.1f us -> %s\n",
+                 mode, ms0 * 1e3, mc.s2.k, ms1 * 1e3, mc.fast_kernel ? "fiber-ordered" : "level-ordered");
   return mc.fast_kernel;
 }
 

@@ -20,6 +20,7 @@
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 #include <vector>
 
 #include "stream2.cuh"
@@ -215,10 +216,12 @@ void rank_of_row_build(Context& c, uint32_t mode, DevBuf<uint32_t>& rank) {
 bool prepare_stream2(Context& c, uint32_t mode) {
   ModeCopy& mc = c.copies[mode];
   ModeCopy::Stream2& p = mc.s2;
-  if (p.tried && p.rank == c.rank && p.key_e0 == mc.shard_e0 && p.key_e1 == mc.shard_e1)
+  if (p.tried && p.rank == c.rank && p.key_e0 == mc.shard_e0 && p.key_e1 == mc.shard_e1 &&
+      p.k_req == mc.s2_force_k)
     return p.ok;
   p = ModeCopy::Stream2();
   p.tried = true;
+  p.k_req = mc.s2_force_k;
   p.rank = c.rank;
   p.key_e0 = mc.shard_e0;
   p.key_e1 = mc.shard_e1;
@@ -306,6 +309,17 @@ bool prepare_stream2(Context& c, uint32_t mode) {
     uint64_t nb = 1;
     double cost = 1e30;
   } best;
+  // the autotune's request (choose_fast_kernel), else MKB_FORCE_K="k0,k1,...": staged-level
+  // count per mode (a negative entry or none = cost model)
+  int force_k = mc.s2_force_k;
+  if (const char* fk = force_k < 0 ? std::getenv("MKB_FORCE_K") : nullptr) {
+    const char* q = fk;
+    for (uint32_t m = 0; m < mode && q; ++m) {
+      q = std::strchr(q, ',');
+      if (q) ++q;
+    }
+    if (q && *q) force_k = std::atoi(q);
+  }
   for (int sw = 0; sw < (nin >= 2 ? 2 : 1); ++sw) {
     std::vector<uint32_t> lo = lv;
     if (sw) std::swap(lo[ni - 1], lo[ni - 2]);
@@ -333,6 +347,7 @@ bool prepare_stream2(Context& c, uint32_t mode) {
         for (uint32_t j = 0; j < nin; ++j) cd.nb *= cd.split[j];
         if (cd.nb > 4096) { ok = false; break; }
       }
+      if (ok && force_k >= 0 && static_cast<int>(k) != force_k) ok = false;
       if (ok) {
         const double free_l1 = std::max(32.0 * 1024, 256.0 * 1024 - staged_bytes() - ring);
         double lsu = nin * kRow + kRec, l2 = 0;
@@ -354,6 +369,7 @@ bool prepare_stream2(Context& c, uint32_t mode) {
       if (k == 0) break;
     }
   }
+  if (best.cost >= 1e29) return false;  // no plan with the requested staged-level count
   if (best.swap) std::swap(lv[ni - 1], lv[ni - 2]);
   uint32_t rows[4], split[4];
   for (uint32_t j = 0; j < 4; ++j) {
@@ -704,8 +720,39 @@ bool launch_sweep2(Context& c, const float* const* in, float* const* outs) {
   const uint32_t G = c.rank / 4;
   size_t smem = 0;
   const ModeCopy::Stream2& p0 = c.copies[0].s2;
-  for (uint32_t d = 0; d < c.n; ++d) {
+  for (uint32_t d = 0; d < c.n; ++d)
     if (choose_fast_kernel(c, d, in, outs[d]) != 0) return false;
+  // The fused kernel needs one staged-level count K for all modes.  When the per-mode timed
+  // choices differ, re-plan every mode for the common K with the least summed time, if that
+  // costs at most 6% over the per-mode choices (the fused launch saves more than that).
+  bool same_k = true;
+  for (uint32_t d = 1; d < c.n; ++d) same_k &= c.copies[d].s2.k == p0.k;
+  if (!same_k) {
+    float best_sum = 0.f, common = 1e30f;
+    int kc = -1;
+    for (uint32_t d = 0; d < c.n; ++d) {
+      const ModeCopy& mc = c.copies[d];
+      best_sum += mc.s2.k < 5 && mc.s2_ms[mc.s2.k] >= 0.f ? mc.s2_ms[mc.s2.k] : 1e30f;
+    }
+    for (int k = 0; k < 5; ++k) {
+      float sum = 0.f;
+      for (uint32_t d = 0; d < c.n; ++d)
+        sum += c.copies[d].s2_ms[k] >= 0.f ? c.copies[d].s2_ms[k] : 1e30f;
+      if (sum < common) common = sum, kc = k;
+    }
+    if (kc < 0 || common > 1.06f * best_sum) return false;
+    for (uint32_t d = 0; d < c.n; ++d) {
+      ModeCopy& mc = c.copies[d];
+      if (mc.s2.k == static_cast<uint32_t>(kc)) continue;
+      mc.s2 = ModeCopy::Stream2();
+      mc.s2_force_k = kc;
+      if (!prepare_stream2(c, d)) return false;
+    }
+    if (std::getenv("MKB_DEBUG"))
+      std::fprintf(stderr, "[mkb] fused sweep: common k=%d (%.1f us vs %.1f us per-mode choices)\n",
+                   kc, common * 1e3, best_sum * 1e3);
+  }
+  for (uint32_t d = 0; d < c.n; ++d) {
     if (!prepare_stream2(c, d)) return false;
     const ModeCopy& mc = c.copies[d];
     const ModeCopy::Stream2& p = mc.s2;

@@ -196,3 +196,27 @@ def test_fused_sweep_nonfinite_reports_first_mode(mk):
     c.upload_factors(f2)
     c.sweep_async(False, False)
     c.synchronize()
+
+
+@pytest.mark.parametrize("dims,nnz,R", [([2482, 2862, 14036, 17], 400_000, 64), ([1000, 1000, 1000], 300_000, 32)])
+def test_autotuned_plans_match_oracle(mk, orc, dims, nnz, R):
+    """Unforced fast path: every staged-level count's plan is timed once per mode and the fastest
+    kept (mttkrp.cu tune_stream2); the fused sweep may re-plan all modes to one common count
+    (stream2_plan.cu launch_sweep2).  Per-mode and fused results both match the oracle."""
+    t = mk.generate_powerlaw(dims, nnz, 1.0, 2) if dims[-1] == 17 else mk.generate_synthetic(dims, nnz, seed=2)
+    f = [m.data for m in mk.random_factors(dims, R, 4)]
+    want = [orc.mttkrp(dims, t.coords, t.values, f, d) for d in range(len(dims))]
+    c = mk.Context()
+    c.upload_tensor(t)
+    c.build_plans(148)
+    c.upload_factors(f)
+    outs = c.mttkrp_all_modes(False, False)  # per-mode choices, then the fused sweep
+    infos = [c.fast_path_info(d) for d in range(len(dims))]
+    for d in range(len(dims)):
+        assert infos[d].kernel in (0, 1)
+        assert mk.verify_against(outs[d], want[d])[0] <= 1e-4, (d, infos[d].as_dict())
+    for rep in range(2):
+        c.sweep_async(False, False)
+        c.synchronize()
+        for d in range(len(dims)):
+            assert mk.verify_against(c.output(d), want[d])[0] <= 1e-4, (rep, d)
