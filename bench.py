@@ -329,8 +329,15 @@ def our_arm(args, cfg, rank, world, local_rank):
     warm_ms = float(np.mean([evw[s][0].elapsed_time(evw[s][1]) for s in range(args.steps)]))
 
     # e2e through the C ABI with pinned host buffers
-    pin_f = [torch.from_numpy(f).pin_memory() for f in factors]
-    pin_o = [torch.empty((d, R), dtype=torch.float32).pin_memory() for d in dims]
+    # one pinned allocation per direction, matrices packed in mode order: the C ABI then moves
+    # all factors (outputs) in one copy instead of one per mode (~6 us of PCIe latency each)
+    offs = np.cumsum([0] + [(d * R + 31) // 32 * 32 for d in dims])
+    arena_f = torch.empty(int(offs[-1]), dtype=torch.float32).pin_memory()
+    arena_o = torch.empty(int(offs[-1]), dtype=torch.float32).pin_memory()
+    pin_f = [arena_f[offs[w]:offs[w] + d * R].view(d, R) for w, d in enumerate(dims)]
+    pin_o = [arena_o[offs[w]:offs[w] + d * R].view(d, R) for w, d in enumerate(dims)]
+    for p_, f_ in zip(pin_f, factors):
+        p_.copy_(torch.from_numpy(f_))
     f_np = [p.numpy() for p in pin_f]
     o_np = [p.numpy() for p in pin_o]
     def e2e_step():

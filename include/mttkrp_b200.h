@@ -131,7 +131,9 @@ int mk_sweep_async(mk_context* ctx, int chain, int exec);
 int mk_mttkrp_mode_async(mk_context* ctx, uint32_t mode, int exec);
 int mk_output_download(mk_context* ctx, uint32_t mode, float* out);
 /* End-to-end step as a caller sees it: H2D of all factors from host memory, the sweep,
- * D2H of all outputs, synchronise. */
+ * D2H of all outputs, synchronise.  When the host matrices are packed in one allocation in
+ * mode order (factor w at float offset sum_{v<w} I_v*R, every I_v*R a multiple of 32, e.g.
+ * R = 32 or 64), each direction is ONE copy; otherwise one copy per mode. */
 int mk_sweep_host(mk_context* ctx, const float* const* factors, float* const* outs, int chain,
                   int exec);
 /* run_timed analogue (kernel.hpp:239-287) timed with CUDA events on the context stream.

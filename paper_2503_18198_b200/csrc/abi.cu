@@ -53,11 +53,36 @@ void need_factors(Context& c) {
     if (!c.factors_set[w]) fail(MK_ESTATE, "kernel: expected one factor matrix per mode");
 }
 
+// Host matrices laid out exactly like the device arena (one allocation, modes in order, no
+// gaps: every factor is a multiple of 32 floats, e.g. R = 32 or 64) move in one copy.
+static bool host_packed(const Context& c, const void* const* h) {
+  for (uint32_t w = 0; w < c.n; ++w) {
+    const size_t cnt = static_cast<size_t>(c.dims[w]) * c.rank;
+    if (c.arena_off[w + 1] - c.arena_off[w] != cnt) return false;
+    if (static_cast<const char*>(h[w]) - static_cast<const char*>(h[0]) !=
+        static_cast<std::ptrdiff_t>(c.arena_off[w] * sizeof(float)))
+      return false;
+  }
+  return true;
+}
+
+static void copy_factors_in(Context& c, const float* const* factors) {
+  if (host_packed(c, reinterpret_cast<const void* const*>(factors))) {
+    MKB_CUDA(cudaMemcpyAsync(c.factor_arena.get(), factors[0], c.arena_off[c.n] * sizeof(float),
+                             cudaMemcpyHostToDevice, c.stream));
+    return;
+  }
+  for (uint32_t w = 0; w < c.n; ++w)
+    MKB_CUDA(cudaMemcpyAsync(c.factors[w].get(), factors[w],
+                             static_cast<size_t>(c.dims[w]) * c.rank * sizeof(float),
+                             cudaMemcpyHostToDevice, c.stream));
+}
+
 void check_nonfinite(Context& c) {
-  unsigned long long tagged = ~0ull;
-  MKB_CUDA(cudaMemcpyAsync(&tagged, c.nonfinite.get(), sizeof tagged, cudaMemcpyDeviceToHost,
-                           c.stream));
+  unsigned long long* h = c.nonfinite_host.get();
+  MKB_CUDA(cudaMemcpyAsync(h, c.nonfinite.get(), sizeof *h, cudaMemcpyDeviceToHost, c.stream));
   MKB_CUDA(cudaStreamSynchronize(c.stream));
+  const unsigned long long tagged = *h;
   if (tagged != ~0ull) {
     MKB_CUDA(cudaMemsetAsync(c.nonfinite.get(), 0xff, sizeof tagged, c.stream));  // reported once
     const uint64_t mode = tagged >> 32, pos = tagged & 0xffffffffull;
@@ -312,16 +337,22 @@ int mk_factors_upload(mk_context* ctx, uint32_t rank, const float* const* factor
     if (c.n == 0) fail(MK_ESTATE, "kernel: no tensor uploaded");
     if (rank < 1) fail(MK_EINVAL, "kernel: rank must be at least 1");
     if (!factors) fail(MK_EINVAL, "kernel: expected one factor matrix per mode");
+    for (uint32_t w = 0; w < c.n; ++w)
+      if (!factors[w]) fail(MK_EINVAL, "kernel: expected one factor matrix per mode");
+    MKB_CUDA(cudaStreamSynchronize(c.stream));  // no launch may still read the old arenas
     c.rank = rank;
+    c.arena_off[0] = 0;
+    for (uint32_t w = 0; w < c.n; ++w)
+      c.arena_off[w + 1] = c.arena_off[w] + ((static_cast<size_t>(c.dims[w]) * rank + 31) & ~size_t(31));
+    c.factor_arena.resize(c.arena_off[c.n]);
+    c.output_arena.resize(c.arena_off[c.n]);
     for (uint32_t w = 0; w < c.n; ++w) {
       const size_t cnt = static_cast<size_t>(c.dims[w]) * rank;
-      c.factors[w].resize(cnt);
-      c.outputs[w].resize(cnt);
-      if (!factors[w]) fail(MK_EINVAL, "kernel: expected one factor matrix per mode");
-      MKB_CUDA(cudaMemcpyAsync(c.factors[w].get(), factors[w], cnt * sizeof(float),
-                               cudaMemcpyHostToDevice, c.stream));
+      c.factors[w].view(c.factor_arena.get() + c.arena_off[w], cnt);
+      c.outputs[w].view(c.output_arena.get() + c.arena_off[w], cnt);
       c.factors_set[w] = true;
     }
+    copy_factors_in(c, factors);
     c.grams_valid = false;
     MKB_CUDA(cudaStreamSynchronize(c.stream));
   });
@@ -447,15 +478,17 @@ int mk_sweep_host(mk_context* ctx, const float* const* factors, float* const* ou
     Context& c = ctx->c;
     need_plans(c);
     need_factors(c);
-    for (uint32_t w = 0; w < c.n; ++w)
-      MKB_CUDA(cudaMemcpyAsync(c.factors[w].get(), factors[w],
-                               static_cast<size_t>(c.dims[w]) * c.rank * sizeof(float),
-                               cudaMemcpyHostToDevice, c.stream));
+    copy_factors_in(c, factors);
     sweep(c, chain, exec);
-    for (uint32_t d = 0; d < c.n; ++d)
-      MKB_CUDA(cudaMemcpyAsync(outs[d], c.outputs[d].get(),
-                               static_cast<size_t>(c.dims[d]) * c.rank * sizeof(float),
+    if (host_packed(c, reinterpret_cast<const void* const*>(outs))) {  // one copy: every copy pays ~6 us of PCIe latency
+      MKB_CUDA(cudaMemcpyAsync(outs[0], c.output_arena.get(), c.arena_off[c.n] * sizeof(float),
                                cudaMemcpyDeviceToHost, c.stream));
+    } else {
+      for (uint32_t d = 0; d < c.n; ++d)
+        MKB_CUDA(cudaMemcpyAsync(outs[d], c.outputs[d].get(),
+                                 static_cast<size_t>(c.dims[d]) * c.rank * sizeof(float),
+                                 cudaMemcpyDeviceToHost, c.stream));
+    }
     check_nonfinite(c);
   });
 }

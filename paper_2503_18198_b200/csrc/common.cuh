@@ -33,6 +33,21 @@ inline void cuda_check(cudaError_t e, const char* what, const char* file, int li
 #define MKB_CUDA(x) ::mkb::cuda_check((x), #x, __FILE__, __LINE__)
 #define MKB_LAUNCH() ::mkb::cuda_check(cudaGetLastError(), "kernel launch", __FILE__, __LINE__)
 
+// One pinned host word (device-to-host status reads without a pageable bounce).
+struct PinnedWord {
+  unsigned long long* p = nullptr;
+  PinnedWord() = default;
+  PinnedWord(const PinnedWord&) = delete;
+  PinnedWord& operator=(const PinnedWord&) = delete;
+  ~PinnedWord() {
+    if (p) cudaFreeHost(p);
+  }
+  unsigned long long* get() {
+    if (!p) MKB_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&p), sizeof *p, cudaHostAllocDefault));
+    return p;
+  }
+};
+
 // Owning device allocation (cudaMalloc; 256-byte aligned, so float4 rows are aligned
 // whenever the row stride is a multiple of 4 floats).
 template <typename T>
@@ -43,9 +58,21 @@ class DevBuf {
   ~DevBuf() { release(); }
   DevBuf(const DevBuf&) = delete;
   DevBuf& operator=(const DevBuf&) = delete;
-  DevBuf(DevBuf&& o) noexcept : p_(o.p_), n_(o.n_) { o.p_ = nullptr; o.n_ = 0; }
+  DevBuf(DevBuf&& o) noexcept : p_(o.p_), n_(o.n_), owned_(o.owned_) {
+    o.p_ = nullptr;
+    o.n_ = 0;
+    o.owned_ = true;
+  }
   DevBuf& operator=(DevBuf&& o) noexcept {
-    if (this != &o) { release(); p_ = o.p_; n_ = o.n_; o.p_ = nullptr; o.n_ = 0; }
+    if (this != &o) {
+      release();
+      p_ = o.p_;
+      n_ = o.n_;
+      owned_ = o.owned_;
+      o.p_ = nullptr;
+      o.n_ = 0;
+      o.owned_ = true;
+    }
     return *this;
   }
   void resize(size_t n) {
@@ -55,10 +82,18 @@ class DevBuf {
     MKB_CUDA(cudaMalloc(&p_, n * sizeof(T)));
     n_ = n;
   }
+  // A non-owning window into another buffer (the factor / output arenas, context.cuh).
+  void view(T* p, size_t n) {
+    release();
+    p_ = p;
+    n_ = n;
+    owned_ = false;
+  }
   void release() {
-    if (p_) cudaFree(p_);
+    if (p_ && owned_) cudaFree(p_);
     p_ = nullptr;
     n_ = 0;
+    owned_ = true;
   }
   T* get() const { return p_; }
   size_t size() const { return n_; }
@@ -67,6 +102,7 @@ class DevBuf {
  private:
   T* p_ = nullptr;
   size_t n_ = 0;
+  bool owned_ = true;
 };
 
 inline unsigned ceil_div(uint64_t a, uint64_t b) { return static_cast<unsigned>((a + b - 1) / b); }

@@ -122,12 +122,17 @@ struct Context {
 
   // factors / outputs (row-major I_d x R)
   uint32_t rank = 0;
+  // factors[w] / outputs[w] are windows into one arena each, at 128-B aligned offsets
+  // arena_off[w] (floats): a host layout with the same offsets moves in one copy
+  DevBuf<float> factor_arena, output_arena;
+  size_t arena_off[kMaxModes + 1] = {};
   DevBuf<float> factors[kMaxModes];
   DevBuf<float> outputs[kMaxModes];
   bool factors_set[kMaxModes] = {};
 
   // device scalars: [0] = min non-finite copy position (uint64, ~0 = none), [1] = mode
   DevBuf<unsigned long long> nonfinite;
+  PinnedWord nonfinite_host;
   DevBuf<uint8_t> flush_buf;
   int force_fast_kernel = -1;  // mk_set_fast_kernel: -1 timed choice, else 0 / 1 / 2
   DevBuf<uint32_t> s2sync;  // streaming kernel: finished-CTA counter + non-finite flag
