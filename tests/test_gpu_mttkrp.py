@@ -268,3 +268,26 @@ def test_sweep_host_and_async_agree(mk):
     ctx.synchronize()
     for d in range(4):
         assert np.array_equal(ctx.output(d), ref[d])
+
+
+def test_cfg5_full_size_vs_oracle(mk, orc):
+    """BASELINE cfg5 at full size (nell-2 shape, 77M nnz, R = 32): the fused fast sweep within
+    the north star's 1e-4 and the deterministic kernel bitwise equal to the C oracle
+    (oracle_mttkrp order, oracle.hpp:20-43) on every mode."""
+    dims = [12092, 9184, 28818]
+    t = mk.generate_synthetic(dims, 77_000_000, seed=1)
+    f = [m.data for m in mk.random_factors(dims, 32, 1)]
+    c = mk.Context()
+    c.upload_tensor(t)
+    c.build_plans(148)
+    c.upload_factors(f)
+    fast = c.mttkrp_all_modes(False, False)
+    c.sweep_async(False, False)  # the fused single-launch sweep (after the per-mode tuning)
+    c.synchronize()
+    fused = [c.output(d) for d in range(3)]
+    det = c.mttkrp_all_modes(False, True)
+    for d in range(3):
+        want = orc.mttkrp(dims, t.coords, t.values, f, d)
+        assert np.array_equal(det[d].view(np.uint32), want.view(np.uint32)), d
+        assert mk.verify_against(fast[d], want)[0] <= 1e-4, d
+        assert mk.verify_against(fused[d], want)[0] <= 1e-4, d
