@@ -74,6 +74,7 @@ struct ModeCopy {
     uint32_t rank = 0;
     uint64_t key_e0 = ~0ull, key_e1 = ~0ull;  // shard range the plan was built for
     uint32_t ni = 0, nout = 0, k = 0, aw = 2;  // input levels, outer levels, staged levels
+    uint32_t nt = 512;                         // threads per CTA
     bool os = false;                           // outer factor staged in shared memory
     uint32_t levels[kMaxModes] = {};           // level -> input mode (outermost first)
     uint32_t rowbits = 0, b0 = 0, m0 = 0, m1 = 0, ob = 0, om = 0;

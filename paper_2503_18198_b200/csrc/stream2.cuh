@@ -388,6 +388,10 @@ constexpr uint32_t kHeader = 1024, kArgsOff = 512;
 #define MKB_S2_NT 512  // threads per CTA (one CTA per SM)
 #endif
 constexpr int kNT = MKB_S2_NT;
+#ifndef MKB_S2_NT_STAGED
+#define MKB_S2_NT_STAGED 384  // threads per CTA when every inner level is staged
+#endif
+constexpr int kNTStaged = MKB_S2_NT_STAGED;
 
 // Per-thread state that persists across the modes of one launch.
 struct Persist {
@@ -699,13 +703,23 @@ void launch_sweep_one(const SweepArgs& a, unsigned grid, size_t smem, cudaStream
                                        params, smem, st));
 }
 
-// Every plan runs 512-thread CTAs, one per SM (the staged factors take most of the shared
-// memory; without staging the rings still do).  `smem` is the dynamic shared memory size.
+// One CTA per SM (the staged factors take most of the shared memory; without staging the
+// rings still do): kNT threads, or kNTStaged when every inner level is staged (the plan's
+// `nt`, stream2_plan.cu).  `smem` is the dynamic shared memory size.
 template <int NI, int NOUT, bool OS, int G, typename A>
-void launch_k(const A& a, uint32_t K, unsigned grid, size_t smem, cudaStream_t st) {
+void launch_k(const A& a, uint32_t K, uint32_t nt, unsigned grid, size_t smem, cudaStream_t st) {
   constexpr int NIN = NI - NOUT;
   auto go = [&](auto kc) {
     constexpr int KK = decltype(kc)::value;
+    if constexpr (KK == NIN && kNTStaged != kNT) {
+      if (nt == static_cast<uint32_t>(kNTStaged)) {
+        if constexpr (std::is_same_v<A, SweepArgs>)
+          return launch_sweep_one<NI, NOUT, KK, OS, G, kNTStaged, 1>(a, grid, smem, st);
+        else
+          return launch_one<NI, NOUT, KK, OS, G, kNTStaged, 1>(a, grid, smem, st);
+      }
+    }
+    if (nt != static_cast<uint32_t>(kNT)) fail(MK_EINVAL, "stream2: no kernel for this CTA size");
     if constexpr (std::is_same_v<A, SweepArgs>)
       launch_sweep_one<NI, NOUT, KK, OS, G, kNT, 1>(a, grid, smem, st);
     else
@@ -724,11 +738,11 @@ void launch_k(const A& a, uint32_t K, unsigned grid, size_t smem, cudaStream_t s
 }
 
 template <int NI, int G, typename A>
-void launch_ni_g(const A& a, uint32_t nout, bool os, uint32_t K, unsigned grid, size_t smem,
-                 cudaStream_t st) {
-  if (nout == 0) return launch_k<NI, 0, false, G>(a, K, grid, smem, st);
-  if (os) return launch_k<NI, 1, true, G>(a, K, grid, smem, st);
-  return launch_k<NI, 1, false, G>(a, K, grid, smem, st);
+void launch_ni_g(const A& a, uint32_t nout, bool os, uint32_t K, uint32_t nt, unsigned grid,
+                 size_t smem, cudaStream_t st) {
+  if (nout == 0) return launch_k<NI, 0, false, G>(a, K, nt, grid, smem, st);
+  if (os) return launch_k<NI, 1, true, G>(a, K, nt, grid, smem, st);
+  return launch_k<NI, 1, false, G>(a, K, nt, grid, smem, st);
 }
 
 }  // namespace s2
@@ -736,9 +750,9 @@ void launch_ni_g(const A& a, uint32_t nout, bool os, uint32_t K, unsigned grid, 
 // per-(N, G) dispatch (stream2_n<N>_g<G>.cu); `smem` = dynamic shared memory bytes
 #define MKB_S2_DECL(N, G)                                                                  \
   void stream2_launch_n##N##_g##G(const s2::Args& a, uint32_t nout, bool os, uint32_t K,   \
-                                  unsigned grid, size_t smem, cudaStream_t st);            \
+                                  uint32_t nt, unsigned grid, size_t smem, cudaStream_t st); \
   void stream2_sweep_n##N##_g##G(const s2::SweepArgs& a, uint32_t nout, bool os, uint32_t K, \
-                                 unsigned grid, size_t smem, cudaStream_t st);
+                                 uint32_t nt, unsigned grid, size_t smem, cudaStream_t st);
 MKB_S2_DECL(3, 8)
 MKB_S2_DECL(3, 16)
 MKB_S2_DECL(4, 8)

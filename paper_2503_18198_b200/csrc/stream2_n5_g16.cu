@@ -3,12 +3,12 @@
 #include "stream2.cuh"
 
 namespace mkb {
-void stream2_launch_n5_g16(const s2::Args& a, uint32_t nout, bool os, uint32_t K,
+void stream2_launch_n5_g16(const s2::Args& a, uint32_t nout, bool os, uint32_t K, uint32_t nt,
                           unsigned grid, size_t smem, cudaStream_t st) {
-  s2::launch_ni_g<4, 16>(a, nout, os, K, grid, smem, st);
+  s2::launch_ni_g<4, 16>(a, nout, os, K, nt, grid, smem, st);
 }
-void stream2_sweep_n5_g16(const s2::SweepArgs& a, uint32_t nout, bool os, uint32_t K,
+void stream2_sweep_n5_g16(const s2::SweepArgs& a, uint32_t nout, bool os, uint32_t K, uint32_t nt,
                          unsigned grid, size_t smem, cudaStream_t st) {
-  s2::launch_ni_g<4, 16>(a, nout, os, K, grid, smem, st);
+  s2::launch_ni_g<4, 16>(a, nout, os, K, nt, grid, smem, st);
 }
 }  // namespace mkb

@@ -295,12 +295,20 @@ bool prepare_stream2(Context& c, uint32_t mode) {
   //      flush = 32 per atomic row flush: every (block, row) pair of a blocked plan
   //      stage = per CTA item: staged slice bytes / 85 B per SM-cycle + a ~6000-cycle stall
   //    cost = LSU + L2 + flush + stage (fitted to the measured cfg2 / cfg3 / cfg5 plans).
-  const size_t ring = s2::ring_bytes_rt(p.aw, G, s2::kNT);
-  size_t budget = s2::kMaxDynSmem - ring - s2::kHeader;
+  //    CTA size: a plan that stages every inner level gathers only from shared memory and
+  //    runs best with 12 warps (smaller rings, more staging room, less barrier skew: cfg2
+  //    0.159 -> 0.156 ms); L1/L2-fed gathers need 16 warps to hide latency (cfg5 2.09 vs
+  //    2.51 ms at 12).  MKB_S2_NT_STAGED=512 keeps 16 warps everywhere.
+  const uint32_t nt_staged = env_int("MKB_S2_NT_STAGED", s2::kNTStaged) == 512 ? 512u : s2::kNTStaged;
+  auto nt_for = [&](uint32_t k) { return k == nin ? nt_staged : static_cast<uint32_t>(s2::kNT); };
+  auto budget_for = [&](uint32_t k) {
+    return s2::kMaxDynSmem - s2::ring_bytes_rt(p.aw, G, nt_for(k)) - s2::kHeader;
+  };
+  const size_t budget0 = budget_for(0);
   const bool stage_on = env_int("MKB_STAGE", 1) != 0;
   const bool block_on = env_int("MKB_BLOCK", 1) != 0 && !sharded;
-  p.os = stage_on && p.nout && fbytes(lv[0]) <= std::min<size_t>(32u << 10, budget / 4);
-  if (p.os) budget -= align128(fbytes(lv[0]));
+  p.os = stage_on && p.nout && fbytes(lv[0]) <= std::min<size_t>(32u << 10, budget0 / 4);
+  const size_t os_bytes = p.os ? align128(fbytes(lv[0])) : 0;
   const double kRow = 0.94 * (rowbytes / 128.0), kRec = (p.aw == 2 ? 1.5 : 2.5) * G / 32.0;
   const double kL2 = 85.0, kL2Gather = 45.0, kFlush = 32.0;
   struct Cand {
@@ -335,6 +343,8 @@ bool prepare_stream2(Context& c, uint32_t mode) {
         return b;
       };
       bool ok = true;
+      const size_t budget = budget_for(k) - os_bytes;
+      const size_t ring = s2::ring_bytes_rt(p.aw, G, nt_for(k));
       while (staged_bytes() > budget) {  // greedy: split the staged slot with the largest slice
         if (!block_on) { ok = false; break; }
         uint32_t jm = nin - k;
@@ -377,6 +387,7 @@ bool prepare_stream2(Context& c, uint32_t mode) {
     split[j] = best.split[j];
   }
   p.k = best.k;
+  p.nt = nt_for(best.k);
   p.nblocks = static_cast<uint32_t>(best.nb);
   p.blocked = best.nb > 1;
   const char* kind = p.blocked ? "blocked" : (p.k == nin ? "unblocked" : "partial");
@@ -461,7 +472,7 @@ bool prepare_stream2(Context& c, uint32_t mode) {
   //    boundaries into items; an item's elements are split evenly over the CTA's lane groups;
   //    a warp's groups stream chunk-interleaved records.
   const uint32_t S = s2::seg_len(p.aw), RS = s2::rec_stride(p.aw), KS = s2::key_stride(p.aw);
-  const uint32_t NW = s2::kNT / 32, GPW = 32 / G, NG = NW * GPW;
+  const uint32_t NW = p.nt / 32, GPW = 32 / G, NG = NW * GPW;
   const unsigned grid = static_cast<unsigned>(c.num_sms);
   const uint64_t E0 = p.blocked ? 0 : mc.shard_e0, E1 = p.blocked ? nnz : mc.shard_e1;
   std::vector<WDesc> wd;
@@ -699,15 +710,15 @@ bool launch_stream2(Context& c, uint32_t mode, const float* const* in, float* ou
   uint32_t* sw = sync_words(c);
   s2::Args a;
   fill_args(c, mode, in, out, a, sw, sw + 2);
-  const size_t smem = p.staged_end + s2::ring_bytes_rt(p.aw, G, s2::kNT);
+  const size_t smem = p.staged_end + s2::ring_bytes_rt(p.aw, G, p.nt);
   const unsigned grid = p.grid;
   switch (c.n * 100 + G) {
-    case 308: stream2_launch_n3_g8(a, p.nout, p.os, p.k, grid, smem, st); break;
-    case 316: stream2_launch_n3_g16(a, p.nout, p.os, p.k, grid, smem, st); break;
-    case 408: stream2_launch_n4_g8(a, p.nout, p.os, p.k, grid, smem, st); break;
-    case 416: stream2_launch_n4_g16(a, p.nout, p.os, p.k, grid, smem, st); break;
-    case 508: stream2_launch_n5_g8(a, p.nout, p.os, p.k, grid, smem, st); break;
-    case 516: stream2_launch_n5_g16(a, p.nout, p.os, p.k, grid, smem, st); break;
+    case 308: stream2_launch_n3_g8(a, p.nout, p.os, p.k, p.nt, grid, smem, st); break;
+    case 316: stream2_launch_n3_g16(a, p.nout, p.os, p.k, p.nt, grid, smem, st); break;
+    case 408: stream2_launch_n4_g8(a, p.nout, p.os, p.k, p.nt, grid, smem, st); break;
+    case 416: stream2_launch_n4_g16(a, p.nout, p.os, p.k, p.nt, grid, smem, st); break;
+    case 508: stream2_launch_n5_g8(a, p.nout, p.os, p.k, p.nt, grid, smem, st); break;
+    case 516: stream2_launch_n5_g16(a, p.nout, p.os, p.k, p.nt, grid, smem, st); break;
     default: return false;
   }
   return true;
@@ -757,9 +768,10 @@ bool launch_sweep2(Context& c, const float* const* in, float* const* outs) {
     const ModeCopy& mc = c.copies[d];
     const ModeCopy::Stream2& p = mc.s2;
     if (p.nitems == 0 || mc.shard_e1 <= mc.shard_e0) return false;
-    if (p.nout != p0.nout || p.os != p0.os || p.k != p0.k || p.aw != p0.aw || p.grid != p0.grid)
+    if (p.nout != p0.nout || p.os != p0.os || p.k != p0.k || p.aw != p0.aw || p.grid != p0.grid ||
+        p.nt != p0.nt)
       return false;
-    smem = std::max(smem, p.staged_end + s2::ring_bytes_rt(p.aw, G, s2::kNT));
+    smem = std::max(smem, p.staged_end + s2::ring_bytes_rt(p.aw, G, p.nt));
   }
   uint32_t* sw = sync_words(c);
   static_assert(sizeof(s2::SweepArgs) <= 32000, "kernel parameter space");
@@ -769,12 +781,12 @@ bool launch_sweep2(Context& c, const float* const* in, float* const* outs) {
   cudaStream_t st = c.stream;
   const unsigned grid = p0.grid;
   switch (c.n * 100 + G) {
-    case 308: stream2_sweep_n3_g8(sa, p0.nout, p0.os, p0.k, grid, smem, st); break;
-    case 316: stream2_sweep_n3_g16(sa, p0.nout, p0.os, p0.k, grid, smem, st); break;
-    case 408: stream2_sweep_n4_g8(sa, p0.nout, p0.os, p0.k, grid, smem, st); break;
-    case 416: stream2_sweep_n4_g16(sa, p0.nout, p0.os, p0.k, grid, smem, st); break;
-    case 508: stream2_sweep_n5_g8(sa, p0.nout, p0.os, p0.k, grid, smem, st); break;
-    case 516: stream2_sweep_n5_g16(sa, p0.nout, p0.os, p0.k, grid, smem, st); break;
+    case 308: stream2_sweep_n3_g8(sa, p0.nout, p0.os, p0.k, p0.nt, grid, smem, st); break;
+    case 316: stream2_sweep_n3_g16(sa, p0.nout, p0.os, p0.k, p0.nt, grid, smem, st); break;
+    case 408: stream2_sweep_n4_g8(sa, p0.nout, p0.os, p0.k, p0.nt, grid, smem, st); break;
+    case 416: stream2_sweep_n4_g16(sa, p0.nout, p0.os, p0.k, p0.nt, grid, smem, st); break;
+    case 508: stream2_sweep_n5_g8(sa, p0.nout, p0.os, p0.k, p0.nt, grid, smem, st); break;
+    case 516: stream2_sweep_n5_g16(sa, p0.nout, p0.os, p0.k, p0.nt, grid, smem, st); break;
     default: return false;
   }
   return true;
