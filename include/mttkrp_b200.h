@@ -136,6 +136,8 @@ int mk_output_download(mk_context* ctx, uint32_t mode, float* out);
  * R = 32 or 64), each direction is ONE copy; otherwise one copy per mode. */
 int mk_sweep_host(mk_context* ctx, const float* const* factors, float* const* outs, int chain,
                   int exec);
+/* Whether the last all-mode sweep ran as one fused launch (1) or one launch per mode (0). */
+int mk_last_sweep_fused(mk_context* ctx, int* fused);
 /* run_timed analogue (kernel.hpp:239-287) timed with CUDA events on the context stream.
  * mode_ms[iters × N] and total_ms[iters]; flush_l2 writes a 2×L2 buffer between
  * iterations (outside the timed events). */

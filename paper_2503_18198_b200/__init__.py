@@ -55,7 +55,7 @@ EXPORTED_SYMBOLS = [
     "mk_copy_export", "mk_factors_upload", "mk_factor_upload", "mk_factor_download",
     "mk_mttkrp_mode", "mk_mttkrp_all_modes", "mk_sweep_async", "mk_mttkrp_mode_async",
     "mk_output_download",
-    "mk_sweep_host", "mk_run_timed", "mk_flush_l2", "mk_cpd_als_iter", "mk_cpd_als",
+    "mk_sweep_host", "mk_run_timed", "mk_flush_l2", "mk_last_sweep_fused", "mk_cpd_als_iter", "mk_cpd_als",
     "mk_generate_synthetic", "mk_generate_powerlaw", "mk_random_factors",
     "mk_set_shard", "mk_shard_rows", "mk_shard_pack", "mk_shard_unpack", "mk_shard_cuts",
     "mk_als_update_mode", "mk_als_fit", "mk_output_device_ptr",
@@ -158,6 +158,7 @@ def load_library() -> C.CDLL:
             "mk_sweep_host": (i32, [vp, vp, vp, i32, i32]),
             "mk_run_timed": (i32, [vp, u64, i32, i32, vp, vp]),
             "mk_flush_l2": (i32, [vp]),
+            "mk_last_sweep_fused": (i32, [vp, P(C.c_int)]),
             "mk_cpd_als_iter": (i32, [vp, P(C.c_double), vp]),
             "mk_cpd_als": (i32, [vp, u64, C.c_double, P(C.c_double), P(u64), vp]),
             "mk_generate_synthetic": (i32, [u32, vp, u64, i32, u64, u64, u64, vp, vp]),
@@ -442,6 +443,12 @@ class Context:
 
     def flush_l2(self):
         _check(self.lib.mk_flush_l2(self.h))
+
+    def last_sweep_fused(self) -> bool:
+        """Whether the last all-mode sweep ran as one fused launch (k_sweep2)."""
+        v = C.c_int(0)
+        _check(self.lib.mk_last_sweep_fused(self.h, C.byref(v)))
+        return bool(v.value)
 
     # multi-GPU shards (SURVEY §8e)
     def set_shard(self, rank: int, world: int):

@@ -104,8 +104,10 @@ void sweep(Context& c, int chain, int exec) {
   if (!chain && exec == MK_EXEC_FAST) {
     float* outs[kMaxModes];
     for (uint32_t d = 0; d < c.n; ++d) outs[d] = c.outputs[d].get();
-    if (launch_sweep2(c, in, outs)) return;  // one fused launch (stream2.cuh k_sweep2)
+    c.last_sweep_fused = launch_sweep2(c, in, outs);  // one launch (stream2.cuh k_sweep2)
+    if (c.last_sweep_fused) return;
   }
+  c.last_sweep_fused = false;
   for (uint32_t d = 0; d < c.n; ++d) {
     launch_mttkrp(c, d, in, c.outputs[d].get(), exec);
     if (chain) in[d] = c.outputs[d].get();
@@ -490,6 +492,14 @@ int mk_sweep_host(mk_context* ctx, const float* const* factors, float* const* ou
                                  cudaMemcpyDeviceToHost, c.stream));
     }
     check_nonfinite(c);
+  });
+}
+
+int mk_last_sweep_fused(mk_context* ctx, int* fused) {
+  return guarded([&] {
+    need_ctx(ctx);
+    if (!fused) fail(MK_EINVAL, "null output");
+    *fused = ctx->c.last_sweep_fused ? 1 : 0;
   });
 }
 

@@ -64,6 +64,7 @@ struct ModeCopy {
   // level-ordered plan autotune: staged-level count to plan for (-1: cost model), and the
   // timed milliseconds of the best plan per staged-level count (< 0: none)
   int s2_force_k = -1;
+  bool s2_no_os = false;  // fused sweep: plan without staging the outer factor
   float s2_ms[5] = {-1.f, -1.f, -1.f, -1.f, -1.f};
   uint64_t fast_e0 = ~0ull, fast_e1 = ~0ull;
   // level-ordered, shared-memory-blocked records of the streaming kernel (stream2_plan.cu),
@@ -71,6 +72,7 @@ struct ModeCopy {
   struct Stream2 {
     bool tried = false, ok = false;
     int k_req = -1;                            // requested staged-level count (-1: model)
+    bool no_os = false;                        // planned with the outer factor unstaged
     uint32_t rank = 0;
     uint64_t key_e0 = ~0ull, key_e1 = ~0ull;  // shard range the plan was built for
     uint32_t ni = 0, nout = 0, k = 0, aw = 2;  // input levels, outer levels, staged levels
@@ -150,6 +152,7 @@ struct Context {
   DevBuf<double> als_scalars;
   DevBuf<int> als_status;
   bool grams_valid = false;
+  bool last_sweep_fused = false;  // the last sweep() ran as one k_sweep2 launch
 };
 
 // One CPD-ALS iteration over all modes (als.cu); fit and optional lambda[R] to host.

@@ -217,11 +217,12 @@ bool prepare_stream2(Context& c, uint32_t mode) {
   ModeCopy& mc = c.copies[mode];
   ModeCopy::Stream2& p = mc.s2;
   if (p.tried && p.rank == c.rank && p.key_e0 == mc.shard_e0 && p.key_e1 == mc.shard_e1 &&
-      p.k_req == mc.s2_force_k)
+      p.k_req == mc.s2_force_k && p.no_os == mc.s2_no_os)
     return p.ok;
   p = ModeCopy::Stream2();
   p.tried = true;
   p.k_req = mc.s2_force_k;
+  p.no_os = mc.s2_no_os;
   p.rank = c.rank;
   p.key_e0 = mc.shard_e0;
   p.key_e1 = mc.shard_e1;
@@ -307,7 +308,8 @@ bool prepare_stream2(Context& c, uint32_t mode) {
   const size_t budget0 = budget_for(0);
   const bool stage_on = env_int("MKB_STAGE", 1) != 0;
   const bool block_on = env_int("MKB_BLOCK", 1) != 0 && !sharded;
-  p.os = stage_on && p.nout && fbytes(lv[0]) <= std::min<size_t>(32u << 10, budget0 / 4);
+  p.os = stage_on && !mc.s2_no_os && p.nout &&
+         fbytes(lv[0]) <= std::min<size_t>(32u << 10, budget0 / 4);
   const size_t os_bytes = p.os ? align128(fbytes(lv[0])) : 0;
   const double kRow = 0.94 * (rowbytes / 128.0), kRec = (p.aw == 2 ? 1.5 : 2.5) * G / 32.0;
   const double kL2 = 85.0, kL2Gather = 45.0, kFlush = 32.0;
@@ -762,6 +764,27 @@ bool launch_sweep2(Context& c, const float* const* in, float* const* outs) {
     if (std::getenv("MKB_DEBUG"))
       std::fprintf(stderr, "[mkb] fused sweep: common k=%d (%.1f us vs %.1f us per-mode choices)\n",
                    kc, common * 1e3, best_sum * 1e3);
+  }
+  // ... and one outer-staging choice: the outer row is read once per outer run, so modes
+  // that stage it are re-planned without (cfg3: mode 3's 2482-row outer factor never fits)
+  bool any_os = false, all_os = true;
+  for (uint32_t d = 0; d < c.n; ++d) {
+    const ModeCopy::Stream2& p = c.copies[d].s2;
+    if (p.nout) {
+      any_os |= p.os;
+      all_os &= p.os;
+    }
+  }
+  if (any_os && !all_os) {
+    for (uint32_t d = 0; d < c.n; ++d) {
+      ModeCopy& mc = c.copies[d];
+      if (!mc.s2.os) continue;
+      mc.s2_force_k = static_cast<int>(mc.s2.k);
+      mc.s2 = ModeCopy::Stream2();
+      mc.s2_no_os = true;
+      if (!prepare_stream2(c, d)) return false;
+    }
+    if (std::getenv("MKB_DEBUG")) std::fprintf(stderr, "[mkb] fused sweep: outer factor unstaged in every mode\n");
   }
   for (uint32_t d = 0; d < c.n; ++d) {
     if (!prepare_stream2(c, d)) return false;

@@ -153,7 +153,7 @@ def test_nonfinite_reported_by_each_kernel(mk):
 
 
 @pytest.mark.parametrize("dims,nnz", [([183, 24, 1140, 1717], 300_000), ([1000, 1000, 1000], 400_000),
-                                      ([6000, 9000, 30000], 600_000)])
+                                      ([6000, 9000, 30000], 600_000), ([2482, 2862, 14036, 17], 300_000)])
 def test_fused_sweep_matches_oracle(mk, orc, dims, nnz):
     """An unchained sweep runs as ONE launch (k_sweep2) when every mode shares the level-ordered
     kernel's specialisation; it must equal the per-mode results and the oracle, repeatedly and
@@ -169,6 +169,11 @@ def test_fused_sweep_matches_oracle(mk, orc, dims, nnz):
     for rep in range(3):
         c.sweep_async(False, False)
         c.synchronize()
+        # one k_sweep2 launch exactly when every mode's plan shares the kernel specialisation
+        # (outer level and staged-level count; outer staging is unified by the sweep itself)
+        infos = [c.fast_path_info(d) for d in range(len(dims))]
+        uniform = len({(i.kernel, i.outer_level, i.staged_levels) for i in infos}) == 1
+        assert c.last_sweep_fused() == uniform, [i.as_dict() for i in infos]
         for d in range(len(dims)):
             assert mk.verify_against(c.output(d), want[d])[0] <= 1e-4, (rep, d)
         single = c.mttkrp_mode(rep % len(dims))
