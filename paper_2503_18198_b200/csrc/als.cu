@@ -26,6 +26,12 @@
 namespace mkb {
 namespace {
 
+#ifndef ALS_NTH32
+#define ALS_NTH32 512
+#endif
+#ifndef ALS_NTH64
+#define ALS_NTH64 512
+#endif
 constexpr int kGramRows = 64;  // rows staged per block iteration
 
 // G += Yᵀ Y over a row range; one thread per (r, s) pair (s >= r mirrored at the end).
@@ -100,25 +106,39 @@ __device__ bool block_inverse(const double* __restrict__ grams, uint32_t n, uint
     if (threadIdx.x == 0) vmax = m;
   }
   __syncthreads();
-  for (uint32_t j = 0; j < R; ++j) {
-    const double piv = A[j * W2 + j];
+  // Gauss-Jordan without pivoting (V is SPD), one barrier per pivot: step j reads X and writes
+  // Y (ping-pong between A and the T|Pm region, free during the inverse).  Only the R + 1
+  // active columns change at step j: left columns [j, R) and right columns [R, R + j]; the
+  // others keep their final (left) or identity (right) values in both buffers.
+  double* bufs[2] = {A, T};
+  for (uint32_t p = threadIdx.x; p < 2 * RR; p += blockDim.x) T[p] = A[p];
+  __syncthreads();
+  uint32_t j = 0;
+  for (; j < R; ++j) {
+    const double* X = bufs[j & 1];
+    double* Y = bufs[(j + 1) & 1];
+    const double piv = X[j * W2 + j];
     if (!(piv > 1e-12 * vmax)) {
       if (threadIdx.x == 0) bad = 1;
       break;
     }
     const double inv = 1.0 / piv;
-    double* prow = scratch;  // the normalised pivot row (2R <= R*R)
-    for (uint32_t c = threadIdx.x; c < W2; c += blockDim.x) prow[c] = A[j * W2 + c] * inv;
-    for (uint32_t i = threadIdx.x; i < R; i += blockDim.x) fac[i] = A[i * W2 + j];
-    __syncthreads();
-    for (uint32_t q = threadIdx.x; q < R * W2; q += blockDim.x) {
-      const uint32_t i = q / W2, c = q % W2;
-      A[q] = i == j ? prow[c] : A[q] - fac[i] * prow[c];
+    const uint32_t act = R + 1;  // active columns: c' in [0, R+1) -> c = j + c'
+    for (uint32_t q = threadIdx.x; q < R * act; q += blockDim.x) {
+      const uint32_t i = q / act, c = j + q % act;
+      const double xjc = X[j * W2 + c] * inv;
+      Y[i * W2 + c] = i == j ? xjc : X[i * W2 + c] - X[i * W2 + j] * xjc;
     }
     __syncthreads();
   }
   __syncthreads();
-  if (!bad) return false;
+  if (!bad) {
+    if (R & 1) {  // odd R: the result sits in T; the callers read A
+      for (uint32_t p = threadIdx.x; p < 2 * RR; p += blockDim.x) A[p] = T[p];
+      __syncthreads();
+    }
+    return false;
+  }
   // cyclic Jacobi eigen-decomposition of V: T = V (diagonalised in place), Wv = eigenvectors
   double* V = T;
   double* Wv = scratch;
@@ -186,8 +206,10 @@ __device__ bool block_inverse(const double* __restrict__ grams, uint32_t n, uint
 // Phase 1: P += MᵀM over this CTA's rows; grid barrier; phase 2 (every CTA, redundantly):
 // V⁻¹, the Gram of M V⁻¹ = V⁻ᵀ P V⁻¹, λ, S = V⁻¹ diag(1/λ) (CTA 0 also writes G_d, λ and
 // the fit terms); phase 3: Y = M S over this CTA's rows.
-template <int RT>  // RT > 0: the rank at compile time (16 / 32 / 64); 0: runtime u.R <= 64
-__global__ void __launch_bounds__(256) k_als_update(const UpdArgs u) {
+// RT > 0: the rank at compile time (16 / 32 / 64); 0: runtime u.R <= 64.  NTH threads: the
+// per-pivot Gauss-Jordan step is R·(R+1) independent updates, so larger ranks get more threads.
+template <int RT, int NTH>
+__global__ void __launch_bounds__(NTH) k_als_update(const UpdArgs u) {
   extern __shared__ double dsm[];
   constexpr int RMAX = RT ? RT : 64;
   const uint32_t R = RT ? RT : u.R, RR = R * R, W2 = 2 * R;
@@ -203,7 +225,7 @@ __global__ void __launch_bounds__(256) k_als_update(const UpdArgs u) {
   const uint32_t r1 = static_cast<uint32_t>(static_cast<uint64_t>(u.rows) * (blockIdx.x + 1) / gridDim.x);
   // phase 1
   {
-    constexpr int PER = (RMAX * RMAX + 255) / 256;
+    constexpr int PER = (RMAX * RMAX + NTH - 1) / NTH;
     double acc[PER];
 #pragma unroll
     for (int k = 0; k < PER; ++k) acc[k] = 0.0;
@@ -215,7 +237,7 @@ __global__ void __launch_bounds__(256) k_als_update(const UpdArgs u) {
       __syncthreads();
 #pragma unroll
       for (int k = 0; k < PER; ++k) {
-        const uint32_t p = threadIdx.x + k * 256;
+        const uint32_t p = threadIdx.x + k * NTH;
         if (p < RR) {
           const uint32_t r = p / R, s = p % R;
           double a = 0.0;
@@ -228,7 +250,7 @@ __global__ void __launch_bounds__(256) k_als_update(const UpdArgs u) {
     if (r1 > r0) {
 #pragma unroll
       for (int k = 0; k < PER; ++k) {
-        const uint32_t p = threadIdx.x + k * 256;
+        const uint32_t p = threadIdx.x + k * NTH;
         if (p < RR) atomicAdd(&u.P[p], acc[k]);
       }
     }
@@ -245,8 +267,10 @@ __global__ void __launch_bounds__(256) k_als_update(const UpdArgs u) {
   }
   __syncthreads();
   // phase 2
-  for (uint32_t p = threadIdx.x; p < RR; p += blockDim.x) Pm[p] = __ldcg(&u.P[p]);
   const bool fell_back = block_inverse(u.grams, u.n, u.d, R, A, T, fac, scratch);
+  // (Pm shares the inverse's ping-pong buffer: loaded after it)
+  for (uint32_t p = threadIdx.x; p < RR; p += blockDim.x) Pm[p] = __ldcg(&u.P[p]);
+  __syncthreads();
   for (uint32_t p = threadIdx.x; p < RR; p += blockDim.x) {  // T = P V⁻¹
     const uint32_t r = p / R, c = p % R;
     double a = 0.0;
@@ -382,17 +406,17 @@ void als_update_mode(Context& c, uint32_t d) {
       c.num_sms, std::max<uint64_t>(1, (u.rows + kGramRows - 1) / kGramRows)));
   u.target = (c.als_bar_count += grid);
   ++c.als_epoch;
-  auto go = [&](auto kern, size_t smem) {
+  auto go = [&](auto kern, unsigned nth, size_t smem) {
     MKB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(smem)));
     void* params[] = {&u};
     MKB_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(kern), dim3(grid),
-                                         dim3(256), params, smem, st));
+                                         dim3(nth), params, smem, st));
   };
-  if (R == 16) go(k_als_update<16>, upd_smem(R));
-  else if (R == 32) go(k_als_update<32>, upd_smem(R));
-  else if (R == 64) go(k_als_update<64>, upd_smem(R));
-  else go(k_als_update<0>, upd_smem(R));
+  if (R == 16) go(k_als_update<16, 256>, 256, upd_smem(R));
+  else if (R == 32) go(k_als_update<32, ALS_NTH32>, ALS_NTH32, upd_smem(R));
+  else if (R == 64) go(k_als_update<64, ALS_NTH64>, ALS_NTH64, upd_smem(R));
+  else go(k_als_update<0, 256>, 256, upd_smem(R));
 }
 
 // fit after the last mode: the last update wrote [⟨X,X̂⟩, ||X̂||²]
