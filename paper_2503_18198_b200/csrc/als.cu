@@ -30,7 +30,7 @@ namespace {
 #define ALS_NTH32 512
 #endif
 #ifndef ALS_NTH64
-#define ALS_NTH64 512
+#define ALS_NTH64 1024
 #endif
 constexpr int kGramRows = 64;  // rows staged per block iteration
 
@@ -79,11 +79,106 @@ struct UpdArgs {
   int* status;
   unsigned int* bar;   // grid barrier counter (monotonic)
   unsigned int target; // barrier target for this launch
+  unsigned long long* prof;  // MKB_ALS_PROF: phase timestamps of CTA 0 (ns), else null
 };
+
+// C (R x R, ldc) = op(A) · B in fp64 shared memory, op(A)(r, k) = A[r*lda + k] or (TA)
+// A[k*lda + r].  Each thread owns a 2 x 4 register tile, so one k step reads 2 + 4 values for
+// 8 FMAs: these small products are shared-memory-bound, not FMA-bound.  VEC: 16-byte loads of
+// the B row segment (R % 4 == 0, 16-byte aligned B rows).
+template <bool TA, bool VEC>
+__device__ void smem_gemm(const double* Am, uint32_t lda, const double* Bm, uint32_t ldb,
+                          double* C, uint32_t ldc, uint32_t R) {
+  const uint32_t tr = (R + 1) / 2, tc = (R + 3) / 4;
+  for (uint32_t t = threadIdx.x; t < tr * tc; t += blockDim.x) {
+    const uint32_t r0 = (t / tc) * 2, c0 = (t % tc) * 4;
+    double acc[2][4] = {};
+    for (uint32_t k = 0; k < R; ++k) {
+      double a[2], b[4];
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        const uint32_t r = min(r0 + i, R - 1);
+        a[i] = TA ? Am[k * lda + r] : Am[r * lda + k];
+      }
+      if constexpr (VEC) {
+        const double2 b0 = *reinterpret_cast<const double2*>(Bm + k * ldb + c0);
+        const double2 b1 = *reinterpret_cast<const double2*>(Bm + k * ldb + c0 + 2);
+        b[0] = b0.x, b[1] = b0.y, b[2] = b1.x, b[3] = b1.y;
+      } else {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) b[j] = Bm[k * ldb + min(c0 + j, R - 1)];
+      }
+#pragma unroll
+      for (int i = 0; i < 2; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = fma(a[i], b[j], acc[i][j]);
+    }
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        if (r0 + i < R && c0 + j < R) C[(r0 + i) * ldc + c0 + j] = acc[i][j];
+  }
+}
 
 // Block-level V⁻¹ of the symmetric positive definite V = ⊛_{w≠d} G_w by Gauss-Jordan on
 // [V | I] (fp64, SMEM); Jacobi pseudo-inverse when a pivot <= 1e-12 max diag(V).  On return
 // A[:, R:] holds the (pseudo-)inverse.  Returns whether the fallback ran.
+// 1/x to ~1 ulp: the SFU's approximation plus two Newton steps (a division is a long
+// dependent sequence on the pivot chain).
+__device__ __forceinline__ double recip(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  double e = fma(-x, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-x, r, 1.0);
+  return fma(r, e, r);
+}
+
+// Gauss-Jordan on [V | I] (R x 2R, in A) with every thread holding one fixed segment of one
+// row in registers for all R steps: per step only the pivot row and the pivot column pass
+// through (double-buffered) shared memory, one barrier.  Returns false on a pivot
+// <= 1e-12 vmax (A is then left unspecified).
+template <int R, int NTH>
+__device__ bool gj_registers(double* A, double vmax) {
+  constexpr int W2 = 2 * R, TPR = NTH / R, CPT = W2 / TPR;
+  static_assert(NTH % R == 0 && W2 % TPR == 0, "thread layout");
+  __shared__ double prow[2][W2];
+  __shared__ double colj[2][R];
+  // thread (i, s) owns columns s + TPR*k of row i: a warp's pivot-row reads are consecutive
+  const int i = threadIdx.x / TPR, s0 = threadIdx.x % TPR;
+  double x[CPT];
+#pragma unroll
+  for (int k = 0; k < CPT; ++k) x[k] = A[i * W2 + s0 + TPR * k];
+  for (int j = 0; j < R; ++j) {
+    const int b = j & 1;
+    if (i == j) {
+#pragma unroll
+      for (int k = 0; k < CPT; ++k) prow[b][s0 + TPR * k] = x[k];
+    }
+#pragma unroll
+    for (int k = 0; k < CPT; ++k)
+      if (s0 + TPR * k == j) colj[b][i] = x[k];
+    __syncthreads();
+    const double piv = prow[b][j];
+    if (!(piv > 1e-12 * vmax)) return false;  // every thread sees the same pivot
+    const double inv = recip(piv);
+    if (i == j) {
+#pragma unroll
+      for (int k = 0; k < CPT; ++k) x[k] = prow[b][s0 + TPR * k] * inv;
+    } else {  // x -= (f / piv) * pivot row: one FMA per element
+      const double g = colj[b][i] * inv;
+#pragma unroll
+      for (int k = 0; k < CPT; ++k) x[k] = fma(-g, prow[b][s0 + TPR * k], x[k]);
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < CPT; ++k) A[i * W2 + s0 + TPR * k] = x[k];
+  __syncthreads();
+  return true;
+}
+
+template <int RT, int NTH>
 __device__ bool block_inverse(const double* __restrict__ grams, uint32_t n, uint32_t d, uint32_t R,
                               double* A, double* T, double* fac, double* scratch) {
   const uint32_t RR = R * R, W2 = 2 * R;
@@ -106,38 +201,43 @@ __device__ bool block_inverse(const double* __restrict__ grams, uint32_t n, uint
     if (threadIdx.x == 0) vmax = m;
   }
   __syncthreads();
-  // Gauss-Jordan without pivoting (V is SPD), one barrier per pivot: step j reads X and writes
-  // Y (ping-pong between A and the T|Pm region, free during the inverse).  Only the R + 1
-  // active columns change at step j: left columns [j, R) and right columns [R, R + j]; the
-  // others keep their final (left) or identity (right) values in both buffers.
-  double* bufs[2] = {A, T};
-  for (uint32_t p = threadIdx.x; p < 2 * RR; p += blockDim.x) T[p] = A[p];
-  __syncthreads();
-  uint32_t j = 0;
-  for (; j < R; ++j) {
-    const double* X = bufs[j & 1];
-    double* Y = bufs[(j + 1) & 1];
-    const double piv = X[j * W2 + j];
-    if (!(piv > 1e-12 * vmax)) {
-      if (threadIdx.x == 0) bad = 1;
-      break;
-    }
-    const double inv = 1.0 / piv;
-    const uint32_t act = R + 1;  // active columns: c' in [0, R+1) -> c = j + c'
-    for (uint32_t q = threadIdx.x; q < R * act; q += blockDim.x) {
-      const uint32_t i = q / act, c = j + q % act;
-      const double xjc = X[j * W2 + c] * inv;
-      Y[i * W2 + c] = i == j ? xjc : X[i * W2 + c] - X[i * W2 + j] * xjc;
-    }
+  if constexpr (RT > 0 && NTH % RT == 0 && (2 * RT) % (NTH / RT) == 0) {
+    if (gj_registers<RT, NTH>(A, vmax)) return false;
+    __syncthreads();  // singular: the Jacobi pseudo-inverse below
+  } else {
+    // Gauss-Jordan without pivoting (V is SPD), one barrier per pivot: step j reads X and writes
+    // Y (ping-pong between A and the T|Pm region, free during the inverse).  Only the R + 1
+    // active columns change at step j: left columns [j, R) and right columns [R, R + j]; the
+    // others keep their final (left) or identity (right) values in both buffers.
+    double* bufs[2] = {A, T};
+    for (uint32_t p = threadIdx.x; p < 2 * RR; p += blockDim.x) T[p] = A[p];
     __syncthreads();
-  }
-  __syncthreads();
-  if (!bad) {
-    if (R & 1) {  // odd R: the result sits in T; the callers read A
-      for (uint32_t p = threadIdx.x; p < 2 * RR; p += blockDim.x) A[p] = T[p];
+    uint32_t j = 0;
+    for (; j < R; ++j) {
+      const double* X = bufs[j & 1];
+      double* Y = bufs[(j + 1) & 1];
+      const double piv = X[j * W2 + j];
+      if (!(piv > 1e-12 * vmax)) {
+        if (threadIdx.x == 0) bad = 1;
+        break;
+      }
+      const double inv = 1.0 / piv;
+      const uint32_t act = R + 1;  // active columns: c' in [0, R+1) -> c = j + c'
+      for (uint32_t q = threadIdx.x; q < R * act; q += blockDim.x) {
+        const uint32_t i = q / act, c = j + q % act;
+        const double xjc = X[j * W2 + c] * inv;
+        Y[i * W2 + c] = i == j ? xjc : X[i * W2 + c] - X[i * W2 + j] * xjc;
+      }
       __syncthreads();
     }
-    return false;
+    __syncthreads();
+    if (!bad) {
+      if (R & 1) {  // odd R: the result sits in T; the callers read A
+        for (uint32_t p = threadIdx.x; p < 2 * RR; p += blockDim.x) A[p] = T[p];
+        __syncthreads();
+      }
+      return false;
+    }
   }
   // cyclic Jacobi eigen-decomposition of V: T = V (diagonalised in place), Wv = eigenvectors
   double* V = T;
@@ -221,14 +321,22 @@ __global__ void __launch_bounds__(NTH) k_als_update(const UpdArgs u) {
   double* fac = lam + R;       // R
   float* S = reinterpret_cast<float*>(fac + R);  // R x R
   float* tile = S + RR;                          // kGramRows x R
+  auto stamp = [&](int k) {
+    if (u.prof && blockIdx.x == 0 && threadIdx.x == 0) {
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      u.prof[k] = t;
+    }
+  };
+  stamp(0);
   const uint32_t r0 = static_cast<uint32_t>(static_cast<uint64_t>(u.rows) * blockIdx.x / gridDim.x);
   const uint32_t r1 = static_cast<uint32_t>(static_cast<uint64_t>(u.rows) * (blockIdx.x + 1) / gridDim.x);
-  // phase 1
+  // phase 1: P += MᵀM over this CTA's rows, 2 x 4 register tiles of P per thread
   {
-    constexpr int PER = (RMAX * RMAX + NTH - 1) / NTH;
-    double acc[PER];
-#pragma unroll
-    for (int k = 0; k < PER; ++k) acc[k] = 0.0;
+    constexpr bool VEC1 = RT > 0 && RT % 4 == 0;
+    constexpr int TPT = ((RMAX + 1) / 2 * ((RMAX + 3) / 4) + NTH - 1) / NTH;
+    const uint32_t tc = (R + 3) / 4, ntile = (R + 1) / 2 * tc;
+    double acc[TPT][2][4] = {};
     for (uint32_t b = r0; b < r1; b += kGramRows) {
       const uint32_t nr = min(r1 - b, static_cast<uint32_t>(kGramRows));
       __syncthreads();
@@ -236,27 +344,46 @@ __global__ void __launch_bounds__(NTH) k_als_update(const UpdArgs u) {
         tile[i] = u.M[static_cast<size_t>(b) * R + i];
       __syncthreads();
 #pragma unroll
-      for (int k = 0; k < PER; ++k) {
-        const uint32_t p = threadIdx.x + k * NTH;
-        if (p < RR) {
-          const uint32_t r = p / R, s = p % R;
-          double a = 0.0;
-          for (uint32_t i = 0; i < nr; ++i)
-            a += static_cast<double>(tile[i * R + r]) * static_cast<double>(tile[i * R + s]);
-          acc[k] += a;
+      for (int q = 0; q < TPT; ++q) {
+        const uint32_t t = threadIdx.x + q * NTH;
+        if (t >= ntile) continue;
+        const uint32_t ra = (t / tc) * 2, rb = min(ra + 1, R - 1), c0 = (t % tc) * 4;
+        for (uint32_t i = 0; i < nr; ++i) {
+          const float* row = tile + i * R;
+          const double a0 = row[ra], a1 = row[rb];
+          double bv[4];
+          if constexpr (VEC1) {
+            const float4 f = *reinterpret_cast<const float4*>(row + c0);
+            bv[0] = f.x, bv[1] = f.y, bv[2] = f.z, bv[3] = f.w;
+          } else {
+#pragma unroll
+            for (int j = 0; j < 4; ++j) bv[j] = row[min(c0 + j, R - 1)];
+          }
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            acc[q][0][j] = fma(a0, bv[j], acc[q][0][j]);
+            acc[q][1][j] = fma(a1, bv[j], acc[q][1][j]);
+          }
         }
       }
     }
     if (r1 > r0) {
 #pragma unroll
-      for (int k = 0; k < PER; ++k) {
-        const uint32_t p = threadIdx.x + k * NTH;
-        if (p < RR) atomicAdd(&u.P[p], acc[k]);
+      for (int q = 0; q < TPT; ++q) {
+        const uint32_t t = threadIdx.x + q * NTH;
+        if (t >= ntile) continue;
+        const uint32_t ra = (t / tc) * 2, c0 = (t % tc) * 4;
+#pragma unroll
+        for (int i = 0; i < 2; ++i)
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+            if (ra + i < R && c0 + j < R) atomicAdd(&u.P[(ra + i) * R + c0 + j], acc[q][i][j]);
       }
     }
   }
   // grid barrier (cooperative launch: every CTA is resident)
   __syncthreads();
+  stamp(1);
   if (threadIdx.x == 0) {
     __threadfence();
     atomicAdd(u.bar, 1u);
@@ -267,17 +394,14 @@ __global__ void __launch_bounds__(NTH) k_als_update(const UpdArgs u) {
   }
   __syncthreads();
   // phase 2
-  const bool fell_back = block_inverse(u.grams, u.n, u.d, R, A, T, fac, scratch);
+  stamp(2);
+  const bool fell_back = block_inverse<RT, NTH>(u.grams, u.n, u.d, R, A, T, fac, scratch);
+  stamp(3);
   // (Pm shares the inverse's ping-pong buffer: loaded after it)
   for (uint32_t p = threadIdx.x; p < RR; p += blockDim.x) Pm[p] = __ldcg(&u.P[p]);
   __syncthreads();
-  for (uint32_t p = threadIdx.x; p < RR; p += blockDim.x) {  // T = P V⁻¹
-    const uint32_t r = p / R, c = p % R;
-    double a = 0.0;
-#pragma unroll 8
-    for (uint32_t k = 0; k < R; ++k) a += Pm[r * R + k] * A[k * W2 + R + c];
-    T[p] = a;
-  }
+  constexpr bool VEC = RT > 0 && RT % 4 == 0;
+  smem_gemm<false, VEC>(Pm, R, A + R, W2, T, R, R);  // T = P V⁻¹
   __syncthreads();
   for (uint32_t r = threadIdx.x; r < R; r += blockDim.x) {
     double a = 0.0;
@@ -290,20 +414,22 @@ __global__ void __launch_bounds__(NTH) k_als_update(const UpdArgs u) {
     S[p] = static_cast<float>(A[(p / R) * W2 + R + p % R] / lam[p % R]);
   if (blockIdx.x == 0) {
     double* G = u.grams + static_cast<size_t>(u.d) * RR;
+    double* Gs = scratch;  // (the Jacobi fallback's buffer, free here)
+    smem_gemm<true, VEC>(A + R, W2, T, R, Gs, R, R);  // V⁻ᵀ P V⁻¹
+    __syncthreads();
     for (uint32_t p = threadIdx.x; p < RR; p += blockDim.x) {
       const uint32_t r = p / R, c = p % R;
-      double a = 0.0;
-      for (uint32_t k = 0; k < R; ++k) a += A[k * W2 + R + r] * T[k * R + c];
-      G[p] = a / (lam[r] * lam[c]);
+      G[p] = Gs[p] / (lam[r] * lam[c]);
       u.P_next[p] = 0.0;
     }
     for (uint32_t r = threadIdx.x; r < R; r += blockDim.x) u.lambda[r] = static_cast<float>(lam[r]);
     __syncthreads();
-    if (u.last && threadIdx.x < 32) {
+    if (u.last) {
       // ⟨X, X̂⟩ = Σ_r λ_r (P S)_rr = trace(P V⁻¹);  ||X̂||² = λᵀ (⊛_w G_w) λ
+      __shared__ double red[2][32];
       double inner = 0.0, model = 0.0;
-      for (uint32_t r = threadIdx.x; r < R; r += 32) inner += T[r * R + r];
-      for (uint32_t p = threadIdx.x; p < RR; p += 32) {
+      for (uint32_t r = threadIdx.x; r < R; r += blockDim.x) inner += T[r * R + r];
+      for (uint32_t p = threadIdx.x; p < RR; p += blockDim.x) {
         double v = lam[p / R] * lam[p % R];
         for (uint32_t w = 0; w < u.n; ++w) v *= u.grams[static_cast<size_t>(w) * RR + p];
         model += v;
@@ -312,14 +438,22 @@ __global__ void __launch_bounds__(NTH) k_als_update(const UpdArgs u) {
         inner += __shfl_xor_sync(0xffffffffu, inner, o);
         model += __shfl_xor_sync(0xffffffffu, model, o);
       }
+      if ((threadIdx.x & 31) == 0) {
+        red[0][threadIdx.x >> 5] = inner;
+        red[1][threadIdx.x >> 5] = model;
+      }
+      __syncthreads();
       if (threadIdx.x == 0) {
-        u.scalars[0] = inner;
-        u.scalars[1] = model;
+        double a = 0.0, b = 0.0;
+        for (uint32_t w = 0; w < blockDim.x / 32; ++w) a += red[0][w], b += red[1][w];
+        u.scalars[0] = a;
+        u.scalars[1] = b;
       }
     }
     if (threadIdx.x == 0) u.status[0] = fell_back ? 1 : 0;
   }
   __syncthreads();
+  stamp(4);
   // phase 3: Y = M S
   for (uint32_t b = r0; b < r1; b += kGramRows) {
     const uint32_t nr = min(r1 - b, static_cast<uint32_t>(kGramRows));
@@ -335,6 +469,7 @@ __global__ void __launch_bounds__(NTH) k_als_update(const UpdArgs u) {
       u.Y[static_cast<size_t>(b) * R + p] = a;
     }
   }
+  stamp(5);
 }
 
 size_t upd_smem(uint32_t R) {
@@ -402,6 +537,10 @@ void als_update_mode(Context& c, uint32_t d) {
   u.last = d + 1 == n ? 1 : 0;
   u.status = c.als_status.get();
   u.bar = c.als_bar.get();
+  static DevBuf<unsigned long long> prof;
+  const bool do_prof = std::getenv("MKB_ALS_PROF") != nullptr;
+  if (do_prof) prof.resize(8);
+  u.prof = do_prof ? prof.get() : nullptr;
   const unsigned grid = static_cast<unsigned>(std::min<uint64_t>(
       c.num_sms, std::max<uint64_t>(1, (u.rows + kGramRows - 1) / kGramRows)));
   u.target = (c.als_bar_count += grid);
@@ -417,6 +556,14 @@ void als_update_mode(Context& c, uint32_t d) {
   else if (R == 32) go(k_als_update<32, ALS_NTH32>, ALS_NTH32, upd_smem(R));
   else if (R == 64) go(k_als_update<64, ALS_NTH64>, ALS_NTH64, upd_smem(R));
   else go(k_als_update<0, 256>, 256, upd_smem(R));
+  if (do_prof) {
+    unsigned long long h[8];
+    MKB_CUDA(cudaMemcpyAsync(h, prof.get(), sizeof h, cudaMemcpyDeviceToHost, st));
+    MKB_CUDA(cudaStreamSynchronize(st));
+    std::fprintf(stderr, "[als] mode %u grid %u: phase1 %.1f barrier %.1f inverse %.1f T/S/G %.1f apply %.1f us\n", d, grid,
+                 (h[1] - h[0]) * 1e-3, (h[2] - h[1]) * 1e-3, (h[3] - h[2]) * 1e-3, (h[4] - h[3]) * 1e-3,
+                 (h[5] - h[4]) * 1e-3);
+  }
 }
 
 // fit after the last mode: the last update wrote [⟨X,X̂⟩, ||X̂||²]
