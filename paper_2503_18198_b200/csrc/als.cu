@@ -91,14 +91,21 @@ __device__ void smem_gemm(const double* Am, uint32_t lda, const double* Bm, uint
                           double* C, uint32_t ldc, uint32_t R) {
   const uint32_t tr = (R + 1) / 2, tc = (R + 3) / 4;
   for (uint32_t t = threadIdx.x; t < tr * tc; t += blockDim.x) {
-    const uint32_t r0 = (t / tc) * 2, c0 = (t % tc) * 4;
+    // TA: lanes walk row pairs (adjacent A elements, one 16-B load) and warps walk column
+    // segments (a broadcast B load); else lanes walk column segments
+    const uint32_t r0 = (TA ? t % tr : t / tc) * 2, c0 = (TA ? t / tr : t % tc) * 4;
     double acc[2][4] = {};
     for (uint32_t k = 0; k < R; ++k) {
       double a[2], b[4];
+      if constexpr (TA && VEC) {
+        const double2 av = *reinterpret_cast<const double2*>(Am + k * lda + r0);
+        a[0] = av.x, a[1] = av.y;
+      } else {
 #pragma unroll
-      for (int i = 0; i < 2; ++i) {
-        const uint32_t r = min(r0 + i, R - 1);
-        a[i] = TA ? Am[k * lda + r] : Am[r * lda + k];
+        for (int i = 0; i < 2; ++i) {
+          const uint32_t r = min(r0 + i, R - 1);
+          a[i] = TA ? Am[k * lda + r] : Am[r * lda + k];
+        }
       }
       if constexpr (VEC) {
         const double2 b0 = *reinterpret_cast<const double2*>(Bm + k * ldb + c0);
@@ -401,7 +408,7 @@ __global__ void __launch_bounds__(NTH) k_als_update(const UpdArgs u) {
   for (uint32_t p = threadIdx.x; p < RR; p += blockDim.x) Pm[p] = __ldcg(&u.P[p]);
   __syncthreads();
   constexpr bool VEC = RT > 0 && RT % 4 == 0;
-  smem_gemm<false, VEC>(Pm, R, A + R, W2, T, R, R);  // T = P V⁻¹
+  smem_gemm<true, VEC>(Pm, R, A + R, W2, T, R, R);  // T = P V⁻¹ = Pᵀ V⁻¹ (P = MᵀM)
   __syncthreads();
   for (uint32_t r = threadIdx.x; r < R; r += blockDim.x) {
     double a = 0.0;
