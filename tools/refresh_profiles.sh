@@ -11,3 +11,6 @@ echo "reference rc=$?"
 TAG=$TAG CFGS="cfg2" bash tools/profile_round.sh
 # cfg3's timed run re-plans every mode to K = 0 (L1-fed gathers): profile that plan
 MKB_FORCE_K=0,0,0,0 TAG=$TAG CFGS="cfg3" bash tools/profile_round.sh
+# cfg5's and cfg1's timed runs keep K = 1 (one inner level staged); the cost model alone
+# would pick K = 2, so the profiled runs force the timed choice
+MKB_FORCE_K=1,1,1 TAG=$TAG CFGS="cfg5 cfg1" bash tools/profile_round.sh
