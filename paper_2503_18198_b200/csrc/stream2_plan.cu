@@ -293,7 +293,8 @@ bool prepare_stream2(Context& c, uint32_t mode) {
   //      LSU   = 0.94 per 128-B row gathered (shared or L1) + the record read
   //      L2    = bytes gathered from L2 / 45 B per SM-cycle: L2-fed gathers are latency-bound
   //              at 16 warps, so they add to the LSU time (L1 hit rate ~ free L1 / factor)
-  //      flush = 32 per atomic row flush: every (block, row) pair of a blocked plan
+  //      flush = 150 per atomic row flush (every (block, row) pair of a blocked plan): a
+  //              128-B vector atomic plus the divergent flagged-element path (cfg5)
   //      stage = per CTA item: staged slice bytes / 85 B per SM-cycle + a ~6000-cycle stall
   //    cost = LSU + L2 + flush + stage (fitted to the measured cfg2 / cfg3 / cfg5 plans).
   //    CTA size: a plan that stages every inner level gathers only from shared memory and
@@ -312,7 +313,7 @@ bool prepare_stream2(Context& c, uint32_t mode) {
          fbytes(lv[0]) <= std::min<size_t>(32u << 10, budget0 / 4);
   const size_t os_bytes = p.os ? align128(fbytes(lv[0])) : 0;
   const double kRow = 0.94 * (rowbytes / 128.0), kRec = (p.aw == 2 ? 1.5 : 2.5) * G / 32.0;
-  const double kL2 = 85.0, kL2Gather = 45.0, kFlush = 32.0;
+  const double kL2 = 85.0, kL2Gather = 45.0, kFlush = env_int("MKB_KFLUSH", 150);
   struct Cand {
     bool swap = false;
     uint32_t k = 0, rows[4] = {1, 1, 1, 1}, split[4] = {1, 1, 1, 1};
