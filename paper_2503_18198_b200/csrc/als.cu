@@ -19,6 +19,7 @@
 //   ||X̂||² = λᵀ (⊛_w G_w) λ — both written by the last mode's update.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <vector>
 
 #include "context.cuh"
@@ -544,10 +545,9 @@ void als_update_mode(Context& c, uint32_t d) {
   u.last = d + 1 == n ? 1 : 0;
   u.status = c.als_status.get();
   u.bar = c.als_bar.get();
-  static DevBuf<unsigned long long> prof;
-  const bool do_prof = std::getenv("MKB_ALS_PROF") != nullptr;
-  if (do_prof) prof.resize(8);
-  u.prof = do_prof ? prof.get() : nullptr;
+  const bool do_prof = std::getenv("MKB_ALS_PROF") != nullptr;  // per-phase times to stderr
+  if (do_prof) c.als_prof.resize(8);
+  u.prof = do_prof ? c.als_prof.get() : nullptr;
   const unsigned grid = static_cast<unsigned>(std::min<uint64_t>(
       c.num_sms, std::max<uint64_t>(1, (u.rows + kGramRows - 1) / kGramRows)));
   u.target = (c.als_bar_count += grid);
@@ -565,7 +565,7 @@ void als_update_mode(Context& c, uint32_t d) {
   else go(k_als_update<0, 256>, 256, upd_smem(R));
   if (do_prof) {
     unsigned long long h[8];
-    MKB_CUDA(cudaMemcpyAsync(h, prof.get(), sizeof h, cudaMemcpyDeviceToHost, st));
+    MKB_CUDA(cudaMemcpyAsync(h, c.als_prof.get(), sizeof h, cudaMemcpyDeviceToHost, st));
     MKB_CUDA(cudaStreamSynchronize(st));
     std::fprintf(stderr, "[als] mode %u grid %u: phase1 %.1f barrier %.1f inverse %.1f T/S/G %.1f apply %.1f us\n", d, grid,
                  (h[1] - h[0]) * 1e-3, (h[2] - h[1]) * 1e-3, (h[3] - h[2]) * 1e-3, (h[4] - h[3]) * 1e-3,

@@ -151,6 +151,7 @@ struct Context {
   DevBuf<float> lambda;   // R
   DevBuf<double> als_scalars;
   DevBuf<int> als_status;
+  DevBuf<unsigned long long> als_prof;  // MKB_ALS_PROF: phase timestamps of the update
   bool grams_valid = false;
   bool last_sweep_fused = false;  // the last sweep() ran as one k_sweep2 launch
 };
