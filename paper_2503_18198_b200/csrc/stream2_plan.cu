@@ -309,7 +309,10 @@ bool prepare_stream2(Context& c, uint32_t mode) {
   const size_t budget0 = budget_for(0);
   const bool stage_on = env_int("MKB_STAGE", 1) != 0;
   const bool block_on = env_int("MKB_BLOCK", 1) != 0 && !sharded;
-  p.os = stage_on && !mc.s2_no_os && p.nout &&
+  // The outer row is read once per outer run (folded, stream2.cuh), through L1/L2 with its
+  // latency hidden until the next fold; staging it costs shared memory the inner levels use
+  // better (cfg2 mode 1: 6 -> 4 blocks, sweep 0.156 -> 0.154 ms).  MKB_OUTER_STAGE=1 stages it.
+  p.os = stage_on && !mc.s2_no_os && env_int("MKB_OUTER_STAGE", 0) && p.nout &&
          fbytes(lv[0]) <= std::min<size_t>(32u << 10, budget0 / 4);
   const size_t os_bytes = p.os ? align128(fbytes(lv[0])) : 0;
   const double kRow = 0.94 * (rowbytes / 128.0), kRec = (p.aw == 2 ? 1.5 : 2.5) * G / 32.0;
