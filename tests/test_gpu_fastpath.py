@@ -13,6 +13,8 @@ Scheme 2 drifts ~5e-6 on far shorter rows.
 import numpy as np
 import pytest
 
+from oracle import als as als_oracle
+
 pytestmark = pytest.mark.gpu
 
 # (dims, nnz, rank, expected level-ordered plan kinds of some mode)
@@ -253,3 +255,34 @@ def test_sweep_host_packed_and_separate_buffers(mk, orc):
         # atomic row flushes make the last bits run-dependent: both against the oracle
         assert mk.verify_against(op[d], want[d])[0] <= 1e-4
         assert mk.verify_against(sep[d], want[d])[0] <= 1e-4
+
+
+def test_fused_sweep_unifies_outer_staging(mk, orc, monkeypatch):
+    """MKB_OUTER_STAGE=1 stages the outer factor where it fits (modes 0-2 of this shape) but not
+    where it does not (mode 3: 2482 rows x 256 B); the fused sweep re-plans every mode without
+    it (stream2_plan.cu launch_sweep2) and still runs as one launch matching the oracle."""
+    monkeypatch.setenv("MKB_OUTER_STAGE", "1")
+    dims = [2482, 2862, 14036, 17]
+    t = mk.generate_powerlaw(dims, 3_100_000, 1.0, 1)  # cfg3 at full size: every mode has an outer level
+    f = [m.data for m in mk.random_factors(dims, 64, 5)]
+    c = mk.Context()
+    c.upload_tensor(t)
+    c.build_plans(148)
+    c.upload_factors(f)  # timed plan choice: every mode settles on K = 0 (see bench cfg3)
+    want = [orc.mttkrp(dims, t.coords, t.values, f, d) for d in range(4)]
+    for rep in range(2):
+        c.sweep_async(False, False)
+        c.synchronize()
+        infos = [c.fast_path_info(d) for d in range(4)]
+        uniform = len({(i.kernel, i.outer_level, i.staged_levels) for i in infos}) == 1
+        assert c.last_sweep_fused() == uniform, [i.as_dict() for i in infos]
+        for d in range(4):
+            got = c.output(d)
+            err = mk.verify_against(got, want[d])[0]
+            if err > 1e-4:
+                # power-law head rows (~1M nnz): the reference's sequential fp32 sum itself
+                # drifts ~1e-4; the fast path must be at least as close to the fp64 truth
+                truth = als_oracle.mttkrp64(dims, t.coords, t.values, f, d)
+                e_fast = mk.verify_against(got.astype(np.float64), truth)[0]
+                e_orc = mk.verify_against(want[d].astype(np.float64), truth)[0]
+                assert e_fast <= e_orc, (rep, d, err, e_fast, e_orc)
