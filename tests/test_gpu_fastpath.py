@@ -286,3 +286,31 @@ def test_fused_sweep_unifies_outer_staging(mk, orc, monkeypatch):
                 e_fast = mk.verify_against(got.astype(np.float64), truth)[0]
                 e_orc = mk.verify_against(want[d].astype(np.float64), truth)[0]
                 assert e_fast <= e_orc, (rep, d, err, e_fast, e_orc)
+
+
+def test_sharded_ranges_timed_choice(mk, orc):
+    """Row-range shards with the timed kernel/plan choice (the multi-GPU bench path): sharded
+    plans cannot block, so some staged-level counts are rejected; owned rows match the oracle."""
+    dims = [183, 24, 1140, 1717]
+    t = mk.generate_synthetic(dims, 400_000, seed=8)
+    f = [m.data for m in mk.random_factors(dims, 32, 8)]
+    want = [orc.mttkrp(dims, t.coords, t.values, f, d) for d in range(4)]
+    world = 2
+    for r in range(world):
+        c = mk.Context()
+        c.upload_tensor(t)
+        c.build_plans(148)
+        c.upload_factors(f)
+        c.set_shard(r, world)
+        for d in range(4):
+            c.mttkrp_mode_async(d)
+            c.synchronize()
+            k0, k1 = c.shard_rows(d, r)
+            seq = orc.build_plan(dims, t.coords, d, 148, 0, 0)
+            order = np.asarray(seq["order"], dtype=np.int64)
+            cd = np.asarray(t.coords)[order, d]
+            own = cd[np.r_[True, cd[1:] != cd[:-1]]][k0:k1]
+            got = c.output(d)
+            if len(own):
+                err = np.abs(got[own] - want[d][own]).max() / max(1.0, np.abs(want[d][own]).max())
+                assert err <= 1e-4, (r, d, err, c.fast_path_info(d).as_dict())
