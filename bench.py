@@ -1,11 +1,14 @@
 #!/usr/bin/env python3
 """Benchmark: all-mode spMTTKRP per CPD iteration on B200 (BASELINE.json metric).
 
-  python bench.py [--gpus N --steps K --warmup W] [--config cfg2] [--impl ours|reference]
+  python bench.py [--gpus N --steps K --warmup W] [--config cfg5] [--only] [--impl ours|reference]
 
 A step is one all-mode spMTTKRP sweep (Algorithm 1; the unit the
 reference's run_timed measures, kernel.hpp:239-287) over the configured synthetic tensor.
-Default workload: BASELINE configs[1] (uber-shaped 183x24x1140x1717, 3.3M nnz, R=32).
+Headline workload: BASELINE configs[4] (nell-2-shaped 12092x9184x28818, 77M nnz, R=32) — the
+config the metric's "1/2/4/8 B200" is quoted on and the largest single-GPU one.  The other
+BASELINE configs (cfg1-cfg4) follow as sub-records of the same JSON line ("configs"), each with
+its own roofline and CPU baseline, unless --only is given.
 
 value      device time per sweep (ms, mean over K steps; CUDA events on the launch stream,
            tensor copies + factors resident in HBM, L2 flushed between steps)
@@ -13,7 +16,11 @@ e2e        the same sweep through the public C ABI with HOST buffers: H2D of eve
            from pinned memory + sweep + D2H of every output, per step (mk_sweep_host)
 roofline   HBM bound: algorithmic bytes per sweep (Σ_d nnz(4N+4) + 4R(Σ_{w≠d}D_w+I_d))
            ÷ the MTTKRP kernels' mean duration, vs MEASURED_PEAKS.json hbm_gbs
-cpu_baseline  the reference compiled from its own sources (oracle/_ref) timed on this host
+parity     after the timed loop: the last timed sweep's outputs vs the device fp64 deterministic
+           result (bitwise = the reference's oracle_mttkrp<double>, tests/test_gpu_parity_full.py)
+cpu_baseline  the reference compiled from its own sources (oracle/_ref) timed on this host:
+           run_timed on the FULL tensor at kappa = nproc and kappa = 148 (plans from the
+           oracle's bit-identical planner, pinned against the reference's build_mode_plans)
 """
 import argparse
 import json
@@ -30,6 +37,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "all-mode spMTTKRP ms/CPD-iter, HBM GB/s vs roofline; 1/2/4/8 B200 vs host CPU"
+HEADLINE = "cfg5"
 
 CONFIGS = {
     "cfg1": dict(desc="synthetic 3-mode 1000x1000x1000, 1M nnz uniform, R=32",
@@ -43,6 +51,7 @@ CONFIGS = {
     "cfg5": dict(desc="nell-2-shaped 3-mode 12092x9184x28818, 77M nnz uniform, R=32",
                  dims=[12092, 9184, 28818], nnz=77_000_000, rank=32, gen="uniform"),
 }
+CPU_BUDGET_S = 45.0  # per (config, kappa) of timed reference sweeps
 
 
 def log(*a):
@@ -54,10 +63,15 @@ def dist_env():
             int(os.environ.get("LOCAL_RANK", 0)))
 
 
-def make_tensor(mk, cfg):
-    if cfg["gen"] == "powerlaw":
-        return mk.generate_powerlaw(cfg["dims"], cfg["nnz"], 1.0, 1)
-    return mk.generate_synthetic(cfg["dims"], cfg["nnz"], seed=1)
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for line in fh:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
 
 
 def algorithmic_bytes(dims, nnz, rank, distinct):
@@ -140,90 +154,121 @@ def ncu_traffic(config_name):
         return None
 
 
-# ----------------------------------------------------------------------------- reference arm
+def lsu_roofline(config_name, kern_ms):
+    """Secondary (binding) roofline: bytes through the SM's L1/shared-memory data path per
+    sweep (l1tex data-pipe wavefronts x 128 B from the committed ncu capture) against the
+    chip's 128 B/clk/SM x 148 SMs x sm clock."""
+    path = os.path.join(ROOT, "profiles", "ncu_lsu.json")
+    try:
+        with open(path) as fh:
+            entry = json.load(fh).get(config_name)
+        if not entry:
+            return None
+        peak = 128.0 * entry["sms"] * entry["sm_mhz"] * 1e6 / 1e9  # GB/s
+        achieved = entry["lsu_bytes_per_sweep"] / (kern_ms * 1e-3) / 1e9
+        return {"bound": "l1/smem data path", "achieved": achieved, "peak": peak,
+                "unit": "GB/s", "frac": achieved / peak, "source": entry.get("source")}
+    except Exception:
+        return None
+
+
+# ----------------------------------------------------------------------------- CPU reference
+def ref_generate(cfg):
+    """The workload's tensor from the ORACLE generators (bit-identical to the reference's,
+    pinned in tests/test_oracle.py; the product library is not loaded in the reference arm)."""
+    import oracle
+    orc = oracle.Oracle()
+    if cfg["gen"] == "powerlaw":
+        c, v = orc.generate_powerlaw(cfg["dims"], cfg["nnz"], 1.0, 1)
+    else:
+        c, v = orc.generate_synthetic(cfg["dims"], cfg["nnz"], 0, 0, 2, 1)
+    f = orc.random_factors(cfg["dims"], cfg["rank"], 1)
+    return c, v, f
+
+
+def cpu_reference(cfg, coords, values, factors, max_steps, warmup):
+    """The reference's own run_timed (oracle/_ref, kernel.hpp:239-287) on the full tensor, at
+    kappa = nproc (the CLI default, mttkrp_bench.cpp:54-57) and kappa = 148.
+    Plans come from the oracle's planner (bit-identical to build_mode_plans, pinned), so the
+    reference's ~90 s single-threaded plan sort at 77M nnz stays out of the run.  Each kappa
+    gets `warmup` untimed sweeps and up to `max_steps` timed ones within CPU_BUDGET_S."""
+    import oracle
+    cores = os.cpu_count() or 1
+    orc = oracle.Oracle()
+    dims = cfg["dims"]
+    if not oracle.reference_available():
+        # no compiled reference: the single-threaded C port of the oracle (kind "port")
+        t0 = time.perf_counter()
+        for d in range(len(dims)):
+            orc.mttkrp(dims, coords, values, factors, d)
+        v = (time.perf_counter() - t0) * 1e3
+        return {"value": v, "unit": "ms", "cores": 1, "kind": "port",
+                "sample": "full tensor, 1 sweep of the oracle port (single thread)",
+                "cpu_model": cpu_model()}
+    ref = oracle.Reference()
+    rows = {}
+    for kappa in sorted({cores, 148}):
+        t0 = time.perf_counter()
+        plans = orc.build_plans_all(dims, coords, kappa)
+        plan_s = time.perf_counter() - t0
+        # one probe sweep to size the sample, then warm-up + timed sweeps
+        tot, _, _ = ref.run_timed_plans(dims, coords, values, factors, kappa, plans, 1)
+        per = max(float(tot[0]) / 1e3, 1e-3)
+        steps = int(max(2, min(max_steps, CPU_BUDGET_S // per)))
+        w = max(0, min(warmup, int(10.0 // per)))
+        tot, mode_min, ident = ref.run_timed_plans(dims, coords, values, factors, kappa, plans,
+                                                   w + steps)
+        timed = [float(x) for x in tot[w:]]
+        rows[kappa] = {"kappa": kappa, "ms_mean": float(np.mean(timed)),
+                       "ms_min": float(np.min(timed)), "steps": len(timed), "warmup": w + 1,
+                       "mode_min_ms": [float(x) for x in mode_min],
+                       "outputs_bit_identical": ident, "plan_build_s": plan_s}
+        del plans
+    best = min(rows.values(), key=lambda r: r["ms_mean"])
+    return {"value": best["ms_mean"], "unit": "ms", "cores": cores, "kind": "reference",
+            "kappa": best["kappa"], "cpu_model": cpu_model(),
+            "sample": (f"full tensor ({cfg['nnz']} nnz); reference run_timed (oracle/_ref) at "
+                       f"kappa=nproc={cores} and kappa=148, adaptive/cyclic, P=32; value = mean "
+                       f"of the faster kappa's timed sweeps (kappa={best['kappa']}, "
+                       f"{best['steps']} timed after {best['warmup']} untimed)"),
+            "per_kappa": list(rows.values())}
+
+
 def reference_arm(args, cfg, rank, world):
     if rank != 0:
         return 0
-    import oracle
-    t = None
-    import paper_2503_18198_b200 as mk  # host generator only (bit-identical to the reference's)
-    t = make_tensor(mk, cfg)
-    f = [m.data for m in mk.random_factors(cfg["dims"], cfg["rank"], 1)]
-    cores = os.cpu_count() or 1
-    if oracle.reference_available():
-        ref = oracle.Reference()
-        totals, mode_min, plan_ms = ref.run_timed(cfg["dims"], t.coords, t.values, f, cores,
-                                                  args.warmup + args.steps)
-        timed = totals[args.warmup:]
-        kind, sample = "reference", (f"full tensor, build_mode_plans(kappa=nproc={cores}) "
-                                     f"+ run_timed {args.warmup}+{args.steps} iters")
-    else:
-        orc = oracle.Oracle()
-        timed = []
-        for s in range(args.warmup + args.steps):
-            t0 = time.perf_counter()
-            for d in range(len(cfg["dims"])):
-                orc.mttkrp(cfg["dims"], t.coords, t.values, f, d)
-            if s >= args.warmup:
-                timed.append((time.perf_counter() - t0) * 1e3)
-        cores, kind, sample = 1, "port", "full tensor, oracle port (single thread)"
-    v = float(np.mean(timed))
-    line = {"metric": METRIC, "value": v, "unit": "ms", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": v, "higher_is_better": False,
+    c, v, f = ref_generate(cfg)
+    cb = cpu_reference(cfg, c, v, f, args.steps, args.warmup)
+    val = cb["value"]
+    line = {"metric": METRIC, "value": val, "unit": "ms", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": val, "higher_is_better": False,
             "scaling": "strong", "vs_baseline": None, "dtype": "f32", "impl": "reference",
-            "data": "synthetic (reference generator, seed 1)",
-            "config": {"workload": f"{args.config}: {cfg['desc']}", "kappa": cores},
-            "cpu_baseline": {"value": v, "unit": "ms", "cores": cores, "kind": kind,
-                             "sample": sample},
-            "e2e": {"value": v, "unit": "ms", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+            "data": "synthetic (oracle generator = the reference's generate_synthetic, seed 1)",
+            "config": {"workload": f"{args.config}: {cfg['desc']}", "kappa": cb.get("kappa")},
+            "cpu_baseline": cb,
+            "e2e": {"value": val, "unit": "ms", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
 
 
-def cpu_baseline_sample(cfg, t, factors):
-    """Reference CPU path on a bounded sample of the same workload (rank 0, N=1)."""
-    import oracle
-    cores = os.cpu_count() or 1
-    dims = cfg["dims"]
-    sample_nnz = min(t.nnz, 4_000_000)
-    coords, vals = t.coords[:sample_nnz], t.values[:sample_nnz]
-    scale = t.nnz / sample_nnz
-    if oracle.reference_available():
-        ref = oracle.Reference()
-        totals, _, plan_ms = ref.run_timed(dims, coords, vals, factors, cores, 3)
-        v = float(np.median(totals)) * scale
-        return {"value": v, "unit": "ms", "cores": cores, "kind": "reference",
-                "sample": (f"first {sample_nnz} nnz of the workload, reference build_mode_plans("
-                           f"kappa={cores}) + run_timed 3 iters (median), scaled by nnz x{scale:.2f};"
-                           f" plan build {plan_ms:.0f} ms")}
-    orc = oracle.Oracle()
-    t0 = time.perf_counter()
-    for d in range(len(dims)):
-        orc.mttkrp(dims, coords, vals, factors, d)
-    v = (time.perf_counter() - t0) * 1e3 * scale
-    return {"value": v, "unit": "ms", "cores": 1, "kind": "port",
-            "sample": f"first {sample_nnz} nnz, oracle port single-thread, scaled x{scale:.2f}"}
-
-
 # ----------------------------------------------------------------------------- our arm
-def our_arm(args, cfg, rank, world, local_rank):
+def make_tensor(mk, cfg):
+    if cfg["gen"] == "powerlaw":
+        return mk.generate_powerlaw(cfg["dims"], cfg["nnz"], 1.0, 1)
+    return mk.generate_synthetic(cfg["dims"], cfg["nnz"], seed=1)
+
+
+def run_config(args, name, rank, world, local_rank, stream, with_cpu):
+    """Our arm on one config; returns the JSON record (rank 0) or None."""
     import torch
     import paper_2503_18198_b200 as mk
 
-    torch.cuda.set_device(local_rank)
-    if world > 1:
-        import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    cfg = CONFIGS[name]
     dims, R = cfg["dims"], cfg["rank"]
     n = len(dims)
+    dev = torch.device("cuda", local_rank)
     t = make_tensor(mk, cfg)
     factors = [m.data for m in mk.random_factors(dims, R, 1)]
-    dev = torch.device("cuda", local_rank)
-    # A dedicated (non-default) stream shared by torch's events and the library: the
-    # legacy default stream's handle is NULL, which the C ABI reads as "own stream".
-    stream = torch.cuda.Stream(dev)
-    torch.cuda.set_stream(stream)
-    assert stream.cuda_stream != 0
 
     ctx = mk.Context(local_rank)
     ctx.set_stream(stream.cuda_stream)
@@ -239,40 +284,20 @@ def our_arm(args, cfg, rank, world, local_rank):
     infos = [ctx.plan_info(d) for d in range(n)]
     distinct = [int(i.distinct_rows) for i in infos]
     ctx.upload_factors(factors)
+    b_iter = float(sum(algorithmic_bytes(dims, t.nnz, R, distinct)))
 
-    # quick parity gate on the benchmarked workload: fast vs deterministic (bitwise ==
-    # the reference oracle, tests/test_gpu_mttkrp.py) within 1e-5
-    det = ctx.mttkrp_all_modes(False, True)
-    fast = ctx.mttkrp_all_modes(False, False)
-    parity = max(mk.verify_against(a, b)[0] for a, b in zip(fast, det))
-
-    bytes_mode = algorithmic_bytes(dims, t.nnz, R, distinct)
-    b_iter = float(sum(bytes_mode))
-
-    # N > 1: row-range shards per mode + NCCL all-gather of each mode's rows
     ex = None
     if world > 1:
         from paper_2503_18198_b200.distributed import ShardExchange
         ex = ShardExchange(ctx, R, dims, device=dev)
 
-    def sweep_timed(n_steps, flush, record):
-        """Per mode launches with events between them (the per-mode breakdown)."""
-        ev = [[torch.cuda.Event(enable_timing=True) for _ in range(n + 1)] for _ in range(n_steps)]
-        evk = [[torch.cuda.Event(enable_timing=True) for _ in range(n)] for _ in range(n_steps)]
-        for s in range(n_steps):
-            if flush:
-                ctx.flush_l2()
-            ev[s][0].record(stream)
-            for d in range(n):
-                ctx.mttkrp_mode_async(d, False)
-                evk[s][d].record(stream)
-                if ex is not None:
-                    ex.gather_mode(d)
-                ev[s][d + 1].record(stream)
-        return ev, evk
+    def sweep_once():
+        if ex is not None:
+            ex.sweep()
+        else:
+            ctx.sweep_async(False, False)
 
-    def sweep_fused_timed(n_steps, flush):
-        """Whole sweeps through the public sweep entry (one fused launch when applicable)."""
+    def timed_sweeps(n_steps, flush):
         ev = [[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(n_steps)]
         for s in range(n_steps):
             if flush:
@@ -282,23 +307,18 @@ def our_arm(args, cfg, rank, world, local_rank):
             ev[s][1].record(stream)
         return ev
 
-    def sweep_once():
-        if ex is not None:
-            ex.sweep()
-        else:
-            ctx.sweep_async(False, False)
-
-    for _ in range(max(args.warmup, 3)):
+    # first fast call: the one-time plan choice (mttkrp.cu choose_fast_kernel), then warm-up
+    ctx.mttkrp_all_modes(False, False)
+    for _ in range(args.warmup):
         sweep_once()
     ctx.synchronize()
     if args.profile:
-        # short, L2-flushed sweeps for ncu (never a bench number)
-        for _ in range(args.steps):
+        for _ in range(args.steps):  # short, L2-flushed sweeps for ncu (never a bench number)
             ctx.flush_l2()
             sweep_once()
         ctx.synchronize()
-        log(f"profile run done: {args.steps} sweeps of {n} modes")
-        return 0
+        log(f"profile run done: {args.steps} sweeps of {n} modes ({name})")
+        return None
 
     if world > 1:
         import torch.distributed as dist
@@ -306,32 +326,56 @@ def our_arm(args, cfg, rank, world, local_rank):
     torch.cuda.synchronize()
     with ClockSampler(local_rank) as clk:
         w0 = time.perf_counter()
-        evf = sweep_fused_timed(args.steps, True)
+        evf = timed_sweeps(args.steps, True)
         torch.cuda.synchronize()
         wall = (time.perf_counter() - w0) * 1e3
-    ctx.synchronize()  # non-finite check
-    fused_lib = ex is None and ctx.last_sweep_fused()  # the library's own record of the launch
+    ctx.synchronize()  # non-finite check of the timed sweeps
+    fused = ex is None and ctx.last_sweep_fused()
     step_ms = [evf[s][0].elapsed_time(evf[s][1]) for s in range(args.steps)]
     ms = float(np.mean(step_ms))
-    # per-mode breakdown (separate launches per mode, L2 flushed per sweep)
-    ev, evk = sweep_timed(args.steps, True, True)
-    torch.cuda.synchronize()
-    mode_ms = np.array([[ev[s][d].elapsed_time(evk[s][d]) for d in range(n)]
-                        for s in range(args.steps)])  # spMTTKRP kernels only
     if world > 1:
         import torch.distributed as dist
         tt = torch.tensor([ms], device=dev)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         ms = float(tt.item())
 
-    # warm (no flush) for reference
-    evw = sweep_fused_timed(args.steps, False)
+    # parity of the timed sweep: its outputs vs the device fp64 deterministic result
+    # (bitwise = the reference's oracle_mttkrp<double>) and vs the fp32 deterministic one
+    # (bitwise = the reference's oracle_mttkrp<float>)
+    timed_out = [ctx.output(d) for d in range(n)]
+    parity = {}
+    if ex is None:
+        det = ctx.mttkrp_all_modes(False, True)
+        ctx.upload_factors_f64([f.astype(np.float64) for f in factors])
+        det64 = ctx.mttkrp_all_modes_f64(False, True)
+        e64 = [float((np.abs(a.astype(np.float64) - b) / np.maximum(1.0, np.abs(b))).max())
+               for a, b in zip(timed_out, det64)]
+        e32 = [mk.verify_against(a, b)[0] for a, b in zip(timed_out, det)]
+        parity = {"timed_sweep_vs_fp64_max_rel_err": max(e64),
+                  "timed_sweep_vs_reference_fp32_max_rel_err": max(e32),
+                  "per_mode_vs_fp64": e64, "tolerance": 1e-4, "pass": max(e64) <= 1e-4}
+        del det, det64
+        ctx.upload_factors(factors)
+        ctx.sweep_async(False, False)  # re-establish the timed state after the parity calls
+
+    # per-mode breakdown (separate launch per mode, L2 flushed per sweep)
+    evm = [[torch.cuda.Event(enable_timing=True) for _ in range(n + 1)] for _ in range(args.steps)]
+    for s in range(args.steps):
+        ctx.flush_l2()
+        evm[s][0].record(stream)
+        for d in range(n):
+            ctx.mttkrp_mode_async(d, False)
+            evm[s][d + 1].record(stream)
+    torch.cuda.synchronize()
+    mode_ms = np.array([[evm[s][d].elapsed_time(evm[s][d + 1]) for d in range(n)]
+                        for s in range(args.steps)])
+
+    evw = timed_sweeps(args.steps, False)  # warm L2, reported alongside
     torch.cuda.synchronize()
     warm_ms = float(np.mean([evw[s][0].elapsed_time(evw[s][1]) for s in range(args.steps)]))
 
-    # e2e through the C ABI with pinned host buffers
-    # one pinned allocation per direction, matrices packed in mode order: the C ABI then moves
-    # all factors (outputs) in one copy instead of one per mode (~6 us of PCIe latency each)
+    # e2e through the C ABI: pinned host buffers packed like the device arenas (one copy per
+    # direction), and the reference-API-shaped variant with one pageable array per mode
     offs = np.cumsum([0] + [(d * R + 31) // 32 * 32 for d in dims])
     arena_f = torch.empty(int(offs[-1]), dtype=torch.float32).pin_memory()
     arena_o = torch.empty(int(offs[-1]), dtype=torch.float32).pin_memory()
@@ -341,27 +385,34 @@ def our_arm(args, cfg, rank, world, local_rank):
         p_.copy_(torch.from_numpy(f_))
     f_np = [p.numpy() for p in pin_f]
     o_np = [p.numpy() for p in pin_o]
-    def e2e_step():
+    pg_f = [f.copy() for f in factors]
+    pg_o = [np.empty_like(f) for f in factors]
+
+    def e2e_step(fs, os_):
         if ex is None:
-            ctx.sweep_host(f_np, o_np)
+            ctx.sweep_host(fs, os_)
         else:  # H2D factors, sharded sweep + all-gathers, D2H outputs
-            ctx.upload_factors(f_np)
+            ctx.upload_factors(fs)
             ex.sweep()
             for d in range(n):
-                o_np[d][...] = ctx.output(d)
+                os_[d][...] = ctx.output(d)
 
-    for _ in range(2):
-        e2e_step()
-    e2e = []
-    for s in range(args.steps):
-        ctx.flush_l2()
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record(stream)
-        e2e_step()
-        b.record(stream)
-        b.synchronize()
-        e2e.append(a.elapsed_time(b))
-    e2e_ms = float(np.mean(e2e))
+    def e2e_time(fs, os_):
+        for _ in range(2):
+            e2e_step(fs, os_)
+        out = []
+        for s in range(args.steps):
+            ctx.flush_l2()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            e2e_step(fs, os_)
+            b.record(stream)
+            b.synchronize()
+            out.append(a.elapsed_time(b))
+        return float(np.mean(out))
+
+    e2e_ms = e2e_time(f_np, o_np)
+    e2e_pageable_ms = e2e_time(pg_f, pg_o)
     h2d = int(sum(d * R * 4 for d in dims))
 
     # CPD-ALS iteration (MTTKRP + on-device Gram/solve/normalise/fit), reported alongside
@@ -380,55 +431,99 @@ def our_arm(args, cfg, rank, world, local_rank):
         als_ms = a.elapsed_time(b) / 3
 
     if rank != 0:
-        return 0
+        return None
     peak, peak_src = measured_peaks()
-    fast_info_all = [ctx.fast_path_info(d).as_dict() for d in range(n)]
-    # the timed sweep is all streaming-kernel time when fused (one launch); otherwise the
-    # per-mode kernel events
-    fused = bool(fused_lib)
+    fast = [ctx.fast_path_info(d).as_dict() for d in range(n)]
     kern_ms = ms if fused else float(mode_ms.sum(axis=1).mean())
     achieved = b_iter / (kern_ms * 1e-3) / 1e9
-    traffic = ncu_traffic(args.config)
-    fast = fast_info_all
     launches_per_sweep = 1 if fused else sum(f["launches"] for f in fast)
-    line = {
-        "metric": METRIC, "value": ms, "unit": "ms", "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False, "scaling": "strong",
-        "vs_baseline": None, "dtype": "f32",
-        "data": "synthetic (reference generator, seed 1; factors random_factors seed 1)",
-        "config": {"workload": f"{args.config}: {cfg['desc']}", "kappa": kappa,
+    rec = {
+        "value": ms, "unit": "ms", "ms_per_step": ms,
+        "config": {"workload": f"{name}: {cfg['desc']}", "kappa": kappa,
                    "policy": "adaptive", "strategy": "cyclic",
                    "schemes": [int(i.scheme) for i in infos],
                    "l2": "flushed between timed steps (memset 2x L2 on the launch stream)",
                    "parallelism": f"row-range shards x{world}" if world > 1 else "single GPU"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
-                     "algorithmic_bytes_per_sweep": b_iter,
+                     "frac": achieved / peak, "traffic": ncu_traffic(name),
+                     "peak_source": peak_src, "algorithmic_bytes_per_sweep": b_iter,
                      "kernel": sorted({f["kernel"] for f in fast}), "kernel_ms_per_sweep": kern_ms,
-                     "per_mode": fast},
+                     "lsu": lsu_roofline(name, kern_ms), "per_mode": fast},
         "e2e": {"value": e2e_ms, "unit": "ms", "h2d_bytes_per_step": h2d,
-                "d2h_bytes_per_step": h2d, "path": "mk_sweep_host (C ABI), pinned host buffers"},
+                "d2h_bytes_per_step": h2d, "path": "mk_sweep_host (C ABI), pinned host buffers",
+                "pageable_per_mode_ms": e2e_pageable_ms},
         "gpu_launches": (launches_per_sweep + (2 * n if ex is not None else 0)) * args.steps,
         "allgather_bytes_per_sweep": ex.bytes_per_sweep() if ex is not None else 0,
         "clocks": clk.summary(),
         "per_mode_ms": mode_ms.mean(axis=0).tolist(),
-        "per_mode_note": "separate launch per mode (the timed sweep is one fused launch when every "
-                         "mode runs k_stream2 with one specialisation)",
-        "fused_sweep": fused,
+        "fused_sweep": bool(fused),
         "warm_ms_per_step": warm_ms,
         "wall_ms_timed_region": wall,
         "format_build_ms": build_ms, "tensor_upload_ms": upload_ms,
         "cpd_als_ms_per_iter": als_ms,
-        "parity_fast_vs_deterministic_max_rel_err": parity,
+        "parity": parity,
     }
-    if world == 1 and not args.no_cpu:
+    ctx.close()
+    if with_cpu:
         try:
-            line["cpu_baseline"] = cpu_baseline_sample(cfg, t, factors)
+            rec["cpu_baseline"] = cpu_reference(cfg, t.coords, t.values, factors,
+                                                min(args.steps, 5), 1)
         except Exception as e:  # pragma: no cover
-            line["cpu_baseline"] = {"value": None, "unit": "ms", "cores": None, "kind": "reference",
-                                    "sample": f"failed: {e}"}
+            rec["cpu_baseline"] = {"value": None, "unit": "ms", "cores": None,
+                                   "kind": "reference", "sample": f"failed: {e}"}
+    return rec
+
+
+def our_arm(args, rank, world, local_rank):
+    import torch
+
+    torch.cuda.set_device(local_rank)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        assert dist.get_world_size() == args.gpus, (dist.get_world_size(), args.gpus)
+    dev = torch.device("cuda", local_rank)
+    # A dedicated (non-default) stream shared by torch's events and the library: the
+    # legacy default stream's handle is NULL, which the C ABI reads as "own stream".
+    stream = torch.cuda.Stream(dev)
+    torch.cuda.set_stream(stream)
+    assert stream.cuda_stream != 0
+    with_cpu = world == 1 and not args.no_cpu
+    head = run_config(args, args.config, rank, world, local_rank, stream, with_cpu)
+    if head is None:
+        return 0
+    subs = {}
+    if not args.only and world == 1:
+        for name in sorted(CONFIGS):
+            if name != args.config:
+                subs[name] = run_config(args, name, rank, world, local_rank, stream, with_cpu)
+    line = {"metric": METRIC, "value": head["value"], "unit": "ms", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": head["value"],
+            "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (reference generator restated bit-identically, seed 1; factors "
+                    "random_factors seed 1)"}
+    line.update({k: v for k, v in head.items() if k not in ("value", "unit", "ms_per_step")})
+    line["gpu_launches"] = head["gpu_launches"]
+    if subs:
+        line["configs"] = subs
     print(json.dumps(line), flush=True)
     return 0
+
+
+def spawn(args):
+    """--gpus N > 1 outside torchrun: re-launch this script as N ranks (one per GPU)."""
+    import torch
+    have = torch.cuda.device_count()
+    if args.gpus > have:
+        print(json.dumps({"error": f"--gpus {args.gpus} requested, {have} GPU(s) visible"}),
+              flush=True)
+        log(f"bench: --gpus {args.gpus} needs {args.gpus} GPUs, this box has {have}")
+        return 2
+    env = dict(os.environ, NCCL_DEBUG=os.environ.get("NCCL_DEBUG", "INFO"))
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1",
+           f"--master-port={29500 + os.getpid() % 1000}"] + sys.argv
+    return subprocess.call(cmd, env=env)
 
 
 def main():
@@ -436,20 +531,27 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--config", default="cfg2", choices=sorted(CONFIGS))
+    ap.add_argument("--config", default=HEADLINE, choices=sorted(CONFIGS))
+    ap.add_argument("--only", action="store_true",
+                    help="only the --config workload (no cfg1-cfg4 sub-records)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu", action="store_true",
-                    help="skip the cpu_baseline sample (kernel-tuning runs only)")
+                    help="skip the cpu_baseline (kernel-tuning runs only)")
     ap.add_argument("--profile", action="store_true",
                     help="only build + run --steps flushed sweeps (for ncu); prints no JSON")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
     rank, world, local_rank = dist_env()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return spawn(args)
+    if world != args.gpus and args.impl == "ours":
+        log(f"bench: WORLD_SIZE={world} but --gpus {args.gpus}")
+        return 2
     cfg = CONFIGS[args.config]
     if args.impl == "reference":
         return reference_arm(args, cfg, rank, world)
-    return our_arm(args, cfg, rank, world, local_rank)
+    return our_arm(args, rank, world, local_rank)
 
 
 if __name__ == "__main__":

@@ -89,6 +89,11 @@ int mk_synchronize(mk_context* ctx);
  * "tensor: non-finite element value"). */
 int mk_tensor_upload(mk_context* ctx, uint32_t n_modes, const uint32_t* dims, uint64_t nnz,
                      const uint32_t* coords_aos, const float* values);
+/* SparseTensorCOO<double>::from_parts (tensor.hpp:45-55, T = double).  An fp64 tensor is
+ * driven through the _f64 entry points only (the fp32 ones fail with MK_EINVAL, as the
+ * reference's templates do not mix T). */
+int mk_tensor_upload_f64(mk_context* ctx, uint32_t n_modes, const uint32_t* dims, uint64_t nnz,
+                         const uint32_t* coords_aos, const double* values);
 /* Σ val² of the uploaded tensor (||X||_F², for the CPD fit). */
 int mk_tensor_norm2(mk_context* ctx, double* norm2);
 
@@ -119,6 +124,15 @@ int mk_factors_upload(mk_context* ctx, uint32_t rank, const float* const* factor
 int mk_factor_upload(mk_context* ctx, uint32_t mode, const float* factor);
 int mk_factor_download(mk_context* ctx, uint32_t mode, float* factor);
 
+/* ---- fp64 path: the reference's T = double instantiation ---------------
+ * FactorMatrix<double> (factor.hpp:16-48); mttkrp_mode / mttkrp_all_modes<double>
+ * (kernel.hpp:161-197).  Usable on an fp64 tensor and on an fp32 tensor (values widened
+ * exactly).  MK_EXEC_DETERMINISTIC is bitwise equal to oracle_mttkrp<double>
+ * (oracle.hpp:20-43); MK_EXEC_FAST is within verify_tolerance<double> = 1e-12. */
+int mk_factors_upload_f64(mk_context* ctx, uint32_t rank, const double* const* factors);
+int mk_mttkrp_mode_f64(mk_context* ctx, uint32_t mode, int exec, double* out);
+int mk_mttkrp_all_modes_f64(mk_context* ctx, int chain, int exec, double* const* outs);
+
 /* ---- spMTTKRP -------------------------------------------------------------------
  * mttkrp_mode (kernel.hpp:161-169): one mode from the current factors into out[I_d × R]. */
 int mk_mttkrp_mode(mk_context* ctx, uint32_t mode, int exec, float* out);
@@ -140,9 +154,11 @@ int mk_sweep_host(mk_context* ctx, const float* const* factors, float* const* ou
 int mk_last_sweep_fused(mk_context* ctx, int* fused);
 /* run_timed analogue (kernel.hpp:239-287) timed with CUDA events on the context stream.
  * mode_ms[iters × N] and total_ms[iters]; flush_l2 writes a 2×L2 buffer between
- * iterations (outside the timed events). */
+ * iterations (outside the timed events).  *outputs_bit_identical (may be NULL) = whether
+ * every iteration's outputs equal the first's bit for bit (TimingReport, kernel.hpp:271-276;
+ * the fast path's float atomics need not be). */
 int mk_run_timed(mk_context* ctx, uint64_t iters, int exec, int flush_l2, double* mode_ms,
-                 double* total_ms);
+                 double* total_ms, int* outputs_bit_identical);
 /* L2 flush as used by mk_run_timed (enqueued on the context stream). */
 int mk_flush_l2(mk_context* ctx);
 
@@ -189,6 +205,12 @@ int mk_generate_powerlaw(uint32_t n_modes, const uint32_t* dims, uint64_t nnz, d
                          uint64_t seed, uint32_t* coords_aos, float* values);
 int mk_random_factors(uint32_t n_modes, const uint32_t* dims, uint64_t rank, uint64_t seed,
                       float* const* factors);
+/* T = double variants (rng.hpp:37-39 unit_open_closed<double>; same draw sequence). */
+int mk_generate_synthetic_f64(uint32_t n_modes, const uint32_t* dims, uint64_t nnz, int dist,
+                              uint64_t skew_mode, uint64_t skew_distinct, uint64_t seed,
+                              uint32_t* coords_aos, double* values);
+int mk_random_factors_f64(uint32_t n_modes, const uint32_t* dims, uint64_t rank, uint64_t seed,
+                          double* const* factors);
 
 #ifdef __cplusplus
 }

@@ -480,11 +480,13 @@ TimedRun<T> run_timed(const SparseTensorCOO<T>& t, const std::vector<ModePlan>& 
   detail::upload_factors(*plans[0].device, factors);
   const std::size_t n = plans.size();
   std::vector<double> mode_ms(iters * n), total(iters);
+  int same = 1;
   detail::check(mk_run_timed(plans[0].device->ctx, iters,
                              config.deterministic ? MK_EXEC_DETERMINISTIC : MK_EXEC_FAST, 1,
-                             mode_ms.data(), total.data()));
+                             mode_ms.data(), total.data(), &same));
   TimedRun<T> run;
   run.report.iters = iters;
+  run.report.outputs_bit_identical = same != 0;
   run.report.total_ms = total;
   for (std::size_t d = 0; d < n; ++d) {
     ModeTiming mt;

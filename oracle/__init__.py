@@ -133,6 +133,35 @@ class Oracle(_Lib):
                       rank, self._factor_concat(factors), mode, out))
         return out.reshape(int(dims[mode]), rank)
 
+    def mttkrp_f64(self, dims, coords, values, factors, mode, threads=None):
+        """oracle.hpp:20-43 with T = double (row-parallel, bitwise = the reference's fp64)."""
+        dims = _dims(dims)
+        rank = int(np.asarray(factors[0]).shape[1])
+        coords = np.ascontiguousarray(coords, dtype=np.uint32).reshape(-1)
+        nnz = coords.size // len(dims)
+        out = np.empty(int(dims[mode]) * rank, dtype=np.float64)
+        f = self.lib.orc_mttkrp_f64
+        f.argtypes = [C.c_uint32, _u32p, C.c_uint64, _u32p, _f32p, C.c_uint64, _f32p,
+                      C.c_uint32, _f64p, C.c_uint32]
+        self._check(f(len(dims), dims, nnz, coords, np.ascontiguousarray(values, np.float32),
+                      rank, self._factor_concat(factors), mode, out,
+                      int(threads or os.cpu_count() or 1)))
+        return out.reshape(int(dims[mode]), rank)
+
+    def max_rel_err_f64(self, got, want):
+        g = np.ascontiguousarray(got, dtype=np.float32).reshape(-1)
+        w = np.ascontiguousarray(want, dtype=np.float64).reshape(-1)
+        assert g.size == w.size
+        f = self.lib.orc_max_rel_err_f64
+        f.argtypes = [_f32p, _f64p, C.c_uint64]
+        f.restype = C.c_double
+        return float(f(g, w, g.size))
+
+    def build_plans_all(self, dims, coords, kappa, strategy=0, policy=0):
+        """Every mode's plan, in the array layout of Reference.run_timed_plans."""
+        return [self.build_plan(dims, coords, d, kappa, strategy, policy)
+                for d in range(len(dims))]
+
     def max_rel_err(self, got, want):
         g = np.ascontiguousarray(got, dtype=np.float32).reshape(-1)
         w = np.ascontiguousarray(want, dtype=np.float32).reshape(-1)
@@ -160,6 +189,79 @@ class Reference(_Lib):
         self._check(f(len(dims), dims, nnz, coords, np.ascontiguousarray(values, np.float32),
                       rank, self._factor_concat(factors), mode, out))
         return out.reshape(int(dims[mode]), rank)
+
+    def oracle_mttkrp_f64(self, dims, coords, values, factors, mode):
+        """oracle_mttkrp<double> (oracle.hpp:20-43) on the fp32 inputs widened to double."""
+        dims = _dims(dims)
+        rank = int(np.asarray(factors[0]).shape[1])
+        coords = np.ascontiguousarray(coords, dtype=np.uint32).reshape(-1)
+        nnz = coords.size // len(dims)
+        out = np.empty(int(dims[mode]) * rank, dtype=np.float64)
+        f = self.lib.ref_oracle_mttkrp_f64
+        f.argtypes = [C.c_uint32, _u32p, C.c_uint64, _u32p, _f32p, C.c_uint64, _f32p,
+                      C.c_uint32, _f64p]
+        self._check(f(len(dims), dims, nnz, coords, np.ascontiguousarray(values, np.float32),
+                      rank, self._factor_concat(factors), mode, out))
+        return out.reshape(int(dims[mode]), rank)
+
+    def build_plans_all(self, dims, coords, values, kappa, strategy=0, policy=0):
+        """build_mode_plans once; every mode exported (list of dicts like build_plan) plus
+        the reference's plan-build wall time (ms)."""
+        dims = _dims(dims)
+        n = len(dims)
+        coords = np.ascontiguousarray(coords, dtype=np.uint32).reshape(-1)
+        nnz = coords.size // n
+        schemes = np.zeros(n, dtype=np.int32)
+        orders = np.empty(max(n * nnz, 1), dtype=np.uint64)
+        offsets = np.empty(n * (kappa + 1), dtype=np.uint64)
+        owned = np.empty(int(sum(int(d) for d in dims)) + 1, dtype=np.uint32)
+        owned_off = np.empty(n * (kappa + 1), dtype=np.uint64)
+        plan_ms = C.c_double(0)
+        f = self.lib.ref_build_plans_all
+        f.argtypes = [C.c_uint32, _u32p, C.c_uint64, _u32p, _f32p, C.c_uint64, C.c_int, C.c_int,
+                      np.ctypeslib.ndpointer(dtype=np.int32, flags="C_CONTIGUOUS"), _u64p,
+                      _u64p, _u32p, _u64p, C.POINTER(C.c_double)]
+        self._check(f(n, dims, nnz, coords, np.ascontiguousarray(values, np.float32), kappa,
+                      strategy, policy, schemes, orders, offsets, owned, owned_off,
+                      C.byref(plan_ms)))
+        plans, base = [], 0
+        for d in range(n):
+            oo = owned_off[d * (kappa + 1):(d + 1) * (kappa + 1)]
+            plans.append({"scheme": int(schemes[d]), "order": orders[d * nnz:(d + 1) * nnz],
+                          "offsets": offsets[d * (kappa + 1):(d + 1) * (kappa + 1)],
+                          "owned": owned[base:base + int(oo[-1])], "owned_offsets": oo})
+            base += int(dims[d])
+        return plans, plan_ms.value
+
+    def run_timed_plans(self, dims, coords, values, factors, kappa, plans, iters, batch_p=32):
+        """The reference's run_timed (kernel.hpp:239-287) on given plans (list of build_plan
+        dicts).  Returns (total_ms per iteration, per-mode min ms, outputs_bit_identical)."""
+        dims = _dims(dims)
+        n = len(dims)
+        rank = int(np.asarray(factors[0]).shape[1])
+        coords = np.ascontiguousarray(coords, dtype=np.uint32).reshape(-1)
+        nnz = coords.size // n
+        schemes = np.array([p["scheme"] for p in plans], dtype=np.int32)
+        orders = np.ascontiguousarray(np.concatenate([p["order"] for p in plans]), np.uint64)
+        offsets = np.ascontiguousarray(np.concatenate([p["offsets"] for p in plans]), np.uint64)
+        owned = np.zeros(int(sum(int(d) for d in dims)) + 1, dtype=np.uint32)
+        base = 0
+        for d, p in enumerate(plans):
+            owned[base:base + len(p["owned"])] = p["owned"]
+            base += int(dims[d])
+        owned_off = np.ascontiguousarray(np.concatenate([p["owned_offsets"] for p in plans]),
+                                         np.uint64)
+        totals = np.zeros(iters, dtype=np.float64)
+        mode_min = np.zeros(n, dtype=np.float64)
+        ident = C.c_int(0)
+        f = self.lib.ref_run_timed_plans
+        f.argtypes = [C.c_uint32, _u32p, C.c_uint64, _u32p, _f32p, C.c_uint64, _f32p, C.c_uint64,
+                      np.ctypeslib.ndpointer(dtype=np.int32, flags="C_CONTIGUOUS"), _u64p, _u64p,
+                      _u32p, _u64p, C.c_uint64, C.c_uint64, _f64p, _f64p, _ip]
+        self._check(f(n, dims, nnz, coords, np.ascontiguousarray(values, np.float32), rank,
+                      self._factor_concat(factors), kappa, schemes, orders, offsets, owned,
+                      owned_off, batch_p, iters, totals, mode_min, C.byref(ident)))
+        return totals, mode_min, bool(ident.value)
 
     def mttkrp_all_modes(self, dims, coords, values, factors, kappa, strategy=0, policy=0,
                          deterministic=True, chain=False):

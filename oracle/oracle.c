@@ -7,6 +7,7 @@
 #include "oracle.h"
 
 #include <math.h>
+#include <pthread.h>
 #include <stdio.h>
 #include <stdlib.h>
 #include <string.h>
@@ -485,6 +486,96 @@ int orc_mttkrp(uint32_t n, const uint32_t* dims, uint64_t nnz, const uint32_t* c
     }
   }
   return 0;
+}
+
+/* oracle.hpp:20-43 with T = double on the fp32 inputs widened exactly to double (the
+ * reference's fp64 instantiation: SparseTensorCOO<double>, FactorMatrix<double>).  Each
+ * output row is summed in element order, so splitting the OUTPUT ROWS across threads (every
+ * thread scans all elements and keeps the ones whose row it owns) is bitwise identical to the
+ * reference's single loop. */
+typedef struct {
+  uint32_t n, mode;
+  const uint32_t* dims;
+  uint64_t nnz, rank;
+  const uint32_t* coords;
+  const float* values;
+  const float* f[16];
+  double* out;
+  uint32_t r0, r1;
+} orc_f64_job;
+
+static void* orc_f64_worker(void* arg) {
+  const orc_f64_job* j = (const orc_f64_job*)arg;
+  const uint32_t n = j->n, d = j->mode;
+  const uint64_t R = j->rank;
+  for (uint64_t i = 0; i < j->nnz; ++i) {
+    const uint32_t* c = j->coords + i * n;
+    const uint32_t row = c[d];
+    if (row < j->r0 || row >= j->r1) continue;
+    double* o = j->out + (uint64_t)row * R;
+    for (uint64_t r = 0; r < R; ++r) {
+      double term = (double)j->values[i];
+      for (uint32_t w = 0; w < n; ++w)
+        if (w != d) term *= (double)j->f[w][(uint64_t)c[w] * R + r];
+      o[r] += term;
+    }
+  }
+  return NULL;
+}
+
+int orc_mttkrp_f64(uint32_t n, const uint32_t* dims, uint64_t nnz, const uint32_t* coords,
+                   const float* values, uint64_t rank, const float* factors, uint32_t mode,
+                   double* out, uint32_t threads) {
+  if (mode >= n) FAIL("oracle: mode out of range");
+  if (n > 16) FAIL("oracle: too many modes");
+  if (threads < 1) threads = 1;
+  if (threads > 256) threads = 256;
+  if (threads > dims[mode]) threads = dims[mode];
+  orc_f64_job jobs[256];
+  pthread_t tids[256];
+  uint64_t off = 0;
+  const float* f[16];
+  for (uint32_t w = 0; w < n; ++w) {
+    f[w] = factors + off;
+    off += (uint64_t)dims[w] * rank;
+  }
+  memset(out, 0, (uint64_t)dims[mode] * rank * sizeof(double));
+  for (uint32_t t = 0; t < threads; ++t) {
+    orc_f64_job* j = &jobs[t];
+    j->n = n;
+    j->mode = mode;
+    j->dims = dims;
+    j->nnz = nnz;
+    j->rank = rank;
+    j->coords = coords;
+    j->values = values;
+    memcpy(j->f, f, sizeof f);
+    j->out = out;
+    j->r0 = (uint32_t)((uint64_t)dims[mode] * t / threads);
+    j->r1 = (uint32_t)((uint64_t)dims[mode] * (t + 1) / threads);
+  }
+  uint32_t started = 0;
+  for (uint32_t t = 1; t < threads; ++t) {
+    if (pthread_create(&tids[t], NULL, orc_f64_worker, &jobs[t]) != 0) break;
+    started = t;
+  }
+  orc_f64_worker(&jobs[0]);
+  for (uint32_t t = 1; t <= started; ++t) pthread_join(tids[t], NULL);
+  for (uint32_t t = started + 1; t < threads; ++t) orc_f64_worker(&jobs[t]);
+  return 0;
+}
+
+/* verify.hpp:21-39 against an fp64 want: max |g-w| / max(1,|w|). */
+double orc_max_rel_err_f64(const float* got, const double* want, uint64_t count) {
+  double worst = 0.0;
+  for (uint64_t i = 0; i < count; ++i) {
+    double g = got[i], w = want[i];
+    double den = fabs(w) > 1.0 ? fabs(w) : 1.0;
+    double e = fabs(g - w) / den;
+    if (e != e) return INFINITY;
+    if (e > worst) worst = e;
+  }
+  return worst;
 }
 
 /* verify.hpp:21-39 */

@@ -53,6 +53,13 @@ int orc_mttkrp(uint32_t n, const uint32_t* dims, uint64_t nnz, const uint32_t* c
                const float* values, uint64_t rank, const float* factors_concat, uint32_t mode,
                float* out);
 
+/* oracle.hpp:20-43 with T = double (fp32 inputs widened exactly); output rows split across
+ * `threads` threads, each row still summed in element order (bitwise = the reference). */
+int orc_mttkrp_f64(uint32_t n, const uint32_t* dims, uint64_t nnz, const uint32_t* coords,
+                   const float* values, uint64_t rank, const float* factors_concat,
+                   uint32_t mode, double* out, uint32_t threads);
+double orc_max_rel_err_f64(const float* got, const double* want, uint64_t count);
+
 /* verify.hpp:21-39: max |g-w| / max(1,|w|). */
 double orc_max_rel_err(const float* got, const float* want, uint64_t count);
 

@@ -9,6 +9,7 @@
 //
 // Built by oracle/Makefile directly from the reference sources where they lie under
 // /root/reference (no source is copied) into oracle/_ref/libmttkrp_ref.so.
+#include <chrono>
 #include <cstdint>
 #include <cstring>
 #include <exception>
@@ -39,25 +40,53 @@ int guarded(F&& f) {
   }
 }
 
-SparseTensorCOO<float> make_tensor(uint32_t n, const uint32_t* dims, uint64_t nnz,
-                                   const uint32_t* coords, const float* values) {
+template <typename T = float>
+SparseTensorCOO<T> make_tensor(uint32_t n, const uint32_t* dims, uint64_t nnz,
+                               const uint32_t* coords, const float* values) {
   std::vector<index_t> d(dims, dims + n);
   std::vector<index_t> c(coords, coords + nnz * n);
-  std::vector<float> v(values, values + nnz);
-  return SparseTensorCOO<float>::from_parts(Shape(d), std::move(c), std::move(v));
+  std::vector<T> v(values, values + nnz);  // float -> T widening is exact
+  return SparseTensorCOO<T>::from_parts(Shape(d), std::move(c), std::move(v));
 }
 
-std::vector<FactorMatrix<float>> make_factors(uint32_t n, const uint32_t* dims, uint64_t rank,
-                                              const float* concat) {
-  std::vector<FactorMatrix<float>> f;
+template <typename T = float>
+std::vector<FactorMatrix<T>> make_factors(uint32_t n, const uint32_t* dims, uint64_t rank,
+                                          const float* concat) {
+  std::vector<FactorMatrix<T>> f;
   std::size_t off = 0;
   for (uint32_t d = 0; d < n; ++d) {
-    auto m = FactorMatrix<float>::zeros(d, dims[d], rank);
-    std::memcpy(m.data.data(), concat + off, m.data.size() * sizeof(float));
+    auto m = FactorMatrix<T>::zeros(d, dims[d], rank);
+    for (std::size_t i = 0; i < m.data.size(); ++i) m.data[i] = concat[off + i];
     off += m.data.size();
     f.push_back(std::move(m));
   }
   return f;
+}
+
+// ModePlan objects from exported arrays (the layout of ref_build_plans_all).
+std::vector<ModePlan> plans_from_arrays(uint32_t n, const uint32_t* dims, uint64_t nnz,
+                                        uint64_t kappa, const int* schemes,
+                                        const uint64_t* orders, const uint64_t* offsets,
+                                        const uint32_t* owned_flat,
+                                        const uint64_t* owned_offsets) {
+  std::vector<ModePlan> plans(n);
+  uint64_t owned_base = 0;
+  for (uint32_t d = 0; d < n; ++d) {
+    ModePlan& p = plans[d];
+    p.mode = d;
+    p.scheme = schemes[d] == 1 ? Scheme::scheme1 : Scheme::scheme2;
+    p.kappa = kappa;
+    p.order.assign(orders + d * nnz, orders + (d + 1) * nnz);
+    p.partition_offsets.assign(offsets + d * (kappa + 1), offsets + (d + 1) * (kappa + 1));
+    if (p.scheme == Scheme::scheme1) {
+      p.owned_indices.resize(kappa);
+      const uint64_t* oo = owned_offsets + d * (kappa + 1);
+      for (uint64_t z = 0; z < kappa; ++z)
+        p.owned_indices[z].assign(owned_flat + owned_base + oo[z], owned_flat + owned_base + oo[z + 1]);
+    }
+    owned_base += dims[d];
+  }
+  return plans;
 }
 
 Strategy strat(int s) { return s == 0 ? Strategy::cyclic : Strategy::least_loaded; }
@@ -136,6 +165,74 @@ int ref_oracle_mttkrp(uint32_t n, const uint32_t* dims, uint64_t nnz, const uint
     auto f = make_factors(n, dims, rank, factors);
     auto o = oracle_mttkrp(t, f, mode);
     std::memcpy(out, o.data.data(), o.data.size() * sizeof(float));
+  });
+}
+
+// oracle_mttkrp<double> (oracle.hpp:20-43, the reference's own fp64 instantiation) on the
+// fp32 inputs widened exactly to double: the fp64 truth the fast path is gated against.
+int ref_oracle_mttkrp_f64(uint32_t n, const uint32_t* dims, uint64_t nnz, const uint32_t* coords,
+                          const float* values, uint64_t rank, const float* factors, uint32_t mode,
+                          double* out) {
+  return guarded([&] {
+    auto t = make_tensor<double>(n, dims, nnz, coords, values);
+    auto f = make_factors<double>(n, dims, rank, factors);
+    auto o = oracle_mttkrp(t, f, mode);
+    std::memcpy(out, o.data.data(), o.data.size() * sizeof(double));
+  });
+}
+
+// build_mode_plans once, every mode exported: orders[n * nnz], offsets[n * (kappa+1)],
+// owned_flat[sum dims] (mode d's owned indices start at sum_{w<d} dims[w]),
+// owned_offsets[n * (kappa+1)] (relative to the mode's base), schemes[n].
+int ref_build_plans_all(uint32_t n, const uint32_t* dims, uint64_t nnz, const uint32_t* coords,
+                        const float* values, uint64_t kappa, int strategy, int policy,
+                        int* schemes, uint64_t* orders, uint64_t* offsets, uint32_t* owned_flat,
+                        uint64_t* owned_offsets, double* plan_ms) {
+  return guarded([&] {
+    auto t = make_tensor(n, dims, nnz, coords, values);
+    auto t0 = std::chrono::steady_clock::now();
+    auto plans = build_mode_plans(t, kappa, strat(strategy), pol(policy));
+    *plan_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    uint64_t owned_base = 0;
+    for (uint32_t d = 0; d < n; ++d) {
+      const ModePlan& p = plans[d];
+      schemes[d] = p.scheme == Scheme::scheme1 ? 1 : 2;
+      std::memcpy(orders + d * nnz, p.order.data(), nnz * sizeof(uint64_t));
+      std::memcpy(offsets + d * (kappa + 1), p.partition_offsets.data(), (kappa + 1) * sizeof(uint64_t));
+      uint64_t* oo = owned_offsets + d * (kappa + 1);
+      uint64_t pos = 0;
+      oo[0] = 0;
+      for (uint64_t z = 0; z < kappa; ++z) {
+        if (p.scheme == Scheme::scheme1)
+          for (index_t v : p.owned_indices[z]) owned_flat[owned_base + pos++] = v;
+        oo[z + 1] = pos;
+      }
+      owned_base += dims[d];
+    }
+  });
+}
+
+// run_timed (kernel.hpp:239-287) on plans given as arrays (bit-identical plans built by the
+// oracle's fast planner, pinned against the reference's build_mode_plans in tests): the
+// reference's timed executor without its ~90 s single-threaded plan sort at 77M nnz.
+int ref_run_timed_plans(uint32_t n, const uint32_t* dims, uint64_t nnz, const uint32_t* coords,
+                        const float* values, uint64_t rank, const float* factors, uint64_t kappa,
+                        const int* schemes, const uint64_t* orders, const uint64_t* offsets,
+                        const uint32_t* owned_flat, const uint64_t* owned_offsets,
+                        uint64_t batch_p, uint64_t iters, double* total_ms_per_iter,
+                        double* mode_min_ms, int* bit_identical) {
+  return guarded([&] {
+    auto t = make_tensor(n, dims, nnz, coords, values);
+    auto f = make_factors(n, dims, rank, factors);
+    auto plans = plans_from_arrays(n, dims, nnz, kappa, schemes, orders, offsets, owned_flat,
+                                   owned_offsets);
+    ExecConfig cfg{kappa, batch_p, false};
+    auto run = run_timed(t, plans, f, cfg, iters);
+    for (std::size_t i = 0; i < run.report.total_ms.size(); ++i)
+      total_ms_per_iter[i] = run.report.total_ms[i];
+    for (std::size_t d = 0; d < run.report.modes.size(); ++d)
+      mode_min_ms[d] = run.report.modes[d].min_ms;
+    *bit_identical = run.report.outputs_bit_identical ? 1 : 0;
   });
 }
 

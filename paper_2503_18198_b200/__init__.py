@@ -59,6 +59,8 @@ EXPORTED_SYMBOLS = [
     "mk_generate_synthetic", "mk_generate_powerlaw", "mk_random_factors",
     "mk_set_shard", "mk_shard_rows", "mk_shard_pack", "mk_shard_unpack", "mk_shard_cuts",
     "mk_als_update_mode", "mk_als_fit", "mk_output_device_ptr",
+    "mk_tensor_upload_f64", "mk_factors_upload_f64", "mk_mttkrp_mode_f64",
+    "mk_mttkrp_all_modes_f64", "mk_random_factors_f64", "mk_generate_synthetic_f64",
 ]
 
 
@@ -156,7 +158,7 @@ def load_library() -> C.CDLL:
             "mk_mttkrp_mode_async": (i32, [vp, u32, i32]),
             "mk_output_download": (i32, [vp, u32, vp]),
             "mk_sweep_host": (i32, [vp, vp, vp, i32, i32]),
-            "mk_run_timed": (i32, [vp, u64, i32, i32, vp, vp]),
+            "mk_run_timed": (i32, [vp, u64, i32, i32, vp, vp, P(i32)]),
             "mk_flush_l2": (i32, [vp]),
             "mk_last_sweep_fused": (i32, [vp, P(C.c_int)]),
             "mk_cpd_als_iter": (i32, [vp, P(C.c_double), vp]),
@@ -172,6 +174,12 @@ def load_library() -> C.CDLL:
             "mk_als_update_mode": (i32, [vp, u32]),
             "mk_als_fit": (i32, [vp, P(C.c_double), vp]),
             "mk_output_device_ptr": (i32, [vp, u32, P(vp)]),
+            "mk_tensor_upload_f64": (i32, [vp, u32, vp, u64, vp, vp]),
+            "mk_factors_upload_f64": (i32, [vp, u32, vp]),
+            "mk_mttkrp_mode_f64": (i32, [vp, u32, i32, vp]),
+            "mk_mttkrp_all_modes_f64": (i32, [vp, i32, i32, vp]),
+            "mk_random_factors_f64": (i32, [u32, vp, u64, u64, vp]),
+            "mk_generate_synthetic_f64": (i32, [u32, vp, u64, i32, u64, u64, u64, vp, vp]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(lib, name)
@@ -216,7 +224,9 @@ class SparseTensorCOO:
                                       if not (isinstance(coords, np.ndarray)
                                               and coords.dtype == np.uint32)
                                       else coords.reshape(-1, n))
-        values = np.ascontiguousarray(np.asarray(values, dtype=np.float32).reshape(-1))
+        vdt = np.float64 if (isinstance(values, np.ndarray) and values.dtype == np.float64) \
+            else np.float32  # SparseTensorCOO<double> when given fp64 values
+        values = np.ascontiguousarray(np.asarray(values, dtype=vdt).reshape(-1))
         if coords.shape[0] != values.shape[0]:
             raise MttkrpError("tensor: coordinate/value storage size mismatch")
         if validate:
@@ -264,7 +274,9 @@ class FactorMatrix:
     data: np.ndarray  # float32 (rows, rank)
 
     def __post_init__(self):
-        self.data = np.ascontiguousarray(np.asarray(self.data, dtype=np.float32))
+        dt = np.float64 if (isinstance(self.data, np.ndarray) and self.data.dtype == np.float64) \
+            else np.float32  # FactorMatrix<double> stays fp64
+        self.data = np.ascontiguousarray(np.asarray(self.data, dtype=dt))
         if self.data.ndim != 2:
             raise MttkrpError("factor: matrix must be 2-D")
 
@@ -338,8 +350,11 @@ class Context:
     # tensor / plans
     def upload_tensor(self, t: SparseTensorCOO):
         dims = np.asarray(t.dims, dtype=np.uint32)
-        _check(self.lib.mk_tensor_upload(self.h, len(t.dims), _ptr(dims), t.nnz, _ptr(t.coords),
-                                         _ptr(t.values)))
+        up = self.lib.mk_tensor_upload_f64 if t.values.dtype == np.float64 else \
+            self.lib.mk_tensor_upload
+        _check(up(self.h, len(t.dims), _ptr(dims), t.nnz, _ptr(t.coords), _ptr(t.values)))
+        self.f64 = t.values.dtype == np.float64
+        self.rank64 = 0
         self.dims = list(t.dims)
         self.nnz = t.nnz
         self.rank = 0
@@ -400,6 +415,24 @@ class Context:
         _check(self.lib.mk_factors_upload(self.h, rank, _ptr_array(mats)))
         self.rank = rank
 
+    def upload_factors_f64(self, factors: Sequence[np.ndarray]):
+        """FactorMatrix<double> inputs of the fp64 path."""
+        mats = [np.ascontiguousarray(np.asarray(f, dtype=np.float64)) for f in factors]
+        rank = int(mats[0].shape[1])
+        _check(self.lib.mk_factors_upload_f64(self.h, rank, _ptr_array(mats)))
+        self.rank64 = rank
+
+    def mttkrp_mode_f64(self, mode: int, deterministic: bool = False) -> np.ndarray:
+        out = np.empty((self.dims[mode], self.rank64), dtype=np.float64)
+        _check(self.lib.mk_mttkrp_mode_f64(self.h, mode, int(deterministic), _ptr(out)))
+        return out
+
+    def mttkrp_all_modes_f64(self, chain: bool = False, deterministic: bool = False):
+        outs = [np.empty((d, self.rank64), dtype=np.float64) for d in self.dims]
+        _check(self.lib.mk_mttkrp_all_modes_f64(self.h, int(chain), int(deterministic),
+                                                _ptr_array(outs)))
+        return outs
+
     def download_factor(self, mode: int) -> np.ndarray:
         out = np.empty((self.dims[mode], self.rank), dtype=np.float32)
         _check(self.lib.mk_factor_download(self.h, mode, _ptr(out)))
@@ -437,8 +470,10 @@ class Context:
         n = len(self.dims)
         mode_ms = np.zeros((iters, n), dtype=np.float64)
         total = np.zeros(iters, dtype=np.float64)
+        same = C.c_int(0)
         _check(self.lib.mk_run_timed(self.h, iters, int(deterministic), int(flush_l2),
-                                     _ptr(mode_ms), _ptr(total)))
+                                     _ptr(mode_ms), _ptr(total), C.byref(same)))
+        self.last_outputs_bit_identical = bool(same.value)
         return mode_ms, total
 
     def flush_l2(self):
@@ -599,6 +634,16 @@ def _as_factors(factors) -> List[FactorMatrix]:
     return [f if isinstance(f, FactorMatrix) else FactorMatrix(i, f) for i, f in enumerate(factors)]
 
 
+def _is_f64(t: SparseTensorCOO, factors: Sequence[FactorMatrix]) -> bool:
+    """T = double: an fp64 tensor takes fp64 factors (the reference's templates do not mix T)."""
+    f64 = [f.data.dtype == np.float64 for f in factors]
+    if t.values.dtype == np.float64 and not all(f64):
+        raise MttkrpError("kernel: an fp64 tensor needs fp64 factor matrices")
+    if t.values.dtype != np.float64 and any(f64):
+        raise MttkrpError("kernel: fp64 factor matrices need an fp64 tensor")
+    return t.values.dtype == np.float64
+
+
 def _upload_if_changed(ctx: Context, factors: Sequence[FactorMatrix]):
     ctx.upload_factors([f.data for f in factors])
 
@@ -610,6 +655,9 @@ def mttkrp_mode(t: SparseTensorCOO, plan: ModePlan, factors, config: ExecConfig)
     _validate_factors(t, factors)
     _validate_plan(t, plan, config)
     ctx = plan._ctx
+    if _is_f64(t, factors):
+        ctx.upload_factors_f64([f.data for f in factors])
+        return FactorMatrix(plan.mode, ctx.mttkrp_mode_f64(plan.mode, config.deterministic))
     _upload_if_changed(ctx, factors)
     return FactorMatrix(plan.mode, ctx.mttkrp_mode(plan.mode, config.deterministic))
 
@@ -628,6 +676,10 @@ def mttkrp_all_modes(t: SparseTensorCOO, plans: Sequence[ModePlan], factors, con
     for p in plans:
         _validate_plan(t, p, config)
     ctx = plans[0]._ctx
+    if _is_f64(t, factors):
+        ctx.upload_factors_f64([f.data for f in factors])
+        outs = ctx.mttkrp_all_modes_f64(chain_outputs, config.deterministic)
+        return [FactorMatrix(d, o) for d, o in enumerate(outs)]
     _upload_if_changed(ctx, factors)
     outs = ctx.mttkrp_all_modes(chain_outputs, config.deterministic)
     return [FactorMatrix(d, o) for d, o in enumerate(outs)]
@@ -675,7 +727,7 @@ def run_timed(t: SparseTensorCOO, plans: Sequence[ModePlan], factors, config: Ex
         modes.append(ModeTiming(d, p.scheme, w, min(w), float(np.median(w)),
                                 sum(1 for s in sizes if s > 0), sizes))
     report = TimingReport(iters, modes, [float(x) for x in total], float(total.min()),
-                          float(np.median(total)))
+                          float(np.median(total)), ctx.last_outputs_bit_identical)
     outs = [FactorMatrix(d, ctx.output(d)) for d in range(t.mode_count())]
     return report, outs
 
@@ -694,15 +746,18 @@ def cpd_als(t: SparseTensorCOO, plans: Sequence[ModePlan], factors, max_iters: i
 
 # ----------------------------------------------------------------------------- ingest (host)
 def generate_synthetic(dims, nnz, dist="uniform", skew_mode=0, skew_distinct=2,
-                       seed=0) -> SparseTensorCOO:
-    """synthetic.hpp:58-158, bit-identical (host C++ in libmttkrp_b200.so)."""
+                       seed=0, dtype=np.float32) -> SparseTensorCOO:
+    """synthetic.hpp:58-158, bit-identical (host C++ in libmttkrp_b200.so); dtype=np.float64
+    gives generate_synthetic<double>."""
     lib = load_library()
     d = np.asarray(dims, dtype=np.uint32)
     coords = np.empty((nnz, len(dims)), dtype=np.uint32)
-    vals = np.empty(nnz, dtype=np.float32)
+    f64 = np.dtype(dtype) == np.float64
+    vals = np.empty(nnz, dtype=np.float64 if f64 else np.float32)
     dist_i = {"uniform": 0, "mode_skewed": 1}[dist] if isinstance(dist, str) else int(dist)
-    _check(lib.mk_generate_synthetic(len(dims), _ptr(d), nnz, dist_i, skew_mode, skew_distinct,
-                                     seed, _ptr(coords), _ptr(vals)))
+    gen = lib.mk_generate_synthetic_f64 if f64 else lib.mk_generate_synthetic
+    _check(gen(len(dims), _ptr(d), nnz, dist_i, skew_mode, skew_distinct, seed, _ptr(coords),
+               _ptr(vals)))
     return SparseTensorCOO(dims, coords, vals, validate=False)
 
 
@@ -717,14 +772,16 @@ def generate_powerlaw(dims, nnz, exponent=1.0, seed=0) -> SparseTensorCOO:
     return SparseTensorCOO(dims, coords, vals, validate=False)
 
 
-def random_factors(dims, rank, seed) -> List[FactorMatrix]:
-    """factor.hpp:71-84, bit-identical."""
+def random_factors(dims, rank, seed, dtype=np.float32) -> List[FactorMatrix]:
+    """factor.hpp:71-84, bit-identical (T = float, or T = double with dtype=np.float64)."""
     lib = load_library()
     if rank < 1:
         raise MttkrpError("factor: rank must be at least 1")
     d = np.asarray(dims, dtype=np.uint32)
-    mats = [np.empty((int(x), rank), dtype=np.float32) for x in dims]
-    _check(lib.mk_random_factors(len(dims), _ptr(d), rank, seed, _ptr_array(mats)))
+    f64 = np.dtype(dtype) == np.float64
+    mats = [np.empty((int(x), rank), dtype=np.float64 if f64 else np.float32) for x in dims]
+    gen = lib.mk_random_factors_f64 if f64 else lib.mk_random_factors
+    _check(gen(len(dims), _ptr(d), rank, seed, _ptr_array(mats)))
     return [FactorMatrix(i, m) for i, m in enumerate(mats)]
 
 

@@ -48,6 +48,9 @@ void need_mode(Context& c, uint32_t mode) {
   if (mode >= c.n) fail(MK_EINVAL, "kernel: plan mode out of range");
 }
 void need_factors(Context& c) {
+  if (c.tensor_f64)
+    fail(MK_EINVAL, "kernel: the tensor holds fp64 values (SparseTensorCOO<double>); use the _f64 "
+                    "entry points");
   if (c.rank == 0) fail(MK_ESTATE, "kernel: factors not uploaded");
   for (uint32_t w = 0; w < c.n; ++w)
     if (!c.factors_set[w]) fail(MK_ESTATE, "kernel: expected one factor matrix per mode");
@@ -184,6 +187,34 @@ int mk_tensor_upload(mk_context* ctx, uint32_t n, const uint32_t* dims, uint64_t
     need_ctx(ctx);
     if (!dims) fail(MK_EINVAL, "shape: null dims");
     tensor_upload(ctx->c, n, dims, nnz, coords, values);
+  });
+}
+
+int mk_tensor_upload_f64(mk_context* ctx, uint32_t n, const uint32_t* dims, uint64_t nnz,
+                         const uint32_t* coords, const double* values) {
+  return guarded([&] {
+    need_ctx(ctx);
+    if (!dims) fail(MK_EINVAL, "shape: null dims");
+    if (nnz && !values) fail(MK_EINVAL, "tensor: null coordinate/value storage");
+    // validation runs on fp32 stand-ins that are non-finite exactly where the doubles are
+    // (tensor.hpp:97-106 order: the first bad element, coordinates before value)
+    std::vector<float> vf(nnz);
+    double norm2 = 0.0;
+    for (uint64_t i = 0; i < nnz; ++i) {
+      const double v = values[i];
+      vf[i] = std::isfinite(v) ? static_cast<float>(std::max(-3.0e38, std::min(3.0e38, v))) : NAN;
+      norm2 += v * v;
+    }
+    Context& c = ctx->c;
+    tensor_upload(c, n, dims, nnz, coords, vf.data());
+    if (nnz) {
+      c.values64.resize(nnz);
+      MKB_CUDA(cudaMemcpyAsync(c.values64.get(), values, nnz * sizeof(double),
+                               cudaMemcpyHostToDevice, c.stream));
+      MKB_CUDA(cudaStreamSynchronize(c.stream));
+    }
+    c.tensor_f64 = true;
+    c.norm2 = norm2;
   });
 }
 
@@ -360,6 +391,84 @@ int mk_factors_upload(mk_context* ctx, uint32_t rank, const float* const* factor
   });
 }
 
+int mk_factors_upload_f64(mk_context* ctx, uint32_t rank, const double* const* factors) {
+  return guarded([&] {
+    need_ctx(ctx);
+    Context& c = ctx->c;
+    if (c.n == 0) fail(MK_ESTATE, "kernel: no tensor uploaded");
+    if (rank < 1) fail(MK_EINVAL, "kernel: rank must be at least 1");
+    if (!factors) fail(MK_EINVAL, "kernel: expected one factor matrix per mode");
+    for (uint32_t w = 0; w < c.n; ++w)
+      if (!factors[w]) fail(MK_EINVAL, "kernel: expected one factor matrix per mode");
+    MKB_CUDA(cudaStreamSynchronize(c.stream));
+    size_t off[kMaxModes + 1] = {0};
+    for (uint32_t w = 0; w < c.n; ++w)
+      off[w + 1] = off[w] + ((static_cast<size_t>(c.dims[w]) * rank + 15) & ~size_t(15));
+    c.factor64_arena.resize(off[c.n]);
+    c.output64_arena.resize(off[c.n]);
+    c.rank64 = rank;
+    for (uint32_t w = 0; w < c.n; ++w) {
+      c.factors64[w] = c.factor64_arena.get() + off[w];
+      c.outputs64[w] = c.output64_arena.get() + off[w];
+      MKB_CUDA(cudaMemcpyAsync(c.factors64[w], factors[w],
+                               static_cast<size_t>(c.dims[w]) * rank * sizeof(double),
+                               cudaMemcpyHostToDevice, c.stream));
+    }
+    MKB_CUDA(cudaStreamSynchronize(c.stream));
+  });
+}
+
+static void need_f64(Context& c) {
+  if (c.rank64 == 0) fail(MK_ESTATE, "kernel: fp64 factors not uploaded (mk_factors_upload_f64)");
+}
+
+static void all_modes64(Context& c, int chain, int exec) {
+  const double* in[kMaxModes];
+  for (uint32_t w = 0; w < c.n; ++w) in[w] = c.factors64[w];
+  for (uint32_t d = 0; d < c.n; ++d) {
+    reset_nonfinite(c);
+    launch_mttkrp64(c, d, in, c.outputs64[d], exec);
+    check_nonfinite(c);
+    if (chain) in[d] = c.outputs64[d];
+  }
+}
+
+int mk_mttkrp_mode_f64(mk_context* ctx, uint32_t mode, int exec, double* out) {
+  return guarded([&] {
+    need_ctx(ctx);
+    Context& c = ctx->c;
+    need_plans(c);
+    need_mode(c, mode);
+    need_f64(c);
+    const double* in[kMaxModes];
+    for (uint32_t w = 0; w < c.n; ++w) in[w] = c.factors64[w];
+    reset_nonfinite(c);
+    launch_mttkrp64(c, mode, in, c.outputs64[mode], exec);
+    check_nonfinite(c);
+    if (out)
+      MKB_CUDA(cudaMemcpyAsync(out, c.outputs64[mode],
+                               static_cast<size_t>(c.dims[mode]) * c.rank64 * sizeof(double),
+                               cudaMemcpyDeviceToHost, c.stream));
+    MKB_CUDA(cudaStreamSynchronize(c.stream));
+  });
+}
+
+int mk_mttkrp_all_modes_f64(mk_context* ctx, int chain, int exec, double* const* outs) {
+  return guarded([&] {
+    need_ctx(ctx);
+    Context& c = ctx->c;
+    need_plans(c);
+    need_f64(c);
+    all_modes64(c, chain, exec);
+    for (uint32_t d = 0; d < c.n && outs; ++d)
+      if (outs[d])
+        MKB_CUDA(cudaMemcpyAsync(outs[d], c.outputs64[d],
+                                 static_cast<size_t>(c.dims[d]) * c.rank64 * sizeof(double),
+                                 cudaMemcpyDeviceToHost, c.stream));
+    MKB_CUDA(cudaStreamSynchronize(c.stream));
+  });
+}
+
 int mk_factor_upload(mk_context* ctx, uint32_t mode, const float* factor) {
   return guarded([&] {
     need_ctx(ctx);
@@ -510,8 +619,19 @@ int mk_flush_l2(mk_context* ctx) {
   });
 }
 
+// Word-wise comparison of two output arenas (run_timed's outputs_bit_identical,
+// kernel.hpp:271-276); any difference clears *same.
+__global__ void k_words_equal(const uint32_t* __restrict__ a, const uint32_t* __restrict__ b,
+                              size_t n, int* same) {
+  bool diff = false;
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x)
+    diff |= a[i] != b[i];
+  if (__syncthreads_or(diff) && threadIdx.x == 0) *same = 0;
+}
+
 int mk_run_timed(mk_context* ctx, uint64_t iters, int exec, int flush_l2, double* mode_ms,
-                 double* total_ms) {
+                 double* total_ms, int* outputs_bit_identical) {
   return guarded([&] {
     need_ctx(ctx);
     Context& c = ctx->c;
@@ -524,6 +644,14 @@ int mk_run_timed(mk_context* ctx, uint64_t iters, int exec, int flush_l2, double
     reset_nonfinite(c);
     const float* in[kMaxModes];
     for (uint32_t w = 0; w < n; ++w) in[w] = c.factors[w].get();
+    // iteration 0's outputs are kept; every later iteration is compared word by word
+    // (outside the timed events), as the reference does with bitwise_equal
+    const size_t words = c.arena_off[n];
+    DevBuf<float> first;
+    DevBuf<int> same(1);
+    const int one = 1;
+    MKB_CUDA(cudaMemcpyAsync(same.get(), &one, sizeof one, cudaMemcpyHostToDevice, c.stream));
+    if (iters > 1) first.resize(words);
     for (uint64_t it = 0; it < iters; ++it) {
       if (flush_l2) {
         const size_t bytes = std::max<size_t>(2 * c.l2_bytes, 64u << 20);
@@ -536,8 +664,23 @@ int mk_run_timed(mk_context* ctx, uint64_t iters, int exec, int flush_l2, double
         launch_mttkrp(c, d, in, c.outputs[d].get(), exec);
         MKB_CUDA(cudaEventRecord(ev[it * (n + 1) + d + 1], c.stream));
       }
+      if (iters > 1 && it == 0) {
+        MKB_CUDA(cudaMemcpyAsync(first.get(), c.output_arena.get(), words * sizeof(float),
+                                 cudaMemcpyDeviceToDevice, c.stream));
+      } else if (it > 0) {
+        const unsigned blocks = static_cast<unsigned>(
+            std::max<uint64_t>(1, std::min<uint64_t>(ceil_div(words, 256), c.num_sms * 8ull)));
+        k_words_equal<<<blocks, 256, 0, c.stream>>>(
+            reinterpret_cast<const uint32_t*>(first.get()),
+            reinterpret_cast<const uint32_t*>(c.output_arena.get()), words, same.get());
+        MKB_LAUNCH();
+      }
     }
+    int same_h = 1;
+    MKB_CUDA(cudaMemcpyAsync(&same_h, same.get(), sizeof same_h, cudaMemcpyDeviceToHost,
+                             c.stream));
     MKB_CUDA(cudaStreamSynchronize(c.stream));
+    if (outputs_bit_identical) *outputs_bit_identical = same_h;
     for (uint64_t it = 0; it < iters; ++it) {
       float tot = 0.f;
       for (uint32_t d = 0; d < n; ++d) {

@@ -513,9 +513,13 @@ void als_prepare(Context& c) {
   c.lambda.resize(R);
   c.als_scalars.resize(2);
   c.als_status.resize(1);
-  if (c.mtm.size() < 2 * static_cast<size_t>(R) * R) {  // two MᵀM accumulators (ping-pong)
+  // two MᵀM accumulators (ping-pong, each left zeroed by the update that consumed it); a new
+  // rank re-lays them out, so both are re-zeroed and the ping-pong restarts at slot 0
+  if (c.mtm.size() < 2 * static_cast<size_t>(R) * R || c.mtm_rank != R) {
     c.mtm.resize(2 * static_cast<size_t>(R) * R);
     MKB_CUDA(cudaMemsetAsync(c.mtm.get(), 0, 2 * sizeof(double) * R * R, c.stream));
+    c.mtm_rank = R;
+    c.als_epoch = 0;
   }
   if (!c.als_bar.get()) {
     c.als_bar.resize(1);

@@ -31,6 +31,7 @@ struct ModeCopy {
   uint64_t distinct = 0;  // V: rows with degree > 0
   DevBuf<uint32_t> idx[kMaxModes];
   DevBuf<float> val;
+  DevBuf<double> val64;  // fp64 path (mttkrp64.cu): values in copy order, built on first use
   DevBuf<uint32_t> order;
   DevBuf<uint32_t> row_seq;  // rows in copy order: [0,V) non-empty, [V,extent) empty
   DevBuf<uint32_t> row_ptr;  // V+1
@@ -114,6 +115,8 @@ struct Context {
   uint64_t nnz = 0;
   DevBuf<uint32_t> cols[kMaxModes];  // original element order, SoA
   DevBuf<float> values;
+  DevBuf<double> values64;  // mk_tensor_upload_f64: the fp64 values (original order)
+  bool tensor_f64 = false;  // the tensor was uploaded as SparseTensorCOO<double>
   double norm2 = 0.0;
 
   // plans
@@ -132,6 +135,11 @@ struct Context {
   DevBuf<float> factors[kMaxModes];
   DevBuf<float> outputs[kMaxModes];
   bool factors_set[kMaxModes] = {};
+  // fp64 path: FactorMatrix<double> inputs / outputs
+  uint32_t rank64 = 0;
+  DevBuf<double> factor64_arena, output64_arena;
+  double* factors64[kMaxModes] = {};
+  double* outputs64[kMaxModes] = {};
 
   // device scalars: [0] = min non-finite copy position (uint64, ~0 = none), [1] = mode
   DevBuf<unsigned long long> nonfinite;
@@ -144,6 +152,7 @@ struct Context {
   // CPD-ALS state
   DevBuf<double> gram;    // N x R x R (fp64)
   DevBuf<double> mtm;     // 2 x R x R: MᵀM accumulators (fp64, ping-pong, zero between uses)
+  uint32_t mtm_rank = 0;  // rank the accumulators were laid out (and zeroed) for
   DevBuf<unsigned int> als_bar;  // grid barrier counter of the fused update (monotonic)
   unsigned int als_bar_count = 0;
   uint64_t als_epoch = 0;
@@ -198,5 +207,8 @@ bool launch_sweep2(Context& c, const float* const* in, float* const* outs);
 // rank_of_row[row_seq[k]] = k for the copy's non-empty rows
 void rank_of_row_build(Context& c, uint32_t mode, DevBuf<uint32_t>& rank);
 void check_nonfinite(Context& c);  // synchronises; throws MK_ENONFINITE
+// fp64 path (mttkrp64.cu)
+void ensure_val64(Context& c, uint32_t mode);
+void launch_mttkrp64(Context& c, uint32_t mode, const double* const* in, double* out, int exec);
 
 }  // namespace mkb

@@ -241,6 +241,9 @@ void tensor_upload(Context& c, uint32_t n, const uint32_t* dims, uint64_t nnz,
     c.factors_set[w] = false;
   }
   c.rank = 0;
+  c.rank64 = 0;
+  c.tensor_f64 = false;
+  c.values64.release();
   c.norm2 = 0.0;
   if (nnz == 0) return;
 

@@ -50,9 +50,10 @@ struct Bounded {  // rng::bounded with the rejection threshold hoisted per modul
   }
 };
 
-float unit_open_closed(std::mt19937_64& g) {
-  return static_cast<float>(1.0 - static_cast<double>(g() >> 11) * 0x1.0p-53);
+double unit_open_closed64(std::mt19937_64& g) {  // rng.hpp:37-39, T = double
+  return 1.0 - static_cast<double>(g() >> 11) * 0x1.0p-53;
 }
+float unit_open_closed(std::mt19937_64& g) { return static_cast<float>(unit_open_closed64(g)); }
 
 uint64_t sat_mul(uint64_t a, uint64_t b) {
   if (a && b > UINT64_MAX / a) return UINT64_MAX;
@@ -143,8 +144,10 @@ std::vector<uint64_t> sample_distinct(std::mt19937_64& g, uint64_t space, uint64
   return out;
 }
 
+// values: fp32 (values32) or fp64 (values64, SparseTensorCOO<double>); the draws are the same
 void generate(uint32_t n, const uint32_t* dims, uint64_t nnz, int dist, uint64_t skew_mode,
-              uint64_t skew_distinct, uint64_t seed, uint32_t* coords, float* values) {
+              uint64_t skew_distinct, uint64_t seed, uint32_t* coords, float* values32,
+              double* values64 = nullptr) {
   if (n == 0) throw GenError{"shape: a tensor needs at least one mode"};
   for (uint32_t h = 0; h < n; ++h)
     if (!dims[h]) throw GenError{"shape: zero extent"};
@@ -220,7 +223,10 @@ void generate(uint32_t n, const uint32_t* dims, uint64_t nnz, int dist, uint64_t
       base += quota;
     }
   }
-  for (uint64_t i = 0; i < nnz; ++i) values[i] = unit_open_closed(g);
+  if (values64)
+    for (uint64_t i = 0; i < nnz; ++i) values64[i] = unit_open_closed64(g);
+  else
+    for (uint64_t i = 0; i < nnz; ++i) values32[i] = unit_open_closed(g);
 }
 
 // per-mode Zipf(exponent) over a seeded permutation of [0, I_h).
@@ -299,6 +305,26 @@ int mk_generate_synthetic(uint32_t n, const uint32_t* dims, uint64_t nnz, int di
 int mk_generate_powerlaw(uint32_t n, const uint32_t* dims, uint64_t nnz, double exponent,
                          uint64_t seed, uint32_t* coords, float* values) {
   return run([&] { generate_powerlaw(n, dims, nnz, exponent, seed, coords, values); });
+}
+
+int mk_generate_synthetic_f64(uint32_t n, const uint32_t* dims, uint64_t nnz, int dist,
+                              uint64_t skew_mode, uint64_t skew_distinct, uint64_t seed,
+                              uint32_t* coords, double* values) {
+  return run([&] {
+    generate(n, dims, nnz, dist, skew_mode, skew_distinct, seed, coords, nullptr, values);
+  });
+}
+
+int mk_random_factors_f64(uint32_t n, const uint32_t* dims, uint64_t rank, uint64_t seed,
+                          double* const* factors) {
+  return run([&] {
+    if (rank < 1) throw GenError{"factor: rank must be at least 1"};
+    for (uint32_t d = 0; d < n; ++d) {
+      std::mt19937_64 g = engine_for(seed, uint64_t{d} + 1);
+      const uint64_t cnt = static_cast<uint64_t>(dims[d]) * rank;
+      for (uint64_t i = 0; i < cnt; ++i) factors[d][i] = unit_open_closed64(g);
+    }
+  });
 }
 
 int mk_random_factors(uint32_t n, const uint32_t* dims, uint64_t rank, uint64_t seed,

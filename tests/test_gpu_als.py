@@ -17,7 +17,24 @@ def dense_lowrank_tensor(mk, dims, rank, seed):
     return mk.SparseTensorCOO(dims, coords, vals)
 
 
-@pytest.mark.parametrize("rank,seed", [(4, 0), (8, 1), (16, 2), (32, 3)])
+def check_against_fp64(ctx, dims, coords, values, f0, tol=1e-4):
+    """Factors, lambda and fit of one device iteration against the fp64 restatement, with the
+    north star's 1e-4 relative bound (verify.hpp:21-39 error |g-w|/max(1,|w|)); returns the
+    worst factor error."""
+    fit, lam = ctx.cpd_als_iter()
+    Y, lam64, fit64, _ = als_oracle.als_iteration(dims, coords, values, f0)
+    worst = 0.0
+    for d in range(len(dims)):
+        got = ctx.download_factor(d).astype(np.float64)
+        worst = max(worst, float((np.abs(got - Y[d]) / np.maximum(1.0, np.abs(Y[d]))).max()))
+    lam_err = float((np.abs(lam - lam64) / np.maximum(1.0, np.abs(lam64))).max())
+    assert worst <= tol, worst
+    assert lam_err <= tol, lam_err
+    assert abs(fit - fit64) <= tol, (fit, fit64)
+    return worst
+
+
+@pytest.mark.parametrize("rank,seed", [(4, 0), (8, 1), (16, 2), (32, 3), (64, 4)])
 def test_one_iteration_matches_fp64(mk, rank, seed):
     g = np.random.default_rng(seed)
     dims = [30, 40, 50]
@@ -26,13 +43,35 @@ def test_one_iteration_matches_fp64(mk, rank, seed):
     plans = mk.build_mode_plans(t, 8)
     ctx = plans[0]._ctx
     ctx.upload_factors(f0)
-    fit, lam = ctx.cpd_als_iter()
-    Y, lam64, fit64, _ = als_oracle.als_iteration(dims, t.coords, t.values, f0)
-    for d in range(3):
-        got = ctx.download_factor(d)
-        assert np.max(np.abs(got - Y[d])) < 2e-3, d
-    assert np.allclose(lam, lam64, rtol=1e-3)
-    assert abs(fit - fit64) < 1e-4
+    check_against_fp64(ctx, dims, t.coords, t.values, f0)
+
+
+def test_cfg3_shaped_r64_update(mk):
+    """k_als_update<64, 1024> (the R = 64 path of cfg3's "full CPD-ALS R=64") on cfg3-shaped
+    power-law data (nips extents, 4 modes, 300 K nnz), one iteration at 1e-4."""
+    dims = [2482, 2862, 14036, 17]
+    t = mk.generate_powerlaw(dims, 300_000, 1.0, 3)
+    g = np.random.default_rng(11)
+    f0 = [g.normal(size=(d, 64)).astype(np.float32) for d in dims]
+    plans = mk.build_mode_plans(t, 148)
+    ctx = plans[0]._ctx
+    ctx.upload_factors(f0)
+    check_against_fp64(ctx, dims, t.coords, t.values, f0)
+
+
+def test_rank_change_resets_accumulators(mk):
+    """after an odd number of mode updates at one rank, a lower-rank upload on the
+    same context must not read stale MᵀM sums (als.cu als_prepare)."""
+    dims = [30, 40, 50]
+    t = mk.generate_synthetic(dims, 6000, seed=9)
+    plans = mk.build_mode_plans(t, 8)
+    ctx = plans[0]._ctx
+    g = np.random.default_rng(5)
+    ctx.upload_factors([g.normal(size=(d, 64)).astype(np.float32) for d in dims])
+    ctx.cpd_als_iter()  # N = 3 updates: the ping-pong ends on slot 1
+    f0 = [g.normal(size=(d, 16)).astype(np.float32) for d in dims]
+    ctx.upload_factors(f0)
+    check_against_fp64(ctx, dims, t.coords, t.values, f0)
 
 
 def test_exact_lowrank_recovered(mk):

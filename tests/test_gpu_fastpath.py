@@ -13,7 +13,6 @@ Scheme 2 drifts ~5e-6 on far shorter rows.
 import numpy as np
 import pytest
 
-from oracle import als as als_oracle
 
 pytestmark = pytest.mark.gpu
 
@@ -269,7 +268,7 @@ def test_fused_sweep_unifies_outer_staging(mk, orc, monkeypatch):
     c.upload_tensor(t)
     c.build_plans(148)
     c.upload_factors(f)  # timed plan choice: every mode settles on K = 0 (see bench cfg3)
-    want = [orc.mttkrp(dims, t.coords, t.values, f, d) for d in range(4)]
+    truth = [orc.mttkrp_f64(dims, t.coords, t.values, f, d) for d in range(4)]
     for rep in range(2):
         c.sweep_async(False, False)
         c.synchronize()
@@ -277,15 +276,9 @@ def test_fused_sweep_unifies_outer_staging(mk, orc, monkeypatch):
         uniform = len({(i.kernel, i.outer_level, i.staged_levels) for i in infos}) == 1
         assert c.last_sweep_fused() == uniform, [i.as_dict() for i in infos]
         for d in range(4):
-            got = c.output(d)
-            err = mk.verify_against(got, want[d])[0]
-            if err > 1e-4:
-                # power-law head rows (~1M nnz): the reference's sequential fp32 sum itself
-                # drifts ~1e-4; the fast path must be at least as close to the fp64 truth
-                truth = als_oracle.mttkrp64(dims, t.coords, t.values, f, d)
-                e_fast = mk.verify_against(got.astype(np.float64), truth)[0]
-                e_orc = mk.verify_against(want[d].astype(np.float64), truth)[0]
-                assert e_fast <= e_orc, (rep, d, err, e_fast, e_orc)
+            # power-law head rows (~1M nnz): the reference's sequential fp32 sum itself drifts
+            # up to 6.3e-4 from the exact value, so the gate is the fp64 truth (hard 1e-4)
+            assert orc.max_rel_err_f64(c.output(d), truth[d]) <= 1e-4, (rep, d)
 
 
 def test_sharded_ranges_timed_choice(mk, orc):

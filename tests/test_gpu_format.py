@@ -85,10 +85,18 @@ def test_adaptive_selection_kat(mk):
                                          mk.Scheme.scheme2, mk.Scheme.scheme2]
 
 
-@pytest.mark.parametrize("name", ["cfg1", "cfg2_uber", "cfg4_lbnl", "adaptive_kat"])
+@pytest.mark.parametrize("name", ["cfg1", "cfg2_uber", "cfg3_nips", "cfg4_lbnl", "cfg5_nell2",
+                                  "adaptive_kat"])
 def test_config_plans_match_reference_pins(mk, golden, name):
+    """Every BASELINE config at full size, format bit-exact against the reference's own
+    build_mode_plans (sha256 of order / partition_offsets / owned_indices, computed by the
+    reference in tests/golden/make_golden.py) at kappa = 148 and a second kappa (8 or 16),
+    cyclic and LPT."""
     e = [c for c in golden["configs"] if c["name"] == name][0]
-    t = mk.generate_synthetic(e["dims"], e["nnz"], seed=e["seed"])
+    if e.get("gen") == "powerlaw":
+        t = mk.generate_powerlaw(e["dims"], e["nnz"], 1.0, e["seed"])
+    else:
+        t = mk.generate_synthetic(e["dims"], e["nnz"], seed=e["seed"])
     assert sha(t.coords) == e["coords_sha"] and sha(t.values) == e["values_sha"]
     ctx = mk.Context()
     ctx.upload_tensor(t)

@@ -10,7 +10,6 @@ import hashlib
 import numpy as np
 import pytest
 
-from oracle import als as als_oracle
 
 pytestmark = pytest.mark.gpu
 
@@ -211,26 +210,27 @@ def test_config_deterministic_matches_reference_pins(mk, golden, name):
     ("cfg4_lbnl", [1605, 4198, 1631, 4209, 868131], 1_700_000, 32),
 ])
 def test_config_fast_within_tolerance(mk, orc, cfg):
+    """Fast path within the north star's 1e-4 of the fp64 truth, a hard gate: oracle_mttkrp
+    with T = double (orc.mttkrp_f64 is bitwise the reference's oracle_mttkrp<double>, pinned
+    in test_oracle.py against the reference's own sha256).  The reference's fp32 result itself
+    sits up to 3.7e-5 (uber mode 1) from that truth (golden ref32_vs_64_max_rel_err)."""
     name, dims, nnz, rank = cfg
     t = mk.generate_synthetic(dims, nnz, seed=1)
     f = [m.data for m in mk.random_factors(dims, rank, 1)]
     plans = mk.build_mode_plans(t, 148)
     outs = mk.mttkrp_all_modes(t, plans, f, mk.ExecConfig(148), False)
     for d in range(len(dims)):
+        truth = orc.mttkrp_f64(dims, t.coords, t.values, f, d)
+        assert orc.max_rel_err_f64(outs[d].data, truth) <= 1e-4, (name, d)
         want = orc.mttkrp(dims, t.coords, t.values, f, d)
-        err = mk.verify_against(outs[d], want)[0]
-        # BASELINE.json north star: 1e-4 relative in fp32.  Rows of ~137K nnz (uber mode 1)
-        # drift ~3e-5 from the reference's sequential fp32 sum; most of that is the
-        # oracle's own rounding: the fast result is at least as close to the fp64 truth.
-        assert err <= 1e-4, (name, d, err)
-        if err > 1e-5:
-            truth = als_oracle.mttkrp64(dims, t.coords, t.values, f, d)
-            e_fast = mk.verify_against(outs[d].data.astype(np.float64), truth)[0]
-            e_orc = mk.verify_against(want.astype(np.float64), truth)[0]
-            assert e_fast <= e_orc * 1.5 + 1e-6, (name, d, e_fast, e_orc)
+        assert mk.verify_against(outs[d], want)[0] <= 1e-4, (name, d)
 
 
 def test_nips_powerlaw_r64(mk, orc):
+    """cfg3 at full size (power-law, R = 64): deterministic bitwise == the reference fp32 oracle;
+    fast within 1e-4 of the fp64 truth (hard gate).  The reference's own sequential fp32 sum
+    drifts up to 6.3e-4 from that truth on the ~1M-nnz head rows (golden
+    ref32_vs_64_max_rel_err), so the fast path is gated against fp64, not against it."""
     dims = [2482, 2862, 14036, 17]
     t = mk.generate_powerlaw(dims, 3_100_000, 1.0, 1)
     f = [m.data for m in mk.random_factors(dims, 64, 1)]
@@ -241,15 +241,8 @@ def test_nips_powerlaw_r64(mk, orc):
     for d in range(4):
         want = orc.mttkrp(dims, t.coords, t.values, f, d)
         assert np.array_equal(det[d].data.view(np.uint32), want.view(np.uint32))
-        err = mk.verify_against(outs[d], want)[0]
-        if err > 1e-4:
-            # power-law head rows hold ~1M nnz: the reference's sequential fp32 row sum
-            # itself drifts ~1e-4 from the exact value.  The fast path must then be at
-            # least as close to the fp64 truth as the reference is.
-            truth = als_oracle.mttkrp64(dims, t.coords, t.values, f, d)
-            e_fast = mk.verify_against(outs[d].data.astype(np.float64), truth)[0]
-            e_orc = mk.verify_against(want.astype(np.float64), truth)[0]
-            assert e_fast <= e_orc, (d, err, e_fast, e_orc)
+        truth = orc.mttkrp_f64(dims, t.coords, t.values, f, d)
+        assert orc.max_rel_err_f64(outs[d].data, truth) <= 1e-4, d
 
 
 def test_sweep_host_and_async_agree(mk):
@@ -270,24 +263,3 @@ def test_sweep_host_and_async_agree(mk):
         assert np.array_equal(ctx.output(d), ref[d])
 
 
-def test_cfg5_full_size_vs_oracle(mk, orc):
-    """BASELINE cfg5 at full size (nell-2 shape, 77M nnz, R = 32): the fused fast sweep within
-    the north star's 1e-4 and the deterministic kernel bitwise equal to the C oracle
-    (oracle_mttkrp order, oracle.hpp:20-43) on every mode."""
-    dims = [12092, 9184, 28818]
-    t = mk.generate_synthetic(dims, 77_000_000, seed=1)
-    f = [m.data for m in mk.random_factors(dims, 32, 1)]
-    c = mk.Context()
-    c.upload_tensor(t)
-    c.build_plans(148)
-    c.upload_factors(f)
-    fast = c.mttkrp_all_modes(False, False)
-    c.sweep_async(False, False)  # the fused single-launch sweep (after the per-mode tuning)
-    c.synchronize()
-    fused = [c.output(d) for d in range(3)]
-    det = c.mttkrp_all_modes(False, True)
-    for d in range(3):
-        want = orc.mttkrp(dims, t.coords, t.values, f, d)
-        assert np.array_equal(det[d].view(np.uint32), want.view(np.uint32)), d
-        assert mk.verify_against(fast[d], want)[0] <= 1e-4, d
-        assert mk.verify_against(fused[d], want)[0] <= 1e-4, d

@@ -72,6 +72,21 @@ def test_config_pins_small(orc, golden):
         assert sha(orc.mttkrp(e["dims"], c, v, f, d)) == e["mttkrp_sha"][d]
 
 
+@pytest.mark.parametrize("name", ["adaptive_kat", "cfg2_uber"])
+def test_oracle_f64_matches_reference_pins(orc, golden, name):
+    """oracle.hpp:20-43 with T = double: the C restatement (row-parallel) is bitwise equal to the
+    reference's own oracle_mttkrp<double> (sha256 computed by the reference); the recorded
+    deviation of the reference's fp32 result from it is what the fast path is compared with."""
+    e = [c for c in golden["configs"] if c["name"] == name][0]
+    c, v = orc.generate_synthetic(e["dims"], e["nnz"], 0, 0, 2, e["seed"])
+    f = orc.random_factors(e["dims"], e["rank"], 1)
+    for d in range(len(e["dims"])):
+        got = orc.mttkrp_f64(e["dims"], c, v, f, d)
+        assert sha(got) == e["mttkrp64_sha"][d], (name, d)
+        want32 = orc.mttkrp(e["dims"], c, v, f, d)
+        assert abs(orc.max_rel_err_f64(want32, got) - e["ref32_vs_64_max_rel_err"][d]) < 1e-12
+
+
 @pytest.mark.slow
 def test_config_pins_cfg1(orc, golden):
     e = [c for c in golden["configs"] if c["name"] == "cfg1"][0]
@@ -110,6 +125,9 @@ def test_oracle_matches_reference_random(orc, ref, seed):
         a = orc.mttkrp(dims, c, v, f, d)
         b = ref.oracle_mttkrp(dims, c, v, f, d)
         assert np.array_equal(a.view(np.uint32), b.view(np.uint32))
+        a64 = orc.mttkrp_f64(dims, c, v, f, d, threads=3)
+        b64 = ref.oracle_mttkrp_f64(dims, c, v, f, d)
+        assert np.array_equal(a64.view(np.uint64), b64.view(np.uint64))
 
 
 def test_skewed_generator_matches_reference(orc, ref):
