@@ -15,9 +15,11 @@
 //                                     kernel.hpp:23-287 — spMTTKRP on the GPU
 //   cpd_als                           (absent in the reference)
 //
-// Only fp32 (T = float) runs on the device; the reference's fp64 instantiation is not
-// provided.  A ModePlan keeps a handle to the device session that owns the uploaded
-// tensor and its mode copies; plans of one build_mode_plans call share it.
+// T = float runs the fast fp32 kernels; T = double (the reference's fp64 instantiation,
+// SURVEY §8 f-4) runs the fp64 device path (mk_*_f64; deterministic = oracle_mttkrp<double>
+// bitwise).  A ModePlan keeps a handle to the device session that owns the uploaded tensor
+// and its mode copies; plans of one build_mode_plans call share it, and every call gets its
+// own session.
 #pragma once
 
 #include <algorithm>
@@ -27,9 +29,11 @@
 #include <cstring>
 #include <initializer_list>
 #include <memory>
+#include <random>
 #include <span>
 #include <stdexcept>
 #include <string>
+#include <type_traits>
 #include <vector>
 
 #include "mttkrp_b200.h"
@@ -65,7 +69,8 @@ struct Shape {
 
 template <typename T>
 class SparseTensorCOO {
-  static_assert(std::is_same_v<T, float>, "the B200 path computes in fp32");
+  static_assert(std::is_same_v<T, float> || std::is_same_v<T, double>,
+                "the device path computes in fp32 or fp64");
 
  public:
   using value_type = T;
@@ -166,14 +171,42 @@ std::vector<FactorMatrix<T>> random_factors(const Shape& shape, std::size_t rank
                                             std::uint64_t seed) {
   if (rank < 1) throw error("factor: rank must be at least 1");
   std::vector<FactorMatrix<T>> out;
-  std::vector<float*> ptrs;
+  std::vector<T*> ptrs;
   for (std::size_t d = 0; d < shape.mode_count(); ++d)
     out.push_back(FactorMatrix<T>::zeros(d, shape.extent(d), rank));
   for (auto& m : out) ptrs.push_back(m.data.data());
-  detail::check(mk_random_factors(static_cast<uint32_t>(shape.mode_count()), shape.dims.data(),
-                                  rank, seed, ptrs.data()));
+  if constexpr (std::is_same_v<T, double>)
+    detail::check(mk_random_factors_f64(static_cast<uint32_t>(shape.mode_count()),
+                                        shape.dims.data(), rank, seed, ptrs.data()));
+  else
+    detail::check(mk_random_factors(static_cast<uint32_t>(shape.mode_count()), shape.dims.data(),
+                                    rank, seed, ptrs.data()));
   return out;
 }
+
+// rng.hpp:12-39: the reference's public random primitives (test support uses them).
+namespace rng {
+using engine = std::mt19937_64;
+inline std::uint64_t splitmix64(std::uint64_t x) {
+  x += 0x9e3779b97f4a7c15ull;
+  x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ull;
+  x = (x ^ (x >> 27)) * 0x94d049bb133111ebull;
+  return x ^ (x >> 31);
+}
+inline engine seeded(std::uint64_t seed, std::uint64_t stream = 0) {
+  return engine(splitmix64(seed ^ splitmix64(stream)));
+}
+inline std::uint64_t bounded(engine& g, std::uint64_t n) {  // rejects the low (2^64 mod n)
+  const std::uint64_t low = (0 - n) % n;
+  std::uint64_t x = g();
+  while (x < low) x = g();
+  return x % n;
+}
+template <typename T>
+inline T unit_open_closed(engine& g) {
+  return static_cast<T>(1.0 - static_cast<double>(g() >> 11) * 0x1.0p-53);
+}
+}  // namespace rng
 
 enum class SyntheticDist { uniform, mode_skewed };
 struct SyntheticSpec {
@@ -190,10 +223,15 @@ SparseTensorCOO<T> generate_synthetic(const SyntheticSpec& spec) {
   Shape shape(spec.dims);
   std::vector<index_t> coords(spec.nnz * shape.mode_count());
   std::vector<T> values(spec.nnz);
-  detail::check(mk_generate_synthetic(static_cast<uint32_t>(shape.mode_count()), spec.dims.data(),
-                                      spec.nnz, spec.dist == SyntheticDist::uniform ? 0 : 1,
-                                      spec.skew_mode, spec.skew_distinct, spec.seed,
-                                      coords.data(), values.data()));
+  auto gen = [&](auto fn) {
+    detail::check(fn(static_cast<uint32_t>(shape.mode_count()), spec.dims.data(), spec.nnz,
+                     spec.dist == SyntheticDist::uniform ? 0 : 1, spec.skew_mode,
+                     spec.skew_distinct, spec.seed, coords.data(), values.data()));
+  };
+  if constexpr (std::is_same_v<T, double>)
+    gen(mk_generate_synthetic_f64);
+  else
+    gen(mk_generate_synthetic);
   return SparseTensorCOO<T>::from_parts(std::move(shape), std::move(coords), std::move(values));
 }
 
@@ -251,8 +289,12 @@ namespace detail {
 template <typename T>
 std::shared_ptr<Session> upload(const SparseTensorCOO<T>& t) {
   auto s = std::make_shared<Session>();
-  check(mk_tensor_upload(s->ctx, static_cast<uint32_t>(t.mode_count()), t.shape().dims.data(),
-                         t.nnz(), t.coord_data(), t.values().data()));
+  if constexpr (std::is_same_v<T, double>)
+    check(mk_tensor_upload_f64(s->ctx, static_cast<uint32_t>(t.mode_count()),
+                               t.shape().dims.data(), t.nnz(), t.coord_data(), t.values().data()));
+  else
+    check(mk_tensor_upload(s->ctx, static_cast<uint32_t>(t.mode_count()), t.shape().dims.data(),
+                           t.nnz(), t.coord_data(), t.values().data()));
   s->tensor = &t;
   s->nnz = t.nnz();
   return s;
@@ -372,10 +414,21 @@ void validate_plan(const SparseTensorCOO<T>& t, const ModePlan& plan, const Exec
 
 template <typename T>
 void upload_factors(Session& s, const std::vector<FactorMatrix<T>>& f) {
-  std::vector<const float*> p;
+  std::vector<const T*> p;
   for (auto& m : f) p.push_back(m.data.data());
-  check(mk_factors_upload(s.ctx, static_cast<uint32_t>(f[0].rank), p.data()));
+  if constexpr (std::is_same_v<T, double>)
+    check(mk_factors_upload_f64(s.ctx, static_cast<uint32_t>(f[0].rank), p.data()));
+  else
+    check(mk_factors_upload(s.ctx, static_cast<uint32_t>(f[0].rank), p.data()));
   s.rank = f[0].rank;
+}
+
+template <typename T>
+int mode_call(mk_context* ctx, uint32_t mode, int exec, T* out) {
+  if constexpr (std::is_same_v<T, double>)
+    return mk_mttkrp_mode_f64(ctx, mode, exec, out);
+  else
+    return mk_mttkrp_mode(ctx, mode, exec, out);
 }
 }  // namespace detail
 
@@ -395,6 +448,15 @@ void element_update(std::span<const index_t> coords, T value,
   }
 }
 
+template <typename T>
+std::vector<T> element_update(const SparseTensorCOO<T>& t, std::size_t element,
+                              const std::vector<FactorMatrix<T>>& factors,
+                              std::size_t output_mode) {  // kernel.hpp:145-153
+  std::vector<T> acc(factors.empty() ? 0 : factors[0].rank);
+  element_update<T>(t.coords(element), t.value(element), factors, output_mode, acc);
+  return acc;
+}
+
 // kernel.hpp:161-169 on the device.
 template <typename T>
 FactorMatrix<T> mttkrp_mode(const SparseTensorCOO<T>& t, const ModePlan& plan,
@@ -404,9 +466,9 @@ FactorMatrix<T> mttkrp_mode(const SparseTensorCOO<T>& t, const ModePlan& plan,
   detail::validate_plan(t, plan, config);
   detail::upload_factors(*plan.device, factors);
   auto out = FactorMatrix<T>::zeros(plan.mode, t.extent(plan.mode), factors[0].rank);
-  detail::check(mk_mttkrp_mode(plan.device->ctx, static_cast<uint32_t>(plan.mode),
-                               config.deterministic ? MK_EXEC_DETERMINISTIC : MK_EXEC_FAST,
-                               out.data.data()));
+  detail::check(detail::mode_call<T>(plan.device->ctx, static_cast<uint32_t>(plan.mode),
+                                     config.deterministic ? MK_EXEC_DETERMINISTIC : MK_EXEC_FAST,
+                                     out.data.data()));
   return out;
 }
 
@@ -424,13 +486,17 @@ std::vector<FactorMatrix<T>> mttkrp_all_modes(const SparseTensorCOO<T>& t,
   for (const auto& p : plans) detail::validate_plan(t, p, config);
   detail::upload_factors(*plans[0].device, factors);
   std::vector<FactorMatrix<T>> outs;
-  std::vector<float*> ptr;
+  std::vector<T*> ptr;
   for (std::size_t d = 0; d < plans.size(); ++d)
     outs.push_back(FactorMatrix<T>::zeros(d, t.extent(d), factors[0].rank));
   for (auto& o : outs) ptr.push_back(o.data.data());
-  detail::check(mk_mttkrp_all_modes(plans[0].device->ctx, chain_outputs ? 1 : 0,
-                                    config.deterministic ? MK_EXEC_DETERMINISTIC : MK_EXEC_FAST,
-                                    ptr.data()));
+  const int exec = config.deterministic ? MK_EXEC_DETERMINISTIC : MK_EXEC_FAST;
+  if constexpr (std::is_same_v<T, double>)
+    detail::check(mk_mttkrp_all_modes_f64(plans[0].device->ctx, chain_outputs ? 1 : 0, exec,
+                                          ptr.data()));
+  else
+    detail::check(mk_mttkrp_all_modes(plans[0].device->ctx, chain_outputs ? 1 : 0, exec,
+                                      ptr.data()));
   return outs;
 }
 
@@ -481,6 +547,49 @@ TimedRun<T> run_timed(const SparseTensorCOO<T>& t, const std::vector<ModePlan>& 
   const std::size_t n = plans.size();
   std::vector<double> mode_ms(iters * n), total(iters);
   int same = 1;
+  if constexpr (std::is_same_v<T, double>) {
+    // fp64: host-timed per-mode calls as in the reference (steady_clock around each mode,
+    // kernel.hpp:258-265), outputs compared bitwise across iterations
+    TimedRun<T> run;
+    run.report.iters = iters;
+    std::vector<ModeTiming> modes(n);
+    for (std::size_t it = 0; it < iters; ++it) {
+      std::vector<FactorMatrix<T>> outs;
+      double tot = 0;
+      for (std::size_t d = 0; d < n; ++d) {
+        auto o = FactorMatrix<T>::zeros(d, t.extent(d), factors[0].rank);
+        const auto t0 = std::chrono::steady_clock::now();
+        detail::check(mk_mttkrp_mode_f64(plans[0].device->ctx, static_cast<uint32_t>(d),
+                                         config.deterministic ? MK_EXEC_DETERMINISTIC : MK_EXEC_FAST,
+                                         o.data.data()));
+        const double ms = std::chrono::duration<double, std::milli>(
+                              std::chrono::steady_clock::now() - t0).count();
+        modes[d].wall_ms.push_back(ms);
+        tot += ms;
+        outs.push_back(std::move(o));
+      }
+      run.report.total_ms.push_back(tot);
+      if (it == 0)
+        run.outputs = std::move(outs);
+      else if (!bitwise_equal(outs, run.outputs))
+        run.report.outputs_bit_identical = false;
+    }
+    for (std::size_t d = 0; d < n; ++d) {
+      ModeTiming& mt = modes[d];
+      mt.mode = d;
+      mt.scheme = plans[d].scheme;
+      mt.min_ms = *std::min_element(mt.wall_ms.begin(), mt.wall_ms.end());
+      mt.median_ms = detail::median_of(mt.wall_ms);
+      for (std::size_t z = 0; z < plans[d].kappa; ++z) {
+        mt.elements_per_worker.push_back(plans[d].partition_size(z));
+        mt.busy_workers += plans[d].partition_size(z) > 0;
+      }
+    }
+    run.report.modes = std::move(modes);
+    run.report.total_min_ms = *std::min_element(run.report.total_ms.begin(), run.report.total_ms.end());
+    run.report.total_median_ms = detail::median_of(run.report.total_ms);
+    return run;
+  } else {
   detail::check(mk_run_timed(plans[0].device->ctx, iters,
                              config.deterministic ? MK_EXEC_DETERMINISTIC : MK_EXEC_FAST, 1,
                              mode_ms.data(), total.data(), &same));
@@ -509,6 +618,7 @@ TimedRun<T> run_timed(const SparseTensorCOO<T>& t, const std::vector<ModePlan>& 
     run.outputs.push_back(std::move(o));
   }
   return run;
+  }
 }
 
 // CPD-ALS driver (no reference counterpart).  Returns the final fit; factors are updated
@@ -517,6 +627,7 @@ template <typename T>
 double cpd_als(const SparseTensorCOO<T>& t, const std::vector<ModePlan>& plans,
                std::vector<FactorMatrix<T>>& factors, std::size_t max_iters, double tol,
                std::vector<T>* lambda = nullptr, std::size_t* iters_done = nullptr) {
+  static_assert(std::is_same_v<T, float>, "cpd_als runs in fp32 on the device");
   detail::validate_factors(t, factors);
   auto& s = *plans.at(0).device;
   detail::upload_factors(s, factors);

@@ -39,6 +39,7 @@ __all__ = [
     "FactorMatrix", "ModePlan", "Context", "build_mode_plans", "mttkrp_mode",
     "mttkrp_all_modes", "run_timed", "generate_synthetic", "generate_powerlaw",
     "random_factors", "verify_against", "verify_tolerance", "mode_degrees", "cpd_als",
+    "element_update",
     "load_library", "library_path", "EXPORTED_SYMBOLS",
 ]
 
@@ -585,11 +586,15 @@ def _context_for(t: SparseTensorCOO) -> Context:
 
 def build_mode_plans(t: SparseTensorCOO, kappa: int, strategy=Strategy.cyclic,
                      policy=SchemePolicy.adaptive) -> List[ModePlan]:
-    """layout.hpp:131-149 — all N mode copies built on the device."""
+    """layout.hpp:131-149 — all N mode copies built on the device.  Every call owns a new
+    device session (as the C++ header's Session), so plans of an earlier call (another kappa
+    or policy on the same tensor) keep describing — and running on — their own copies."""
     if kappa < 1:
         raise MttkrpError("layout: kappa must be at least 1")
-    ctx = _context_for(t)
+    ctx = Context()
+    ctx.upload_tensor(t)
     ctx.build_plans(kappa, strategy, policy)
+    t._ctx = ctx  # the latest session also serves mode_degrees
     return [ModePlan(ctx, d, t) for d in range(t.mode_count())]
 
 
@@ -683,6 +688,21 @@ def mttkrp_all_modes(t: SparseTensorCOO, plans: Sequence[ModePlan], factors, con
     _upload_if_changed(ctx, factors)
     outs = ctx.mttkrp_all_modes(chain_outputs, config.deterministic)
     return [FactorMatrix(d, o) for d, o in enumerate(outs)]
+
+
+def element_update(t: SparseTensorCOO, element: int, factors, output_mode: int) -> np.ndarray:
+    """kernel.hpp:133-153 (host arithmetic, API parity): acc[r] = value * prod_{w != d}
+    Y_w(c_w, r), multiplied in ascending mode order."""
+    factors = _as_factors(factors)
+    rank = factors[0].rank if factors else 0
+    if any(f.rank != rank for f in factors):
+        raise MttkrpError("kernel: factor matrices disagree on rank")
+    dt = t.values.dtype
+    acc = np.full(rank, t.values[element], dtype=dt)
+    for w, f in enumerate(factors):
+        if w != output_mode:
+            acc = (acc * f.data[int(t.coords[element, w])].astype(dt)).astype(dt)
+    return acc
 
 
 @dataclass

@@ -38,6 +38,10 @@ class ShardExchange:
         self.R = int(rank_count)
         self.device = device if device is not None else torch.device("cuda",
                                                                       torch.cuda.current_device())
+        # the library enqueues on torch's current stream, the one NCCL's all-gather runs on:
+        # pack -> all_gather -> unpack are then ordered without extra events
+        if self.device.type == "cuda":
+            ctx.set_stream(torch.cuda.current_stream(self.device).cuda_stream)
         ctx.set_shard(self.rank, self.world)
         self.stride, self.send, self.recv, self.owned = [], [], [], []
         for d in range(len(self.dims)):

@@ -1,6 +1,7 @@
 // The reference's own kernel/layout test cases (proj/tests/test_kernel.cpp,
 // test_layout.cpp), re-stated against the C++ drop-in header so they read like the
 // reference's tests: only the include and the namespace alias change.
+#include <cmath>
 #include <cstdio>
 #include <functional>
 #include <set>
@@ -133,6 +134,7 @@ void determinism_and_chain() {
   CHECK(timed.report.iters == 3 && timed.report.total_ms.size() == 3);
   CHECK(timed.report.modes[1].busy_workers == 8);
   CHECK(bitwise_equal(timed.outputs, base));
+  CHECK(timed.report.outputs_bit_identical);  // deterministic exec: computed, kernel.hpp:271-276
 }
 
 void errors() {
@@ -163,11 +165,64 @@ void errors() {
   CHECK(got);
 }
 
+void element_updates() {  // test_kernel.cpp:39-55
+  SparseTensorCOO<float> ones(Shape({2, 2, 2}));
+  ones.add({0, 1, 0}, 1.0f);
+  auto all_ones = matrices_from<float>({{{1, 1}, {1, 1}}, {{1, 1}, {1, 1}}, {{1, 1}, {1, 1}}});
+  CHECK(element_update(ones, 0, all_ones, 2) == std::vector<float>({1, 1}));
+  SparseTensorCOO<float> t(Shape({1, 2, 1}));
+  t.add({0, 1, 0}, 3.0f);
+  auto f = matrices_from<float>({{{1, 2}}, {{9, 9}, {2, 1}}, {{5, 5}}});
+  CHECK(element_update(t, 0, f, 2) == std::vector<float>({6, 6}));
+  auto disjoint = matrices_from<float>({{{1, 0}}, {{9, 9}, {0, 1}}, {{5, 5}}});
+  SparseTensorCOO<float> t2(Shape({1, 2, 1}));
+  t2.add({0, 1, 0}, 2.0f);
+  CHECK(element_update(t2, 0, disjoint, 2) == std::vector<float>({0, 0}));
+  auto bad = f;
+  bad[1] = FactorMatrix<float>::zeros(1, 2, 3);
+  CHECK_THROWS(element_update(t, 0, bad, 2));
+}
+
+void fp64_path() {  // T = double: deterministic == oracle_mttkrp<double> order (f-4)
+  SyntheticSpec spec;
+  spec.dims = {40, 30, 20};
+  spec.nnz = 3000;
+  spec.seed = 5;
+  auto t = generate_synthetic<double>(spec);
+  auto factors = random_factors<double>(t.shape(), 8, 3);
+  auto plans = build_mode_plans(t, 8);
+  auto det = mttkrp_all_modes(t, plans, factors, ExecConfig{8, 32, true}, false);
+  auto fast = mttkrp_all_modes(t, plans, factors, ExecConfig{8, 32, false}, false);
+  for (std::size_t d = 0; d < 3; ++d) {
+    auto want = FactorMatrix<double>::zeros(d, t.extent(d), 8);
+    for (std::size_t i = 0; i < t.nnz(); ++i) {
+      auto c = t.coords(i);
+      for (std::size_t r = 0; r < 8; ++r) {
+        double term = t.value(i);
+        for (std::size_t w = 0; w < 3; ++w)
+          if (w != d) term *= factors[w].at(c[w], r);
+        want.at(c[d], r) += term;
+      }
+    }
+    CHECK(bitwise_equal(det[d], want));
+    double worst = 0;
+    for (std::size_t k = 0; k < want.data.size(); ++k)
+      worst = std::max(worst, std::abs(fast[d].data[k] - want.data[k]) /
+                                  std::max(1.0, std::abs(want.data[k])));
+    CHECK(worst <= 1e-12);
+  }
+  auto timed = run_timed(t, plans, factors, ExecConfig{8, 32, true}, 2);
+  CHECK(timed.report.outputs_bit_identical && bitwise_equal(timed.outputs, det));
+  auto g = rng::seeded(7);
+  auto g2 = rng::seeded(7);
+  CHECK(rng::bounded(g, 10) == rng::bounded(g2, 10));
+}
+
 int main() {
   const std::vector<std::pair<const char*, std::function<void()>>> cases = {
       {"single nonzero", single_nonzero}, {"partition KATs", partition_kats},
       {"adaptive selection", adaptive_selection}, {"determinism & chain", determinism_and_chain},
-      {"errors", errors}};
+      {"errors", errors}, {"element_update", element_updates}, {"fp64 path", fp64_path}};
   for (auto& [name, fn] : cases) {
     const int before = g_fail;
     try {

@@ -118,3 +118,18 @@ def test_no_cpu_fallback_without_gpu(mk):
         pytest.skip("GPU present")
     with pytest.raises(mk.MttkrpError):
         mk.Context()
+
+
+def test_element_update(mk):
+    """kernel.hpp:133-153 via test_kernel.cpp:39-55 (host arithmetic, API parity)."""
+    ones = mk.SparseTensorCOO([2, 2, 2], [[0, 1, 0]], [1.0])
+    all_ones = [np.ones((2, 2), np.float32)] * 3
+    assert mk.element_update(ones, 0, all_ones, 2).tolist() == [1, 1]
+    t = mk.SparseTensorCOO([1, 2, 1], [[0, 1, 0]], [3.0])
+    f = [np.array(m, np.float32) for m in ([[1, 2]], [[9, 9], [2, 1]], [[5, 5]])]
+    assert mk.element_update(t, 0, f, 2).tolist() == [6, 6]
+    t2 = mk.SparseTensorCOO([1, 2, 1], [[0, 1, 0]], [2.0])
+    disjoint = [np.array(m, np.float32) for m in ([[1, 0]], [[9, 9], [0, 1]], [[5, 5]])]
+    assert mk.element_update(t2, 0, disjoint, 2).tolist() == [0, 0]
+    with pytest.raises(mk.MttkrpError, match="disagree on rank"):
+        mk.element_update(t, 0, [f[0], np.zeros((2, 3), np.float32), f[2]], 2)
