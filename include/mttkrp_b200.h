@@ -74,6 +74,8 @@ typedef struct {
 const char* mk_last_error(void);
 const char* mk_version(void);
 int mk_device_count(int* count);
+/* streaming multiprocessors of `device` (the CLI's default kappa for the GPU backend) */
+int mk_device_sm_count(int device, int* sms);
 int mk_create(int device, mk_context** out);
 int mk_destroy(mk_context* ctx);
 /* Run all work on an external CUDA stream (cudaStream_t passed as void*).  NULL is the
@@ -211,6 +213,40 @@ int mk_generate_synthetic_f64(uint32_t n_modes, const uint32_t* dims, uint64_t n
                               uint32_t* coords_aos, double* values);
 int mk_random_factors_f64(uint32_t n_modes, const uint32_t* dims, uint64_t rank, uint64_t seed,
                           double* const* factors);
+
+/* ---- FROSTT text and binary tensor cache (frostt.hpp:19-211) -----------
+ * Multithreaded parse with the reference's semantics and error texts ("frostt: line N: ..."):
+ * 1-based indices, '#' comments and blank lines skipped, values parsed in `prec` (32 / 64)
+ * precision with std::from_chars, duplicates summed in file order into the first occurrence
+ * (merge_duplicates != 0, FrosttOptions::merge_duplicates) or rejected, extents inferred
+ * unless n_override > 0 (FrosttOptions::dims_override).  threads = 0: all host threads.
+ * The result is a host tensor handle; read it with mk_host_tensor_info/_export, free it with
+ * mk_host_tensor_free. */
+typedef struct mk_host_tensor mk_host_tensor;
+int mk_frostt_parse(const char* text, uint64_t len, int prec, int merge_duplicates,
+                    const uint32_t* dims_override, uint32_t n_override, uint32_t threads,
+                    mk_host_tensor** out);                       /* parse_frostt, frostt.hpp:74 */
+int mk_frostt_read_file(const char* path, int prec, int merge_duplicates,
+                        const uint32_t* dims_override, uint32_t n_override, uint32_t threads,
+                        mk_host_tensor** out);                   /* read_frostt_file, :194-199 */
+int mk_host_tensor_info(const mk_host_tensor* t, uint32_t* n_modes, uint32_t* dims,
+                        uint32_t dims_capacity, uint64_t* nnz, uint64_t* duplicates_merged,
+                        int* prec);                              /* FrosttParseResult, :31-35 */
+/* coords_aos: nnz*n_modes uint32; values: nnz floats (prec 32) or doubles (prec 64). */
+int mk_host_tensor_export(const mk_host_tensor* t, uint32_t* coords_aos, void* values);
+int mk_host_tensor_free(mk_host_tensor* t);
+/* write_frostt (frostt.hpp:165-186): 1-based indices, shortest round-trip values.  With
+ * buf == NULL only *len (bytes) is returned. */
+int mk_frostt_format(uint32_t n_modes, uint64_t nnz, const uint32_t* coords_aos,
+                     const void* values, int prec, uint32_t threads, char* buf, uint64_t cap,
+                     uint64_t* len);
+int mk_frostt_write_file(const char* path, uint32_t n_modes, uint64_t nnz,
+                         const uint32_t* coords_aos, const void* values, int prec,
+                         uint32_t threads);                      /* write_frostt_file, :201-206 */
+/* Binary tensor cache ("MKBT" v1, checksummed; no reference counterpart). */
+int mk_tensor_cache_write(const char* path, uint32_t n_modes, const uint32_t* dims, uint64_t nnz,
+                          const uint32_t* coords_aos, const void* values, int prec);
+int mk_tensor_cache_read(const char* path, mk_host_tensor** out);
 
 #ifdef __cplusplus
 }

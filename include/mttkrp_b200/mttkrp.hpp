@@ -33,6 +33,7 @@
 #include <span>
 #include <stdexcept>
 #include <string>
+#include <string_view>
 #include <type_traits>
 #include <vector>
 
@@ -151,6 +152,35 @@ struct FactorMatrix {
   T at(index_t i, std::size_t r) const { return data[static_cast<std::size_t>(i) * rank + r]; }
   bool operator==(const FactorMatrix&) const = default;
 };
+
+// verify.hpp:15-45: |got - want| / max(1, |want|), worst entry
+struct VerifyResult {
+  double max_rel_err = 0.0;
+  index_t worst_row = 0;
+  std::size_t worst_col = 0;
+};
+
+template <typename T>
+VerifyResult verify_against(const FactorMatrix<T>& got, const FactorMatrix<T>& want) {
+  if (got.rows != want.rows || got.rank != want.rank) throw error("verify: matrix shapes differ");
+  VerifyResult res;
+  for (index_t i = 0; i < got.rows; ++i)
+    for (std::size_t r = 0; r < got.rank; ++r) {
+      const double g = static_cast<double>(got.at(i, r)), w = static_cast<double>(want.at(i, r));
+      const double err = std::abs(g - w) / std::max(1.0, std::abs(w));
+      if (err > res.max_rel_err) {
+        res.max_rel_err = err;
+        res.worst_row = i;
+        res.worst_col = r;
+      }
+    }
+  return res;
+}
+
+template <typename T>
+constexpr double verify_tolerance() {
+  return sizeof(T) == 4 ? 1e-5 : 1e-12;
+}
 
 template <typename T>
 bool bitwise_equal(const FactorMatrix<T>& a, const FactorMatrix<T>& b) {
@@ -367,6 +397,106 @@ DegreeProfile mode_degrees(const SparseTensorCOO<T>& t, std::size_t d) {
   p.degrees.resize(t.extent(d));
   detail::check(mk_mode_degrees(s->ctx, static_cast<uint32_t>(d), p.degrees.data()));
   p.total = t.nnz();
+  return p;
+}
+
+inline std::string_view to_string(Scheme s) {  // layout.cpp:9-11
+  return s == Scheme::scheme1 ? "scheme1" : "scheme2";
+}
+inline std::string_view to_string(Strategy s) {  // layout.cpp:13-15
+  return s == Strategy::cyclic ? "cyclic" : "least_loaded";
+}
+inline std::string_view to_string(SchemePolicy p) {  // layout.cpp:17-23
+  return p == SchemePolicy::scheme1_only ? "s1-only"
+                                         : (p == SchemePolicy::scheme2_only ? "s2-only" : "adaptive");
+}
+
+// types.hpp:50-55: ceil(log2(extent)) with a 1-bit floor
+inline std::uint64_t index_bits(index_t extent) {
+  if (extent <= 2) return 1;
+  std::uint64_t v = static_cast<std::uint64_t>(extent) - 1, b = 0;
+  while (v) {
+    ++b;
+    v >>= 1;
+  }
+  return b;
+}
+
+// layout.hpp:66-86 — host-side report structs (no device work involved)
+struct MemoryEstimate {
+  std::uint64_t bits_per_element = 0;
+  std::uint64_t total_copy_bits = 0;
+  std::uint64_t total_copy_bytes = 0;
+  std::uint64_t factor_matrix_bytes = 0;
+  std::uint64_t storage_bytes_actual = 0;
+};
+
+struct BalanceMetrics {
+  std::size_t mode = 0;
+  Scheme scheme = Scheme::scheme1;
+  std::size_t kappa = 1;
+  std::vector<std::uint64_t> loads;
+  std::vector<std::uint64_t> owned_index_counts;
+  double max_over_mean = 1.0;
+  std::size_t empty_partitions = 0;
+};
+
+// layout.cpp:30-48
+inline MemoryEstimate estimate_memory_for(const Shape& shape, std::size_t nnz, std::size_t rank,
+                                          unsigned beta_float_bits) {
+  if (rank < 1) throw error("layout: rank must be at least 1");
+  if (beta_float_bits != 32 && beta_float_bits != 64)
+    throw error("layout: value width must be 32 or 64 bits");
+  MemoryEstimate m;
+  for (index_t e : shape.dims) m.bits_per_element += index_bits(e);
+  m.bits_per_element += beta_float_bits;
+  const std::uint64_t n = shape.mode_count();
+  m.total_copy_bits = n * static_cast<std::uint64_t>(nnz) * m.bits_per_element;
+  m.total_copy_bytes = (m.total_copy_bits + 7) / 8;
+  for (index_t e : shape.dims)
+    m.factor_matrix_bytes += static_cast<std::uint64_t>(e) * rank * (beta_float_bits / 8);
+  m.storage_bytes_actual =
+      n * static_cast<std::uint64_t>(nnz) * (n * sizeof(index_t) + beta_float_bits / 8);
+  return m;
+}
+
+template <typename T>
+MemoryEstimate estimate_memory(const SparseTensorCOO<T>& t, std::size_t rank,
+                               unsigned beta_float_bits = sizeof(T) * 8) {  // layout.hpp:151-155
+  return estimate_memory_for(t.shape(), t.nnz(), rank, beta_float_bits);
+}
+
+// layout.cpp:50-72
+inline BalanceMetrics balance_metrics(const ModePlan& plan, const DegreeProfile& profile) {
+  if (plan.mode != profile.mode)
+    throw error("layout: plan and degree profile describe different modes");
+  if (plan.nnz() != profile.total)
+    throw error("layout: plan and degree profile describe different tensors");
+  BalanceMetrics bm;
+  bm.mode = plan.mode;
+  bm.scheme = plan.scheme;
+  bm.kappa = plan.kappa;
+  for (std::size_t z = 0; z < plan.kappa; ++z) {
+    const std::uint64_t load = plan.partition_size(z);
+    bm.loads.push_back(load);
+    bm.empty_partitions += load == 0;
+  }
+  for (const auto& owned : plan.owned_indices) bm.owned_index_counts.push_back(owned.size());
+  const std::uint64_t max_load =
+      bm.loads.empty() ? 0 : *std::max_element(bm.loads.begin(), bm.loads.end());
+  const double mean = static_cast<double>(plan.nnz()) / static_cast<double>(plan.kappa);
+  bm.max_over_mean = plan.nnz() == 0 ? 1.0 : static_cast<double>(max_load) / mean;
+  return bm;
+}
+
+// mode_degrees read from a plan's own device copy (no second upload of the tensor)
+template <typename T>
+DegreeProfile plan_degrees(const SparseTensorCOO<T>& t, const ModePlan& plan) {
+  DegreeProfile p;
+  p.mode = plan.mode;
+  p.degrees.resize(t.extent(plan.mode));
+  detail::check(mk_mode_degrees(plan.device->ctx, static_cast<uint32_t>(plan.mode), p.degrees.data()));
+  p.total = plan.nnz();
   return p;
 }
 

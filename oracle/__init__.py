@@ -45,11 +45,12 @@ class _Lib:
         if not os.path.exists(self.path):
             raise FileNotFoundError(self.path)
         self.lib = C.CDLL(self.path)
-        self.lib[self.prefix + "last_error"].restype = C.c_char_p
+        # attribute access caches the function object (lib[...] builds a new one per call)
+        getattr(self.lib, self.prefix + "last_error").restype = C.c_char_p
 
     def _check(self, rc):
         if rc != 0:
-            raise OracleError(self.lib[self.prefix + "last_error"]().decode())
+            raise OracleError(getattr(self.lib, self.prefix + "last_error")().decode())
 
     def random_factors(self, dims, rank, seed):
         dims = _dims(dims)
@@ -232,6 +233,44 @@ class Reference(_Lib):
                           "owned": owned[base:base + int(oo[-1])], "owned_offsets": oo})
             base += int(dims[d])
         return plans, plan_ms.value
+
+    def frostt_parse(self, text, prec=32, merge=True, dims_override=None, max_modes=16):
+        """parse_frostt<T> (frostt.hpp:74-160): (dims, coords, values, duplicates_merged)."""
+        raw = text.encode() if isinstance(text, str) else bytes(text)
+        cap = raw.count(b"\n") + 1
+        ovr = np.asarray(dims_override if dims_override else [0], dtype=np.uint32)
+        n, nnz, dups = C.c_uint32(), C.c_uint64(), C.c_uint64()
+        dims = np.zeros(max_modes, dtype=np.uint32)
+        coords = np.empty(cap * max_modes, dtype=np.uint32)
+        vals = np.empty(cap, dtype=np.float64 if prec == 64 else np.float32)
+        f = self.lib.ref_frostt_parse
+        f.argtypes = [C.c_char_p, C.c_uint64, C.c_int, C.c_int, C.c_void_p, C.c_uint32,
+                      C.c_uint64, C.c_uint32, C.POINTER(C.c_uint32), C.c_void_p,
+                      C.POINTER(C.c_uint64), C.POINTER(C.c_uint64), C.c_void_p, C.c_void_p]
+        self._check(f(raw, len(raw), prec, 1 if merge else 0, ovr.ctypes.data,
+                      len(dims_override) if dims_override else 0, cap, max_modes,
+                      C.byref(n), dims.ctypes.data, C.byref(nnz), C.byref(dups),
+                      coords.ctypes.data, vals.ctypes.data))
+        k, m = n.value, nnz.value
+        return (dims[:k].tolist(), coords[:m * k].reshape(m, k).copy(), vals[:m].copy(),
+                dups.value)
+
+    def frostt_write(self, dims, coords, values):
+        """write_frostt_string (frostt.hpp:165-192) of a tensor (fp32 or fp64 values)."""
+        dims = _dims(dims)
+        coords = np.ascontiguousarray(coords, dtype=np.uint32).reshape(-1)
+        prec = 64 if np.asarray(values).dtype == np.float64 else 32
+        values = np.ascontiguousarray(values, dtype=np.float64 if prec == 64 else np.float32)
+        nnz = values.size
+        cap = nnz * (len(dims) * 11 + 32) + 1
+        out = C.create_string_buffer(cap)
+        ln = C.c_uint64()
+        f = self.lib.ref_frostt_write
+        f.argtypes = [C.c_uint32, _u32p, C.c_uint64, C.c_void_p, C.c_void_p, C.c_int,
+                      C.c_char_p, C.c_uint64, C.POINTER(C.c_uint64)]
+        self._check(f(len(dims), dims, nnz, coords.ctypes.data, values.ctypes.data, prec, out,
+                      cap, C.byref(ln)))
+        return out.raw[:ln.value].decode()
 
     def run_timed_plans(self, dims, coords, values, factors, kappa, plans, iters, batch_p=32):
         """The reference's run_timed (kernel.hpp:239-287) on given plans (list of build_plan

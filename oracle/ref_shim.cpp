@@ -17,6 +17,7 @@
 #include <vector>
 
 #include "mttkrp/factor.hpp"
+#include "mttkrp/frostt.hpp"
 #include "mttkrp/kernel.hpp"
 #include "mttkrp/layout.hpp"
 #include "mttkrp/oracle.hpp"
@@ -274,6 +275,55 @@ int ref_run_timed(uint32_t n, const uint32_t* dims, uint64_t nnz, const uint32_t
       total_ms_per_iter[i] = run.report.total_ms[i];
     for (std::size_t d = 0; d < run.report.modes.size(); ++d)
       mode_min_ms[d] = run.report.modes[d].min_ms;
+  });
+}
+
+// The reference's FROSTT parser (frostt.hpp:74-160) on a text buffer.  Outputs go to caller
+// buffers sized for `cap` elements of up to `max_modes` modes; returns the element count.
+int ref_frostt_parse(const char* text, uint64_t len, int prec, int merge,
+                     const uint32_t* dims_override, uint32_t n_override, uint64_t cap,
+                     uint32_t max_modes, uint32_t* n_out, uint32_t* dims_out, uint64_t* nnz_out,
+                     uint64_t* dups_out, uint32_t* coords_out, void* values_out) {
+  return guarded([&] {
+    FrosttOptions opt;
+    opt.merge_duplicates = merge != 0;
+    if (n_override) opt.dims_override.assign(dims_override, dims_override + n_override);
+    auto emit = [&](const auto& res) {
+      const auto& t = res.tensor;
+      if (t.nnz() > cap || t.mode_count() > max_modes) throw error("shim: buffer too small");
+      *n_out = static_cast<uint32_t>(t.mode_count());
+      for (std::size_t h = 0; h < t.mode_count(); ++h) dims_out[h] = t.extent(h);
+      *nnz_out = t.nnz();
+      *dups_out = res.duplicates_merged;
+      using V = typename std::decay_t<decltype(t)>::value_type;
+      for (std::size_t i = 0; i < t.nnz(); ++i) {
+        auto c = t.coords(i);
+        std::memcpy(coords_out + i * t.mode_count(), c.data(), t.mode_count() * sizeof(uint32_t));
+        static_cast<V*>(values_out)[i] = t.value(i);
+      }
+    };
+    const std::string_view sv(text, len);
+    if (prec == 64) emit(parse_frostt<double>(sv, opt));
+    else emit(parse_frostt<float>(sv, opt));
+  });
+}
+
+// The reference's writer (frostt.hpp:165-192); returns the byte length, copies up to cap.
+int ref_frostt_write(uint32_t n, const uint32_t* dims, uint64_t nnz, const uint32_t* coords,
+                     const void* values, int prec, char* out, uint64_t cap, uint64_t* len) {
+  return guarded([&] {
+    auto go = [&](auto tag) {
+      using V = decltype(tag);
+      std::vector<index_t> d(dims, dims + n);
+      std::vector<index_t> c(coords, coords + nnz * n);
+      std::vector<V> v(static_cast<const V*>(values), static_cast<const V*>(values) + nnz);
+      auto t = SparseTensorCOO<V>::from_parts(Shape(d), std::move(c), std::move(v));
+      const std::string s = write_frostt_string(t);
+      *len = s.size();
+      std::memcpy(out, s.data(), std::min<uint64_t>(cap, s.size()));
+    };
+    if (prec == 64) go(double{});
+    else go(float{});
   });
 }
 

@@ -16,6 +16,9 @@ mttkrp_mode                            mttkrp_mode (kernel.hpp:161-169)
 mttkrp_all_modes                       mttkrp_all_modes (kernel.hpp:177-197)
 run_timed                              run_timed (kernel.hpp:239-287)
 verify_against / verify_tolerance      verify_against / verify_tolerance (verify.hpp)
+parse_frostt / read_frostt_file        parse_frostt / read_frostt_file (frostt.hpp:74-199)
+write_frostt(_string/_file)            write_frostt_string / write_frostt_file (:165-206)
+(absent)                               save/load_tensor_cache, load_tensor (binary cache)
 (absent, SPEC.md:13)                   cpd_als / Context.cpd_als_iter
 =====================================  ===============================================
 
@@ -30,7 +33,7 @@ import enum
 import os
 import threading
 from dataclasses import dataclass, field
-from typing import List, Optional, Sequence
+from typing import List, Optional, Sequence, Tuple
 
 import numpy as np
 
@@ -39,7 +42,9 @@ __all__ = [
     "FactorMatrix", "ModePlan", "Context", "build_mode_plans", "mttkrp_mode",
     "mttkrp_all_modes", "run_timed", "generate_synthetic", "generate_powerlaw",
     "random_factors", "verify_against", "verify_tolerance", "mode_degrees", "cpd_als",
-    "element_update",
+    "element_update", "FrosttOptions", "FrosttParseResult", "parse_frostt", "read_frostt_file",
+    "write_frostt_string", "write_frostt_file", "save_tensor_cache", "load_tensor_cache",
+    "load_tensor",
     "load_library", "library_path", "EXPORTED_SYMBOLS",
 ]
 
@@ -50,7 +55,7 @@ MK_OK, MK_EINVAL, MK_ENOMEM, MK_ECUDA, MK_ENONFINITE, MK_ESTATE, MK_ENCCL = rang
 EXEC_FAST, EXEC_DETERMINISTIC = 0, 1
 
 EXPORTED_SYMBOLS = [
-    "mk_last_error", "mk_version", "mk_device_count", "mk_create", "mk_destroy",
+    "mk_last_error", "mk_version", "mk_device_count", "mk_device_sm_count", "mk_create", "mk_destroy",
     "mk_set_stream", "mk_synchronize", "mk_tensor_upload", "mk_tensor_norm2",
     "mk_build_plans", "mk_get_plan_info", "mk_fast_path_info", "mk_set_fast_kernel", "mk_plan_export", "mk_mode_degrees",
     "mk_copy_export", "mk_factors_upload", "mk_factor_upload", "mk_factor_download",
@@ -62,6 +67,9 @@ EXPORTED_SYMBOLS = [
     "mk_als_update_mode", "mk_als_fit", "mk_output_device_ptr",
     "mk_tensor_upload_f64", "mk_factors_upload_f64", "mk_mttkrp_mode_f64",
     "mk_mttkrp_all_modes_f64", "mk_random_factors_f64", "mk_generate_synthetic_f64",
+    "mk_frostt_parse", "mk_frostt_read_file", "mk_host_tensor_info", "mk_host_tensor_export",
+    "mk_host_tensor_free", "mk_frostt_format", "mk_frostt_write_file", "mk_tensor_cache_write",
+    "mk_tensor_cache_read",
 ]
 
 
@@ -137,6 +145,7 @@ def load_library() -> C.CDLL:
             "mk_last_error": (C.c_char_p, []),
             "mk_version": (C.c_char_p, []),
             "mk_device_count": (i32, [P(i32)]),
+            "mk_device_sm_count": (i32, [i32, P(i32)]),
             "mk_create": (i32, [i32, P(vp)]),
             "mk_destroy": (i32, [vp]),
             "mk_set_stream": (i32, [vp, vp]),
@@ -181,6 +190,15 @@ def load_library() -> C.CDLL:
             "mk_mttkrp_all_modes_f64": (i32, [vp, i32, i32, vp]),
             "mk_random_factors_f64": (i32, [u32, vp, u64, u64, vp]),
             "mk_generate_synthetic_f64": (i32, [u32, vp, u64, i32, u64, u64, u64, vp, vp]),
+            "mk_frostt_parse": (i32, [C.c_char_p, u64, i32, i32, vp, u32, u32, P(vp)]),
+            "mk_frostt_read_file": (i32, [C.c_char_p, i32, i32, vp, u32, u32, P(vp)]),
+            "mk_host_tensor_info": (i32, [vp, P(u32), vp, u32, P(u64), P(u64), P(i32)]),
+            "mk_host_tensor_export": (i32, [vp, vp, vp]),
+            "mk_host_tensor_free": (i32, [vp]),
+            "mk_frostt_format": (i32, [u32, u64, vp, vp, i32, u32, vp, u64, P(u64)]),
+            "mk_frostt_write_file": (i32, [C.c_char_p, u32, u64, vp, vp, i32, u32]),
+            "mk_tensor_cache_write": (i32, [C.c_char_p, u32, vp, u64, vp, vp, i32]),
+            "mk_tensor_cache_read": (i32, [C.c_char_p, P(vp)]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(lib, name)
@@ -803,6 +821,132 @@ def random_factors(dims, rank, seed, dtype=np.float32) -> List[FactorMatrix]:
     gen = lib.mk_random_factors_f64 if f64 else lib.mk_random_factors
     _check(gen(len(dims), _ptr(d), rank, seed, _ptr_array(mats)))
     return [FactorMatrix(i, m) for i, m in enumerate(mats)]
+
+
+@dataclass
+class FrosttOptions:  # frostt.hpp:22-29
+    merge_duplicates: bool = True
+    dims_override: Optional[Sequence[int]] = None
+
+
+@dataclass
+class FrosttParseResult:  # frostt.hpp:31-35
+    tensor: SparseTensorCOO
+    duplicates_merged: int = 0
+
+
+def _prec_of(dtype) -> int:
+    return 64 if np.dtype(dtype) == np.float64 else 32
+
+
+def _take_host_tensor(handle) -> Tuple[SparseTensorCOO, int]:
+    lib = load_library()
+    try:
+        n, nnz, dups, prec = C.c_uint32(), C.c_uint64(), C.c_uint64(), C.c_int()
+        dims = np.zeros(64, dtype=np.uint32)
+        _check(lib.mk_host_tensor_info(handle, C.byref(n), _ptr(dims), 64, C.byref(nnz),
+                                       C.byref(dups), C.byref(prec)))
+        coords = np.empty((nnz.value, n.value), dtype=np.uint32)
+        vals = np.empty(nnz.value, dtype=np.float64 if prec.value == 64 else np.float32)
+        _check(lib.mk_host_tensor_export(handle, _ptr(coords), _ptr(vals)))
+    finally:
+        lib.mk_host_tensor_free(handle)
+    # the parser already validated bounds (inferred or checked extents) and finiteness
+    return SparseTensorCOO([int(x) for x in dims[:n.value]], coords, vals,
+                           validate=False), int(dups.value)
+
+
+def _override_args(opt: Optional[FrosttOptions]):
+    ovr = None if opt is None or not opt.dims_override else \
+        np.asarray(opt.dims_override, dtype=np.uint32)
+    merge = 1 if opt is None or opt.merge_duplicates else 0
+    return merge, (None if ovr is None else _ptr(ovr)), (0 if ovr is None else ovr.size), ovr
+
+
+def parse_frostt(text, options: Optional[FrosttOptions] = None, dtype=np.float32,
+                 threads: int = 0) -> FrosttParseResult:
+    """frostt.hpp:74-160 parse_frostt<T> on a string (multithreaded host C++)."""
+    lib = load_library()
+    raw = text.encode() if isinstance(text, str) else bytes(text)
+    merge, op, on, _keep = _override_args(options)
+    h = C.c_void_p()
+    _check(lib.mk_frostt_parse(raw, len(raw), _prec_of(dtype), merge, op, on, threads,
+                               C.byref(h)))
+    t, dups = _take_host_tensor(h)
+    return FrosttParseResult(t, dups)
+
+
+def read_frostt_file(path, options: Optional[FrosttOptions] = None, dtype=np.float32,
+                     threads: int = 0) -> FrosttParseResult:
+    """frostt.hpp:194-199 read_frostt_file<T>."""
+    lib = load_library()
+    merge, op, on, _keep = _override_args(options)
+    h = C.c_void_p()
+    _check(lib.mk_frostt_read_file(os.fsencode(path), _prec_of(dtype), merge, op, on, threads,
+                                   C.byref(h)))
+    t, dups = _take_host_tensor(h)
+    return FrosttParseResult(t, dups)
+
+
+def _value_prec(t: SparseTensorCOO) -> int:
+    return 64 if t.values.dtype == np.float64 else 32
+
+
+def write_frostt_string(t: SparseTensorCOO, threads: int = 0) -> str:
+    """frostt.hpp:165-192 write_frostt / write_frostt_string."""
+    lib = load_library()
+    n = C.c_uint64()
+    _check(lib.mk_frostt_format(t.mode_count(), t.nnz, _ptr(t.coords), _ptr(t.values),
+                                _value_prec(t), threads, None, 0, C.byref(n)))
+    buf = C.create_string_buffer(max(n.value, 1))
+    _check(lib.mk_frostt_format(t.mode_count(), t.nnz, _ptr(t.coords), _ptr(t.values),
+                                _value_prec(t), threads, buf, n.value, C.byref(n)))
+    return buf.raw[:n.value].decode()
+
+
+def write_frostt_file(t: SparseTensorCOO, path, threads: int = 0) -> None:
+    """frostt.hpp:201-206 write_frostt_file."""
+    _check(load_library().mk_frostt_write_file(os.fsencode(path), t.mode_count(), t.nnz,
+                                               _ptr(t.coords), _ptr(t.values), _value_prec(t),
+                                               threads))
+
+
+def save_tensor_cache(t: SparseTensorCOO, path) -> None:
+    """Binary tensor cache ("MKBT" v1, checksummed AoS coordinates + values)."""
+    d = np.asarray(t.dims, dtype=np.uint32)
+    _check(load_library().mk_tensor_cache_write(os.fsencode(path), t.mode_count(), _ptr(d),
+                                                t.nnz, _ptr(t.coords), _ptr(t.values),
+                                                _value_prec(t)))
+
+
+def load_tensor_cache(path) -> SparseTensorCOO:
+    h = C.c_void_p()
+    _check(load_library().mk_tensor_cache_read(os.fsencode(path), C.byref(h)))
+    return _take_host_tensor(h)[0]
+
+
+def load_tensor(path, options: Optional[FrosttOptions] = None, dtype=np.float32,
+                cache: bool = True) -> FrosttParseResult:
+    """A FROSTT file through the binary cache `<path>.mkbt`: the cache is used when it is
+    newer than the text and was written with the same precision (else the text is parsed
+    and the cache rewritten).  The cache stores the parse result, so duplicates_merged of a
+    cached load is reported as 0."""
+    cpath = os.fspath(path) + ".mkbt"
+    if cache and options is None and os.path.exists(cpath) and \
+            os.path.getmtime(cpath) >= os.path.getmtime(path):
+        try:
+            t = load_tensor_cache(cpath)
+            if t.values.dtype == np.dtype(dtype):
+                return FrosttParseResult(t, 0)
+        except MttkrpError:
+            pass  # stale or corrupt cache: re-parse below
+    res = read_frostt_file(path, options, dtype)
+    if cache and options is None:
+        try:
+            save_tensor_cache(res.tensor, cpath)
+        except MttkrpError:
+            pass  # read-only location: the parse result is still returned
+    return res
 
 
 def shard_cuts(row_ptr, world: int) -> np.ndarray:

@@ -130,6 +130,13 @@ int mk_device_count(int* count) {
   return guarded([&] { MKB_CUDA(cudaGetDeviceCount(count)); });
 }
 
+int mk_device_sm_count(int device, int* sms) {
+  return guarded([&] {
+    if (!sms) fail(MK_EINVAL, "null output");
+    MKB_CUDA(cudaDeviceGetAttribute(sms, cudaDevAttrMultiProcessorCount, device));
+  });
+}
+
 int mk_create(int device, mk_context** out) {
   return guarded([&] {
     if (!out) fail(MK_EINVAL, "null output");

@@ -8,6 +8,7 @@
 #include <string>
 #include <vector>
 
+#include "mttkrp_b200/frostt.hpp"
 #include "mttkrp_b200/mttkrp.hpp"
 
 namespace mttkrp = mttkrp_b200;
@@ -218,11 +219,51 @@ void fp64_path() {  // T = double: deterministic == oracle_mttkrp<double> order 
   CHECK(rng::bounded(g, 10) == rng::bounded(g2, 10));
 }
 
+// test_frostt.cpp:8-100 through the drop-in frostt.hpp (host ingest, no device work)
+void frostt_cases() {
+  auto res = parse_frostt<float>("1 1 1 2.0\n2 2 2 3.0\n");
+  CHECK(res.tensor.shape().dims == std::vector<index_t>({2, 2, 2}));
+  CHECK(res.tensor.nnz() == 2 && res.tensor.value(1) == 3.0f && res.tensor.index(1, 2) == 1);
+  auto merged = parse_frostt<float>("1 1 1 2.0\n1 1 1 3.0\n");
+  CHECK(merged.tensor.nnz() == 1 && merged.tensor.value(0) == 5.0f && merged.duplicates_merged == 1);
+  FrosttOptions strict;
+  strict.merge_duplicates = false;
+  CHECK_THROWS(parse_frostt<float>("1 1 1 2.0\n1 1 1 3.0\n", strict));
+  auto sci = parse_frostt<double>("# header comment\n\n  \n1 2 1.5e2\n#tail\n2 1 -3e-1\n");
+  CHECK(sci.tensor.value(0) == 150.0 && sci.tensor.value(1) == -0.3);
+  for (const char* bad : {"", "# comments only\n\n", "1 1 1 1\n1 1 1\n", "1 x 1 1\n",
+                          "1 1 1 abc\n", "0 1 1 1\n", "1\n", "1 1 1 inf\n",
+                          "5000000000 1 1 1\n"})
+    CHECK_THROWS(parse_frostt<float>(bad));
+  try {
+    (void)parse_frostt<float>("1 1 1 1\n1 1 1\n");
+  } catch (const error& e) {
+    CHECK(std::string(e.what()).find("line 2") != std::string::npos);
+  }
+  FrosttOptions ovr;
+  ovr.dims_override = {4, 4, 4};
+  CHECK(parse_frostt<float>("1 1 1 1\n", ovr).tensor.shape().dims == std::vector<index_t>({4, 4, 4}));
+  SparseTensorCOO<double> u(Shape({2, 3}));
+  u.add({1, 2}, 0.1);
+  u.add({0, 0}, -1e30);
+  CHECK(write_frostt_string(u) == "2 3 0.1\n1 1 -1e+30\n");
+  auto g = generate_synthetic<float>(SyntheticSpec{{30, 20, 10}, 400, SyntheticDist::uniform, 0, 2, 3});
+  FrosttOptions exact;
+  exact.merge_duplicates = false;
+  exact.dims_override = g.shape().dims;
+  CHECK(parse_frostt<float>(write_frostt_string(g), exact).tensor == g);
+  const char* path = "/tmp/mkb_dropin_cache.mkbt";
+  save_tensor_cache(g, path);
+  CHECK(load_tensor_cache<float>(path) == g);
+  std::remove(path);
+}
+
 int main() {
   const std::vector<std::pair<const char*, std::function<void()>>> cases = {
       {"single nonzero", single_nonzero}, {"partition KATs", partition_kats},
       {"adaptive selection", adaptive_selection}, {"determinism & chain", determinism_and_chain},
-      {"errors", errors}, {"element_update", element_updates}, {"fp64 path", fp64_path}};
+      {"errors", errors}, {"element_update", element_updates}, {"fp64 path", fp64_path},
+      {"frostt I/O", frostt_cases}};
   for (auto& [name, fn] : cases) {
     const int before = g_fail;
     try {
