@@ -43,6 +43,10 @@ enum {
   MK_EXEC_DETERMINISTIC = 1, /* one owner per output row, element order, no FMA:
                                 bitwise equal to ExecConfig{deterministic=true}
                                 (kernel.hpp:26-28) and to oracle_mttkrp (oracle.hpp:20-43) */
+  MK_EXEC_PARTITIONED = 2,   /* the reference's work split: partition z of the plan on CTA z
+                                (for_each_partition, parallel.hpp:16-49; Algorithm 2), atomics
+                                only where Scheme 2 partitions or the CTA-internal split cut a
+                                row; the GPU form of the paper's scheme ablation (fp32 only) */
 };
 
 typedef struct mk_context mk_context;

@@ -504,6 +504,10 @@ struct ExecConfig {
   std::size_t kappa = 1;
   std::size_t batch_p = 32;
   bool deterministic = false;
+  bool partitioned = false;  // MK_EXEC_PARTITIONED: the reference's partition-per-worker split
+  int exec_code() const {
+    return deterministic ? MK_EXEC_DETERMINISTIC : (partitioned ? MK_EXEC_PARTITIONED : MK_EXEC_FAST);
+  }
   void validate() const {
     if (kappa < 1) throw error("kernel: kappa must be at least 1");
     if (batch_p < 1) throw error("kernel: batch size P must be at least 1");
@@ -596,9 +600,10 @@ FactorMatrix<T> mttkrp_mode(const SparseTensorCOO<T>& t, const ModePlan& plan,
   detail::validate_plan(t, plan, config);
   detail::upload_factors(*plan.device, factors);
   auto out = FactorMatrix<T>::zeros(plan.mode, t.extent(plan.mode), factors[0].rank);
-  detail::check(detail::mode_call<T>(plan.device->ctx, static_cast<uint32_t>(plan.mode),
-                                     config.deterministic ? MK_EXEC_DETERMINISTIC : MK_EXEC_FAST,
-                                     out.data.data()));
+  detail::check(detail::mode_call<T>(
+      plan.device->ctx, static_cast<uint32_t>(plan.mode),
+      std::is_same_v<T, double> && !config.deterministic ? MK_EXEC_FAST : config.exec_code(),
+      out.data.data()));
   return out;
 }
 
@@ -620,7 +625,8 @@ std::vector<FactorMatrix<T>> mttkrp_all_modes(const SparseTensorCOO<T>& t,
   for (std::size_t d = 0; d < plans.size(); ++d)
     outs.push_back(FactorMatrix<T>::zeros(d, t.extent(d), factors[0].rank));
   for (auto& o : outs) ptr.push_back(o.data.data());
-  const int exec = config.deterministic ? MK_EXEC_DETERMINISTIC : MK_EXEC_FAST;
+  const int exec = std::is_same_v<T, double> && !config.deterministic ? MK_EXEC_FAST
+                                                                       : config.exec_code();
   if constexpr (std::is_same_v<T, double>)
     detail::check(mk_mttkrp_all_modes_f64(plans[0].device->ctx, chain_outputs ? 1 : 0, exec,
                                           ptr.data()));
@@ -721,7 +727,7 @@ TimedRun<T> run_timed(const SparseTensorCOO<T>& t, const std::vector<ModePlan>& 
     return run;
   } else {
   detail::check(mk_run_timed(plans[0].device->ctx, iters,
-                             config.deterministic ? MK_EXEC_DETERMINISTIC : MK_EXEC_FAST, 1,
+                             config.exec_code(), 1,
                              mode_ms.data(), total.data(), &same));
   TimedRun<T> run;
   run.report.iters = iters;

@@ -52,7 +52,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 _LIB_NAME = "libmttkrp_b200.so"
 
 MK_OK, MK_EINVAL, MK_ENOMEM, MK_ECUDA, MK_ENONFINITE, MK_ESTATE, MK_ENCCL = range(7)
-EXEC_FAST, EXEC_DETERMINISTIC = 0, 1
+EXEC_FAST, EXEC_DETERMINISTIC, EXEC_PARTITIONED = 0, 1, 2
 
 EXPORTED_SYMBOLS = [
     "mk_last_error", "mk_version", "mk_device_count", "mk_device_sm_count", "mk_create", "mk_destroy",
@@ -322,6 +322,14 @@ class ExecConfig:
     kappa: int = 1
     batch_p: int = 32
     deterministic: bool = False
+    # the reference's work split on the GPU (partition z of the plan on CTA z; the paper's
+    # scheme ablation, MK_EXEC_PARTITIONED); no reference counterpart flag
+    partitioned: bool = False
+
+    def exec_code(self) -> int:
+        if self.deterministic:
+            return EXEC_DETERMINISTIC
+        return EXEC_PARTITIONED if self.partitioned else EXEC_FAST
 
     def validate(self):
         if self.kappa < 1:
@@ -682,7 +690,7 @@ def mttkrp_mode(t: SparseTensorCOO, plan: ModePlan, factors, config: ExecConfig)
         ctx.upload_factors_f64([f.data for f in factors])
         return FactorMatrix(plan.mode, ctx.mttkrp_mode_f64(plan.mode, config.deterministic))
     _upload_if_changed(ctx, factors)
-    return FactorMatrix(plan.mode, ctx.mttkrp_mode(plan.mode, config.deterministic))
+    return FactorMatrix(plan.mode, ctx.mttkrp_mode(plan.mode, config.exec_code()))
 
 
 def mttkrp_all_modes(t: SparseTensorCOO, plans: Sequence[ModePlan], factors, config: ExecConfig,
@@ -704,7 +712,7 @@ def mttkrp_all_modes(t: SparseTensorCOO, plans: Sequence[ModePlan], factors, con
         outs = ctx.mttkrp_all_modes_f64(chain_outputs, config.deterministic)
         return [FactorMatrix(d, o) for d, o in enumerate(outs)]
     _upload_if_changed(ctx, factors)
-    outs = ctx.mttkrp_all_modes(chain_outputs, config.deterministic)
+    outs = ctx.mttkrp_all_modes(chain_outputs, config.exec_code())
     return [FactorMatrix(d, o) for d, o in enumerate(outs)]
 
 
@@ -757,7 +765,7 @@ def run_timed(t: SparseTensorCOO, plans: Sequence[ModePlan], factors, config: Ex
         _validate_plan(t, p, config)
     ctx = plans[0]._ctx
     _upload_if_changed(ctx, factors)
-    mode_ms, total = ctx.run_timed(iters, config.deterministic, flush_l2)
+    mode_ms, total = ctx.run_timed(iters, config.exec_code(), flush_l2)
     modes = []
     for d, p in enumerate(plans):
         sizes = [p.partition_size(z) for z in range(p.kappa)]

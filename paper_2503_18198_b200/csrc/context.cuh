@@ -42,6 +42,10 @@ struct ModeCopy {
   std::vector<uint64_t> partition_offsets;  // kappa+1 (host)
   std::vector<uint64_t> owned_offsets;      // kappa+1 (host); rows = row_seq[...]
   DevBuf<uint32_t> degrees;                 // extent
+  // partitioned executor (mttkrp.cu launch_partitioned): per-lane-group tile bounds
+  DevBuf<uint64_t> part_tiles;
+  uint32_t part_gpb = 0;
+  uint64_t part_tiles_kappa = 0;
   // packed element records for the streaming kernel (stream.cu): part A 16 B/element,
   // part B 0/4/8/16 B/element; padded to a multiple of 4 elements
   DevBuf<uint32_t> recA, recB;

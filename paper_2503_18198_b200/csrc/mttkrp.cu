@@ -45,6 +45,7 @@ struct MttkrpArgs {
   unsigned long long tag;         // mode << 32
   uint64_t nnz;       // total elements of the copy
   uint64_t e0, e1;    // owned element range (whole copy unless sharded)
+  const uint64_t* tile_bounds;  // partitioned executor: tile t = [tb[t], tb[t+1]) (else null)
   uint32_t k0;        // first owned copy row (deterministic kernel)
   uint32_t rank;
   uint32_t tile;
@@ -158,8 +159,15 @@ __global__ void __launch_bounds__(256) k_mttkrp_tiles(const MttkrpArgs a) {
   const uint32_t gid = (blockIdx.x * blockDim.x + threadIdx.x) / G;
 
   for (uint32_t t = gid; t < a.ntiles; t += groups) {
-    const uint64_t ta = a.e0 + static_cast<uint64_t>(t) * a.tile;
-    const uint64_t tb = min(ta + a.tile, a.e1);
+    uint64_t ta, tb;
+    if (a.tile_bounds) {  // partitioned executor: tiles inside partition blockIdx.x
+      ta = __ldg(a.tile_bounds + t);
+      tb = __ldg(a.tile_bounds + t + 1);
+      if (ta >= tb) continue;
+    } else {
+      ta = a.e0 + static_cast<uint64_t>(t) * a.tile;
+      tb = min(ta + a.tile, a.e1);
+    }
     const bool head_split = ta > 0 && __ldg(a.out_idx + ta - 1) == __ldg(a.out_idx + ta);
     const bool tail_split = tb < a.nnz && __ldg(a.out_idx + tb) == __ldg(a.out_idx + tb - 1);
     uint32_t cur = __ldg(a.out_idx + ta);
@@ -312,8 +320,44 @@ __global__ void k_zero_rows(float* __restrict__ out, uint32_t R,
 
 __global__ void k_init_nonfinite(unsigned long long* p) { *p = ~0ull; }
 
+// Partitioned executor (MK_EXEC_PARTITIONED): the reference's work split on the GPU —
+// Algorithm 2 with partition z of the plan (partition_offsets[z..z+1],
+// layout.cpp:141-183) processed by CTA z, as for_each_partition hands partition z to one
+// worker (parallel.hpp:16-49).  Inside the CTA the partition is cut into one contiguous
+// sub-range per lane group.  Scheme 1 partitions own their rows, so only rows cut by the
+// CTA-internal split are added atomically; Scheme 2 partitions also share the rows that
+// straddle partition boundaries (Global_Update).  The output is zeroed first (memset).
+// This is the paper's load-balancing experiment (§V-B) on B200, not the fast path: the
+// fast executors split every copy into equal-nnz slices regardless of the scheme.
+template <int NI, int VEC, int G, int KREP>
+void launch_partitioned(Context& c, MttkrpArgs a, ModeCopy& mc, uint32_t mode) {
+  cudaStream_t st = c.stream;
+  constexpr uint32_t gpb = 256 / G;
+  if (mc.part_gpb != gpb || mc.part_tiles_kappa != mc.kappa) {
+    std::vector<uint64_t> tb(mc.kappa * gpb + 1);
+    for (uint64_t z = 0; z < mc.kappa; ++z) {
+      const uint64_t p0 = mc.partition_offsets[z], p1 = mc.partition_offsets[z + 1];
+      for (uint32_t g = 0; g < gpb; ++g) tb[z * gpb + g] = p0 + (p1 - p0) * g / gpb;
+    }
+    tb.back() = mc.partition_offsets[mc.kappa];
+    mc.part_tiles.resize(tb.size());
+    MKB_CUDA(cudaMemcpyAsync(mc.part_tiles.get(), tb.data(), tb.size() * sizeof(uint64_t),
+                             cudaMemcpyHostToDevice, st));
+    MKB_CUDA(cudaStreamSynchronize(st));
+    mc.part_gpb = gpb;
+    mc.part_tiles_kappa = mc.kappa;
+  }
+  MKB_CUDA(cudaMemsetAsync(a.out, 0, static_cast<size_t>(c.dims[mode]) * a.rank * sizeof(float), st));
+  if (c.nnz == 0) return;
+  a.tile_bounds = mc.part_tiles.get();
+  a.ntiles = static_cast<uint32_t>(mc.kappa * gpb);
+  k_mttkrp_tiles<NI, VEC, G, KREP><<<static_cast<unsigned>(mc.kappa), 256, 0, st>>>(a);
+  MKB_LAUNCH();
+}
+
 template <int NI, int VEC, int G, int KREP>
 void launch_cfg(Context& c, const MttkrpArgs& a, ModeCopy& mc, uint32_t mode, int exec) {
+  if (exec == MK_EXEC_PARTITIONED) return launch_partitioned<NI, VEC, G, KREP>(c, a, mc, mode);
   cudaStream_t st = c.stream;
   const int per_block = 256 / G;
   ModeCopy::ZeroList& zl = mc.zl_tiles;
