@@ -287,9 +287,9 @@ def run_config(args, name, rank, world, local_rank, stream, with_cpu):
     b_iter = float(sum(algorithmic_bytes(dims, t.nnz, R, distinct)))
 
     ex = None
-    if world > 1:
-        from paper_2503_18198_b200.distributed import ShardExchange
-        ex = ShardExchange(ctx, R, dims, device=dev)
+    if world > 1:  # NCCL inside the library (comm.cu): sharded sweep captured in a CUDA graph
+        from paper_2503_18198_b200.distributed import NcclExchange
+        ex = NcclExchange(ctx)
 
     def sweep_once():
         if ex is not None:
@@ -330,7 +330,7 @@ def run_config(args, name, rank, world, local_rank, stream, with_cpu):
         torch.cuda.synchronize()
         wall = (time.perf_counter() - w0) * 1e3
     ctx.synchronize()  # non-finite check of the timed sweeps
-    fused = ex is None and ctx.last_sweep_fused()
+    fused = ctx.last_sweep_fused()  # sharded: the local part of every rank's sweep
     step_ms = [evf[s][0].elapsed_time(evf[s][1]) for s in range(args.steps)]
     ms = float(np.mean(step_ms))
     if world > 1:
@@ -453,7 +453,7 @@ def run_config(args, name, rank, world, local_rank, stream, with_cpu):
                 "d2h_bytes_per_step": h2d, "path": "mk_sweep_host (C ABI), pinned host buffers",
                 "pageable_per_mode_ms": e2e_pageable_ms},
         "gpu_launches": (launches_per_sweep + (2 * n if ex is not None else 0)) * args.steps,
-        "allgather_bytes_per_sweep": ex.bytes_per_sweep() if ex is not None else 0,
+        "allgather_bytes_per_sweep": ex.bytes_per_sweep(R, n) if ex is not None else 0,
         "clocks": clk.summary(),
         "per_mode_ms": mode_ms.mean(axis=0).tolist(),
         "fused_sweep": bool(fused),

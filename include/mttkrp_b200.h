@@ -177,22 +177,46 @@ int mk_cpd_als_iter(mk_context* ctx, double* fit, float* lambda);
 int mk_cpd_als(mk_context* ctx, uint64_t max_iters, double tol, double* fit,
                uint64_t* iters_done, float* lambda);
 
-/* ---- multi-GPU row-range shards (no reference counterpart) ---------------
- * Rank `rank` of `world` owns, in every mode copy, the copy rows [k_rank, k_rank+1) with
- * k_r = first copy row starting at or after floor(r * nnz / world).  Subsequent fast and
- * deterministic MTTKRP calls compute only the owned rows.  world = 1 restores the full copy. */
+/* ---- multi-GPU shards of the mode copies (no reference counterpart) --------
+ * Rank `rank` of `world` owns, in every mode copy, the element range [e_rank, e_rank+1)
+ * (mk_shard_split: nnz-balanced cuts moved to the next row start, except inside a heavy row
+ * of more than nnz/(8 world) elements, which is split between ranks).  It touches the copy
+ * rows [k0, k1) — whole rows plus at most one partial row at each end.  Subsequent fast,
+ * deterministic and fp64 MTTKRP calls compute only the owned elements.  world = 1 restores
+ * the full copy. */
 int mk_set_shard(mk_context* ctx, uint32_t rank, uint32_t world);
-/* Copy-row range [k0, k1) owned by `rank` in `mode` (any rank of the current world). */
+/* Copy rows [k0, k1) touched by `rank` in `mode` (any rank of the current world). */
 int mk_shard_rows(mk_context* ctx, uint32_t mode, uint32_t rank, uint64_t* k0, uint64_t* k1);
-/* Pack this rank's output rows of `mode` (copy-row order, R floats each) into dst (device). */
+/* Element range [e0, e1) and touched copy rows [k0, k1) of `rank` (NULL outputs skipped). */
+int mk_shard_range(mk_context* ctx, uint32_t mode, uint32_t rank, uint64_t* e0, uint64_t* e1,
+                   uint64_t* k0, uint64_t* k1);
+/* Pack this rank's output rows k0..k1-1 of `mode` (copy-row order, R floats each; the end
+ * rows may be partial sums) into dst (device). */
 int mk_shard_pack(mk_context* ctx, uint32_t mode, float* dst_device);
-/* Scatter an all-gathered buffer (world blocks of stride_rows rows, device) into the
- * output of `mode` in row-index order. */
+/* Scatter an all-gathered buffer (world blocks of stride_rows rows, device) into the output
+ * of `mode` in row-index order, summing the partial sums of split rows in rank order. */
 int mk_shard_unpack(mk_context* ctx, uint32_t mode, const float* src_device,
                     uint64_t stride_rows);
-/* Host helper: the cut points above for a CSR row pointer (row_ptr[nrows] = nnz);
- * cuts[world + 1]. */
+/* Host helpers on a CSR row pointer (row_ptr[nrows] = nnz), cuts[world + 1]:
+ * mk_shard_cuts — copy-row cuts (first row starting at or after floor(r nnz / world));
+ * mk_shard_split — the element cuts mk_set_shard uses (heavy rows split). */
 int mk_shard_cuts(const uint32_t* row_ptr, uint64_t nrows, uint32_t world, uint64_t* cuts);
+int mk_shard_split(const uint32_t* row_ptr, uint64_t nrows, uint32_t world, uint64_t* ecuts);
+/* NCCL inside the library (one process per GPU; libnccl.so.2 is opened on first use).
+ * Rank 0 creates the unique id (MK_NCCL_ID_BYTES opaque bytes) and the caller's launcher
+ * hands it to every rank (any channel: MPI, a file, torch.distributed); mk_comm_init then
+ * builds the communicator and applies mk_set_shard(rank, world) to the context's plans. */
+#define MK_NCCL_ID_BYTES 128
+int mk_comm_unique_id(void* id);
+int mk_comm_init(mk_context* ctx, uint32_t world, uint32_t rank, const void* id);
+int mk_comm_destroy(mk_context* ctx);
+/* The sharded all-mode sweep (unchained, like run_timed, kernel.hpp:239-287): per mode the
+ * rank's spMTTKRP, pack, ncclAllGather over NVLink, unpack — every rank ends with all N
+ * outputs.  Enqueued on the context stream (mk_synchronize surfaces errors); captured into
+ * a CUDA graph from the second call on (MKB_GRAPH=0 disables). */
+int mk_sweep_sharded(mk_context* ctx);
+/* One CPD-ALS iteration with the per-mode exchange; factors stay replicated. */
+int mk_cpd_als_iter_sharded(mk_context* ctx, double* fit, float* lambda);
 /* CPD-ALS pieces for a sharded driver: the Gram/solve/normalise update of mode d from the
  * (gathered) MTTKRP output, and the fit after the last mode. */
 int mk_als_update_mode(mk_context* ctx, uint32_t mode);

@@ -64,6 +64,8 @@ EXPORTED_SYMBOLS = [
     "mk_sweep_host", "mk_run_timed", "mk_flush_l2", "mk_last_sweep_fused", "mk_cpd_als_iter", "mk_cpd_als",
     "mk_generate_synthetic", "mk_generate_powerlaw", "mk_random_factors",
     "mk_set_shard", "mk_shard_rows", "mk_shard_pack", "mk_shard_unpack", "mk_shard_cuts",
+    "mk_shard_split", "mk_shard_range", "mk_comm_unique_id", "mk_comm_init", "mk_comm_destroy",
+    "mk_sweep_sharded", "mk_cpd_als_iter_sharded",
     "mk_als_update_mode", "mk_als_fit", "mk_output_device_ptr",
     "mk_tensor_upload_f64", "mk_factors_upload_f64", "mk_mttkrp_mode_f64",
     "mk_mttkrp_all_modes_f64", "mk_random_factors_f64", "mk_generate_synthetic_f64",
@@ -181,6 +183,13 @@ def load_library() -> C.CDLL:
             "mk_shard_pack": (i32, [vp, u32, vp]),
             "mk_shard_unpack": (i32, [vp, u32, vp, u64]),
             "mk_shard_cuts": (i32, [vp, u64, u32, vp]),
+            "mk_shard_split": (i32, [vp, u64, u32, vp]),
+            "mk_comm_unique_id": (i32, [vp]),
+            "mk_comm_init": (i32, [vp, u32, u32, vp]),
+            "mk_comm_destroy": (i32, [vp]),
+            "mk_sweep_sharded": (i32, [vp]),
+            "mk_cpd_als_iter_sharded": (i32, [vp, P(C.c_double), vp]),
+            "mk_shard_range": (i32, [vp, u32, u32, P(u64), P(u64), P(u64), P(u64)]),
             "mk_als_update_mode": (i32, [vp, u32]),
             "mk_als_fit": (i32, [vp, P(C.c_double), vp]),
             "mk_output_device_ptr": (i32, [vp, u32, P(vp)]),
@@ -520,6 +529,35 @@ class Context:
         k0, k1 = C.c_uint64(), C.c_uint64()
         _check(self.lib.mk_shard_rows(self.h, mode, rank, C.byref(k0), C.byref(k1)))
         return int(k0.value), int(k1.value)
+
+    # ---- NCCL inside the library (comm.cu)
+    @staticmethod
+    def comm_unique_id() -> bytes:
+        buf = C.create_string_buffer(128)
+        _check(load_library().mk_comm_unique_id(buf))
+        return buf.raw
+
+    def comm_init(self, world: int, rank: int, unique_id: bytes):
+        buf = C.create_string_buffer(bytes(unique_id), 128)
+        _check(self.lib.mk_comm_init(self.h, world, rank, buf))
+
+    def comm_destroy(self):
+        _check(self.lib.mk_comm_destroy(self.h))
+
+    def sweep_sharded(self):
+        _check(self.lib.mk_sweep_sharded(self.h))
+
+    def cpd_als_iter_sharded(self):
+        fit = C.c_double()
+        lam = np.empty(max(self.rank, 1), dtype=np.float32)
+        _check(self.lib.mk_cpd_als_iter_sharded(self.h, C.byref(fit), _ptr(lam)))
+        return fit.value, lam
+
+    def shard_range(self, mode: int, rank: int):
+        """(e0, e1, k0, k1): owned elements and touched copy rows of `rank` in `mode`."""
+        v = [C.c_uint64() for _ in range(4)]
+        _check(self.lib.mk_shard_range(self.h, mode, rank, *[C.byref(x) for x in v]))
+        return tuple(int(x.value) for x in v)
 
     def shard_pack(self, mode: int, dst):
         """dst: device pointer or CUDA tensor (>= owned rows x R fp32)."""
@@ -955,6 +993,15 @@ def load_tensor(path, options: Optional[FrosttOptions] = None, dtype=np.float32,
         except MttkrpError:
             pass  # read-only location: the parse result is still returned
     return res
+
+
+def shard_split(row_ptr, world: int) -> np.ndarray:
+    """mk_shard_split: the element cut points of mk_set_shard (heavy rows split) (host)."""
+    lib = load_library()
+    rp = np.ascontiguousarray(np.asarray(row_ptr, dtype=np.uint32))
+    cuts = np.empty(world + 1, dtype=np.uint64)
+    _check(lib.mk_shard_split(_ptr(rp), rp.size - 1, world, _ptr(cuts)))
+    return cuts
 
 
 def shard_cuts(row_ptr, world: int) -> np.ndarray:

@@ -166,6 +166,7 @@ int mk_destroy(mk_context* ctx) {
     if (!ctx) return;
     cudaSetDevice(ctx->c.device);
     cudaStreamSynchronize(ctx->c.stream);
+    comm_destroy(ctx->c);
     cudaStream_t own = ctx->c.own_stream;
     delete ctx;
     if (own) cudaStreamDestroy(own);
@@ -238,6 +239,7 @@ int mk_build_plans(mk_context* ctx, uint64_t kappa, int strategy, int policy) {
     if (strategy != MK_CYCLIC && strategy != MK_LEAST_LOADED)
       fail(MK_EINVAL, "layout: unknown strategy");
     if (policy < MK_ADAPTIVE || policy > MK_SCHEME2_ONLY) fail(MK_EINVAL, "layout: unknown policy");
+    invalidate_graph(ctx->c);
     build_plans(ctx->c, kappa, strategy, policy);
   });
 }
@@ -380,6 +382,7 @@ int mk_factors_upload(mk_context* ctx, uint32_t rank, const float* const* factor
     for (uint32_t w = 0; w < c.n; ++w)
       if (!factors[w]) fail(MK_EINVAL, "kernel: expected one factor matrix per mode");
     MKB_CUDA(cudaStreamSynchronize(c.stream));  // no launch may still read the old arenas
+    if (rank != c.rank) invalidate_graph(c);     // the arenas may move
     c.rank = rank;
     c.arena_off[0] = 0;
     for (uint32_t w = 0; w < c.n; ++w)
@@ -746,7 +749,50 @@ extern "C" {
 int mk_set_shard(mk_context* ctx, uint32_t rank, uint32_t world) {
   return guarded([&] {
     need_ctx(ctx);
+    invalidate_graph(ctx->c);
     set_shard(ctx->c, rank, world);
+  });
+}
+
+int mk_comm_unique_id(void* id) {
+  return guarded([&] {
+    if (!id) fail(MK_EINVAL, "comm: null unique id");
+    comm_unique_id(id);
+  });
+}
+
+int mk_comm_init(mk_context* ctx, uint32_t world, uint32_t rank, const void* id) {
+  return guarded([&] {
+    need_ctx(ctx);
+    comm_init(ctx->c, world, rank, id);
+  });
+}
+
+int mk_comm_destroy(mk_context* ctx) {
+  return guarded([&] {
+    need_ctx(ctx);
+    MKB_CUDA(cudaStreamSynchronize(ctx->c.stream));
+    comm_destroy(ctx->c);
+  });
+}
+
+int mk_sweep_sharded(mk_context* ctx) {
+  return guarded([&] {
+    need_ctx(ctx);
+    need_plans(ctx->c);
+    need_factors(ctx->c);
+    sweep_sharded(ctx->c);
+  });
+}
+
+int mk_cpd_als_iter_sharded(mk_context* ctx, double* fit, float* lambda) {
+  return guarded([&] {
+    need_ctx(ctx);
+    need_plans(ctx->c);
+    need_factors(ctx->c);
+    double f = 0.0;
+    als_iteration_sharded(ctx->c, &f, lambda);
+    if (fit) *fit = f;
   });
 }
 
@@ -763,9 +809,34 @@ int mk_shard_rows(mk_context* ctx, uint32_t mode, uint32_t rank, uint64_t* k0, u
       *k1 = mc.distinct;
       return;
     }
-    if (rank + 1 >= mc.shard_cuts.size()) fail(MK_EINVAL, "shard: rank must be below world size");
-    *k0 = mc.shard_cuts[rank];
-    *k1 = mc.shard_cuts[rank + 1];
+    if (2 * rank + 1 >= mc.shard_krange.size()) fail(MK_EINVAL, "shard: rank must be below world size");
+    *k0 = mc.shard_krange[2 * rank];
+    *k1 = mc.shard_krange[2 * rank + 1];
+  });
+}
+
+int mk_shard_range(mk_context* ctx, uint32_t mode, uint32_t rank, uint64_t* e0, uint64_t* e1,
+                   uint64_t* k0, uint64_t* k1) {
+  return guarded([&] {
+    need_ctx(ctx);
+    Context& c = ctx->c;
+    need_plans(c);
+    need_mode(c, mode);
+    const ModeCopy& mc = c.copies[mode];
+    uint64_t a = 0, b = c.nnz, ka = 0, kb = mc.distinct;
+    if (!mc.shard_ecuts.empty()) {
+      if (rank + 1 >= mc.shard_ecuts.size()) fail(MK_EINVAL, "shard: rank must be below world size");
+      a = mc.shard_ecuts[rank];
+      b = mc.shard_ecuts[rank + 1];
+      ka = mc.shard_krange[2 * rank];
+      kb = mc.shard_krange[2 * rank + 1];
+    } else if (rank != 0) {
+      fail(MK_EINVAL, "shard: rank must be below world size");
+    }
+    if (e0) *e0 = a;
+    if (e1) *e1 = b;
+    if (k0) *k0 = ka;
+    if (k1) *k1 = kb;
   });
 }
 

@@ -101,7 +101,10 @@ struct ModeCopy {
   } s2;
   // multi-GPU row-range shard of this copy: copy rows [k0, k1) = elements [e0, e1)
   uint64_t shard_k0 = 0, shard_k1 = 0, shard_e0 = 0, shard_e1 = 0;
-  std::vector<uint64_t> shard_cuts;  // world+1 copy-row cut points (all ranks)
+  std::vector<uint64_t> shard_cuts;  // world+1: first copy row touched by each rank (+ V)
+  std::vector<uint64_t> shard_ecuts;   // world+1 element cut points (mk_shard_split)
+  std::vector<uint64_t> shard_krange;  // 2*world: copy rows [k0_r, k1_r) touched by rank r
+  bool shard_split_row = false;        // this rank's range starts or ends inside a row
   std::vector<uint32_t> row_ptr_host;
   bool built = false;
 };
@@ -167,6 +170,14 @@ struct Context {
   DevBuf<unsigned long long> als_prof;  // MKB_ALS_PROF: phase timestamps of the update
   bool grams_valid = false;
   bool last_sweep_fused = false;  // the last sweep() ran as one k_sweep2 launch
+
+  // NCCL communicator and the sharded sweep's exchange buffers / CUDA graph (comm.cu)
+  void* nccl_comm = nullptr;
+  uint32_t comm_world = 0;
+  DevBuf<float> xsend, xrecv;
+  uint64_t xstride[kMaxModes] = {};
+  void* graph_exec = nullptr;  // cudaGraphExec_t of the captured sharded sweep
+  bool graph_warm = false;     // one eager sweep ran (the fast path's kernel choice is made)
 };
 
 // One CPD-ALS iteration over all modes (als.cu); fit and optional lambda[R] to host.
@@ -190,6 +201,13 @@ void ensure_zero_list(Context& c, uint32_t mode, ModeCopy::ZeroList& zl, uint32_
 void set_shard(Context& c, uint32_t rank, uint32_t world);
 void shard_pack(Context& c, uint32_t mode, float* dst);
 void shard_unpack(Context& c, uint32_t mode, const float* src, uint64_t stride_rows);
+// NCCL communicator + sharded sweep / ALS iteration (comm.cu)
+void comm_unique_id(void* id128);
+void comm_init(Context& c, uint32_t world, uint32_t rank, const void* unique_id);
+void comm_destroy(Context& c);
+void invalidate_graph(Context& c);
+void sweep_sharded(Context& c);
+void als_iteration_sharded(Context& c, double* fit, float* lambda_host);
 // ALS pieces (als.cu), used by the single-GPU iteration and the sharded driver.
 void als_prepare(Context& c);
 void als_update_mode(Context& c, uint32_t d);

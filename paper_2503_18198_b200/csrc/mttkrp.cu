@@ -168,8 +168,10 @@ __global__ void __launch_bounds__(256) k_mttkrp_tiles(const MttkrpArgs a) {
       ta = a.e0 + static_cast<uint64_t>(t) * a.tile;
       tb = min(ta + a.tile, a.e1);
     }
-    const bool head_split = ta > 0 && __ldg(a.out_idx + ta - 1) == __ldg(a.out_idx + ta);
-    const bool tail_split = tb < a.nnz && __ldg(a.out_idx + tb) == __ldg(a.out_idx + tb - 1);
+    // a run continuing past this launch's range [e0, e1) is local: a row split between
+    // shard ranks is summed by the exchange (shard.cu k_unpack_sum)
+    const bool head_split = ta > a.e0 && __ldg(a.out_idx + ta - 1) == __ldg(a.out_idx + ta);
+    const bool tail_split = tb < a.e1 && __ldg(a.out_idx + tb) == __ldg(a.out_idx + tb - 1);
     uint32_t cur = __ldg(a.out_idx + ta);
     uint64_t run_start = ta;
     bool first_run = true;
@@ -249,7 +251,9 @@ __global__ void __launch_bounds__(256) k_mttkrp_rows(const MttkrpArgs a) {
 
   for (uint32_t k = a.k0 + gid; k < a.k0 + a.nrows; k += groups) {
     const uint32_t row = __ldg(a.row_seq + k);
-    const uint64_t s = __ldg(a.row_ptr + k), e = __ldg(a.row_ptr + k + 1);
+    // clamped to the launch's range: the end rows of a shard may be partial
+    const uint64_t s = max(static_cast<uint64_t>(__ldg(a.row_ptr + k)), a.e0),
+                   e = min(static_cast<uint64_t>(__ldg(a.row_ptr + k + 1)), a.e1);
     float acc[F];
 #pragma unroll
     for (int q = 0; q < F; ++q) acc[q] = 0.0f;
@@ -488,7 +492,9 @@ int choose_fast_kernel(Context& c, uint32_t mode, const float* const* in, float*
   if (c.force_fast_kernel >= 0) force = c.force_fast_kernel == 0 ? "s2" : (c.force_fast_kernel == 1 ? "stream" : "tiles");
   if (!force.empty()) mc.s2_force_k = -1;  // a forced kernel runs the cost model's plan
   const bool s2_ok = force != "stream" && force != "tiles" && prepare_stream2(c, mode);
-  const bool st_ok = force != "s2" && force != "tiles" && prepare_stream(c, mode);
+  // the fiber-ordered records permute elements inside rows: no partial (shard-split) rows
+  const bool st_ok = force != "s2" && force != "tiles" && !mc.shard_split_row &&
+                     prepare_stream(c, mode);
   if (!s2_ok && !st_ok) return mc.fast_kernel = 2;
   if (!st_ok) return mc.fast_kernel = 0;
   if (!s2_ok) return mc.fast_kernel = 1;
@@ -503,11 +509,13 @@ int choose_fast_kernel(Context& c, uint32_t mode, const float* const* in, float*
   return mc.fast_kernel;
 }
 
+static bool mc_split(const Context& c, uint32_t mode) { return c.copies[mode].shard_split_row; }
+
 void launch_mttkrp(Context& c, uint32_t mode, const float* const* in, float* out, int exec) {
   if (exec == MK_EXEC_FAST) {
     const int k = choose_fast_kernel(c, mode, in, out);
     if (k == 0 && launch_stream2(c, mode, in, out)) return;
-    if (k == 1 && launch_stream(c, mode, in, out)) return;
+    if (k == 1 && !mc_split(c, mode) && launch_stream(c, mode, in, out)) return;
   }
   ModeCopy& mc = c.copies[mode];
   MttkrpArgs a{};

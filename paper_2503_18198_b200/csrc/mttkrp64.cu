@@ -60,7 +60,8 @@ __global__ void __launch_bounds__(256) k_rows64(const Args64 a) {
   for (uint32_t k = a.k0 + (blockIdx.x * blockDim.x + threadIdx.x) / 32; k < a.k0 + a.nrows;
        k += warps) {
     const uint32_t row = a.row_seq[k];
-    const uint64_t s = a.row_ptr[k], e = a.row_ptr[k + 1];
+    const uint64_t s = max(static_cast<uint64_t>(a.row_ptr[k]), a.e0),
+                   e = min(static_cast<uint64_t>(a.row_ptr[k + 1]), a.e1);
     double acc[KR];
 #pragma unroll
     for (int q = 0; q < KR; ++q) acc[q] = 0.0;

@@ -197,7 +197,7 @@ __global__ void __launch_bounds__(NT, MINB) k_mttkrp_stream(const StreamArgs a) 
   const int tid = threadIdx.x;
   const int lane_g = tid % G;
   const int g = tid / G;
-  const uint32_t nnz = a.nnz, e0a = a.e0a, e0 = a.e0, e1 = a.e1;
+  const uint32_t e0a = a.e0a, e0 = a.e0, e1 = a.e1;
   const uint32_t ntiles = (e1 - e0a + TILE - 1) / TILE;
 
   // per-lane base pointers: row c of input i is Yv[i][c * G] (global or staged in SMEM)
@@ -272,8 +272,8 @@ __global__ void __launch_bounds__(NT, MINB) k_mttkrp_stream(const StreamArgs a) 
       const uint32_t* rb =
           reinterpret_cast<const uint32_t*>(smem + 2 * BYTES_A + stage * BYTES_B) +
           (p0 - base) * BW;
-      const bool head_split = p0 > 0 && __ldg(gcd + p0 - 1) == __ldg(gcd + p0);
-      const bool tail_split = p1 < nnz && __ldg(gcd + p1) == __ldg(gcd + p1 - 1);
+      const bool head_split = p0 > e0 && __ldg(gcd + p0 - 1) == __ldg(gcd + p0);
+      const bool tail_split = p1 < e1 && __ldg(gcd + p1) == __ldg(gcd + p1 - 1);
       const uint32_t n = p1 - p0;
       uint32_t fc = 0;              // FIB: current fiber coordinate
       float4 yf = make_float4(0.f, 0.f, 0.f, 0.f);  // FIB: its factor row

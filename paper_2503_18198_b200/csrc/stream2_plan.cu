@@ -69,6 +69,11 @@ __device__ __forceinline__ uint32_t block_of(const Split& sp, uint32_t s) {
   return b;
 }
 
+__global__ void k_iota_from(uint32_t* __restrict__ p, uint64_t n, uint32_t base) {
+  const uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+  if (i < n) p[i] = base + static_cast<uint32_t>(i);
+}
+
 __global__ void k_block_keys(Split sp, const uint32_t* __restrict__ perm, uint64_t n,
                              uint32_t* __restrict__ keys, uint32_t* __restrict__ counts) {
   for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
@@ -234,11 +239,14 @@ bool prepare_stream2(Context& c, uint32_t mode) {
   const uint32_t ni = c.n - 1, G = c.rank / 4;
   const int rowbits = bits_for(c.dims[mode] - 1);
   if (rowbits > 31) return false;
-  const bool sharded = mc.shard_e0 != 0 || mc.shard_e1 != nnz;
+  // The plan covers the copy positions [E0s, E1s) this context owns (the whole copy unless
+  // sharded): every sort below runs on that window of perm/keys only, so a shard's records,
+  // blocks and work split describe exactly its own elements (a partial end row included).
+  const uint64_t E0s = mc.shard_e0, E1s = mc.shard_e1, ns = E1s - E0s;
   p.ni = ni;
   p.rowbits = static_cast<uint32_t>(rowbits);
   const unsigned gblocks =
-      static_cast<unsigned>(std::min<uint64_t>((nnz + 255) / 256, c.num_sms * 16ull));
+      static_cast<unsigned>(std::min<uint64_t>((ns + 255) / 256 + 1, c.num_sms * 16ull));
   const size_t rowbytes = static_cast<size_t>(c.rank) * 4u;
   auto fbytes = [&](uint32_t w) { return static_cast<size_t>(c.dims[w]) * rowbytes; };
 
@@ -252,33 +260,39 @@ bool prepare_stream2(Context& c, uint32_t mode) {
   // 2. outer level: distinct (row, c_0) pairs
   DevBuf<uint32_t> perm(nnz), keys(nnz), rank;
   rank_of_row_build(c, mode, rank);
+  uint32_t* const wperm = perm.get() + E0s;  // the window [E0s, E1s)
+  uint32_t* const wkeys = keys.get() + E0s;
   auto sort_by = [&](const uint32_t* col, int bits) {
-    k_keys_of<<<gblocks, 256, 0, st>>>(col, perm.get(), nnz, keys.get());
+    k_keys_of<<<gblocks, 256, 0, st>>>(col, wperm, ns, wkeys);
     MKB_LAUNCH();
-    radix_sort_pairs(keys.get(), perm.get(), nnz, bits, c.scratch, st);
+    radix_sort_pairs(wkeys, wperm, ns, bits, c.scratch, st);
   };
   auto sort_by_row = [&] {
     if (mc.distinct <= 1) return;
-    k_row_keys<<<gblocks, 256, 0, st>>>(mc.idx[mode].get(), rank.get(), perm.get(), nnz,
-                                        keys.get());
+    k_row_keys<<<gblocks, 256, 0, st>>>(mc.idx[mode].get(), rank.get(), wperm, ns, wkeys);
     MKB_LAUNCH();
-    radix_sort_pairs(keys.get(), perm.get(), nnz, bits_for(mc.distinct - 1), c.scratch, st);
+    radix_sort_pairs(wkeys, wperm, ns, bits_for(mc.distinct - 1), c.scratch, st);
+  };
+  auto window_iota = [&] {
+    if (!ns) return;
+    k_iota_from<<<ceil_div(ns, 256), 256, 0, st>>>(wperm, ns, static_cast<uint32_t>(E0s));
+    MKB_LAUNCH();
   };
   {
-    iota_u32(perm.get(), nnz, st);
+    window_iota();
     sort_by(mc.idx[lv[0]].get(), bits_for(c.dims[lv[0]] - 1));
     sort_by_row();
     DevBuf<unsigned long long> cnt(1);
     MKB_CUDA(cudaMemsetAsync(cnt.get(), 0, sizeof(unsigned long long), st));
-    k_count_runs<<<gblocks, 256, 0, st>>>(mc.idx[mode].get(), mc.idx[lv[0]].get(), perm.get(),
-                                          nnz, cnt.get());
+    k_count_runs<<<gblocks, 256, 0, st>>>(mc.idx[mode].get(), mc.idx[lv[0]].get(), wperm, ns,
+                                          cnt.get());
     MKB_LAUNCH();
     unsigned long long runs = 0;
     MKB_CUDA(cudaMemcpyAsync(&runs, cnt.get(), sizeof runs, cudaMemcpyDeviceToHost, st));
     MKB_CUDA(cudaStreamSynchronize(st));
     p.outer_runs = runs;
     const int outer_div = env_int("MKB_OUTER_DIV", 16);  // 0 disables the outer level
-    p.nout = (outer_div > 0 && runs * outer_div < nnz &&
+    p.nout = (outer_div > 0 && runs * outer_div < ns &&
               rowbits + bits_for(c.dims[lv[0]] - 1) <= 32)
                  ? 1u
                  : 0u;
@@ -308,7 +322,7 @@ bool prepare_stream2(Context& c, uint32_t mode) {
   };
   const size_t budget0 = budget_for(0);
   const bool stage_on = env_int("MKB_STAGE", 1) != 0;
-  const bool block_on = env_int("MKB_BLOCK", 1) != 0 && !sharded;
+  const bool block_on = env_int("MKB_BLOCK", 1) != 0;
   // The outer row is read once per outer run (folded, stream2.cuh), through L1/L2 with its
   // latency hidden until the next fold; staging it costs shared memory the inner levels use
   // better (cfg2 mode 1: 6 -> 4 blocks, sweep 0.156 -> 0.154 ms).  MKB_OUTER_STAGE=1 stages it.
@@ -372,13 +386,13 @@ bool prepare_stream2(Context& c, uint32_t mode) {
           l2 += (1.0 - hit) * rowbytes / kL2Gather;
         }
         const double flushes =
-            cd.nb > 1 ? std::min<double>(nnz, static_cast<double>(cd.nb) *
-                                                  std::max<uint64_t>(mc.distinct, 1))
+            cd.nb > 1 ? std::min<double>(ns, static_cast<double>(cd.nb) *
+                                                 std::max<uint64_t>(mc.distinct, 1))
                       : 0.0;
         // every CTA item restages: bandwidth + a ~6000-cycle stall (barrier + TMA round trip)
         const double stage =
             static_cast<double>(c.num_sms + cd.nb) * (staged_bytes() / kL2 + (k ? 6000.0 : 0.0));
-        cd.cost = lsu + l2 + (kFlush * flushes + stage) / static_cast<double>(nnz);
+        cd.cost = lsu + l2 + (kFlush * flushes + stage) / static_cast<double>(std::max<uint64_t>(ns, 1));
         // prefer the simpler plan (fewer blocks, no swap) within 3%
         if (cd.cost < best.cost * (cd.nb < best.nb ? 1.03 : 0.97)) best = cd;
       }
@@ -431,7 +445,7 @@ bool prepare_stream2(Context& c, uint32_t mode) {
   }
 
   // 4. kernel order: levels (innermost first), row rank, block
-  iota_u32(perm.get(), nnz, st);
+  window_iota();
   for (int l = static_cast<int>(ni) - 1; l >= 0; --l)
     sort_by(mc.idx[lv[l]].get(), bits_for(c.dims[lv[l]] - 1));
   sort_by_row();
@@ -446,18 +460,21 @@ bool prepare_stream2(Context& c, uint32_t mode) {
       stride *= split[j];
     }
   }
-  std::vector<uint32_t> bcount(p.nblocks, 0), bstart(p.nblocks + 1, 0);
+  std::vector<uint32_t> bcount(p.nblocks, 0);
+  std::vector<uint64_t> bstart(p.nblocks + 1, E0s);  // kernel positions: blocks of the window
   if (p.nblocks > 1) {
     DevBuf<uint32_t> counts(p.nblocks);
     MKB_CUDA(cudaMemsetAsync(counts.get(), 0, p.nblocks * sizeof(uint32_t), st));
-    k_block_keys<<<gblocks, 256, 0, st>>>(sp, perm.get(), nnz, keys.get(), counts.get());
-    MKB_LAUNCH();
-    radix_sort_pairs(keys.get(), perm.get(), nnz, bits_for(p.nblocks - 1), c.scratch, st);
+    if (ns) {
+      k_block_keys<<<gblocks, 256, 0, st>>>(sp, wperm, ns, wkeys, counts.get());
+      MKB_LAUNCH();
+      radix_sort_pairs(wkeys, wperm, ns, bits_for(p.nblocks - 1), c.scratch, st);
+    }
     MKB_CUDA(cudaMemcpyAsync(bcount.data(), counts.get(), p.nblocks * sizeof(uint32_t),
                              cudaMemcpyDeviceToHost, st));
     MKB_CUDA(cudaStreamSynchronize(st));
   } else {
-    bcount[0] = static_cast<uint32_t>(nnz);
+    bcount[0] = static_cast<uint32_t>(ns);
   }
   for (uint32_t b = 0; b < p.nblocks; ++b) bstart[b + 1] = bstart[b] + bcount[b];
   std::vector<Blk> blks(p.nblocks);
@@ -480,7 +497,7 @@ bool prepare_stream2(Context& c, uint32_t mode) {
   const uint32_t S = s2::seg_len(p.aw), RS = s2::rec_stride(p.aw), KS = s2::key_stride(p.aw);
   const uint32_t NW = p.nt / 32, GPW = 32 / G, NG = NW * GPW;
   const unsigned grid = static_cast<unsigned>(c.num_sms);
-  const uint64_t E0 = p.blocked ? 0 : mc.shard_e0, E1 = p.blocked ? nnz : mc.shard_e1;
+  const uint64_t E0 = E0s, E1 = E1s;
   std::vector<WDesc> wd;
   std::vector<uint32_t> gstart, dblk, items, cta(grid + 1, 0);
   uint64_t tile_n = 0;
