@@ -102,6 +102,7 @@ void check_nonfinite(Context& c) {
 // barrier.  With chain, later modes read the fresh outputs of earlier modes
 // (kernel.hpp:186-195).  Non-finite detection reports the first failing mode.
 void sweep(Context& c, int chain, int exec) {
+  NvtxRange nv(chain ? "all-mode sweep (chained)" : "all-mode sweep");
   const float* in[kMaxModes];
   for (uint32_t w = 0; w < c.n; ++w) in[w] = c.factors[w].get();
   if (!chain && exec == MK_EXEC_FAST) {

@@ -531,6 +531,7 @@ void als_prepare(Context& c) {
 // Y_d = M_d V⁻¹ diag(1/λ) with V = ⊛_{w≠d} G_w; G_d, λ and (last mode) the fit terms.
 // M_d is the (possibly all-gathered) MTTKRP output in c.outputs[d].
 void als_update_mode(Context& c, uint32_t d) {
+  NvtxRange nv("CPD-ALS update", d);
   als_prepare(c);
   const uint32_t R = c.rank, n = c.n;
   cudaStream_t st = c.stream;

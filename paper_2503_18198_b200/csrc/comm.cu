@@ -125,6 +125,7 @@ void ensure_exchange(Context& c) {
 }
 
 void exchange_mode(Context& c, uint32_t d) {
+  NvtxRange nv("shard exchange (pack / ncclAllGather / unpack)", d);
   const uint64_t count = c.xstride[d] * c.rank;
   shard_pack(c, d, c.xsend.get());
   nccl_check(nccl().AllGather(c.xsend.get(), c.xrecv.get(), count, ncclFloat32,

@@ -9,9 +9,27 @@
 #include <string>
 #include <utility>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "mttkrp_b200.h"
 
 namespace mkb {
+
+// NVTX range (header-only NVTX v3: a no-op unless a profiler injects itself).  The library
+// marks format builds, every mode's spMTTKRP launch, the fused sweep, the shard exchange and
+// the ALS update, so an nsys / ncu timeline shows the mode structure of a CPD iteration.
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  NvtxRange(const char* what, unsigned mode) {
+    char b[96];
+    std::snprintf(b, sizeof b, "%s mode %u", what, mode);
+    nvtxRangePushA(b);
+  }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
+
 
 // Internal exception carrying an mk_status; converted at the C-ABI boundary.
 struct Error : std::runtime_error {

@@ -292,6 +292,7 @@ void tensor_upload(Context& c, uint32_t n, const uint32_t* dims, uint64_t nnz,
 }
 
 void build_plans(Context& c, uint64_t kappa, int strategy, int policy) {
+  NvtxRange nv("build_mode_plans");
   if (kappa < 1) fail(MK_EINVAL, "layout: kappa must be at least 1");
   if (c.n == 0) fail(MK_ESTATE, "layout: no tensor uploaded");
   if (kappa >= 0xffffffffull) fail(MK_EINVAL, "layout: kappa too large");

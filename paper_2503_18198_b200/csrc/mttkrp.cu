@@ -512,6 +512,9 @@ int choose_fast_kernel(Context& c, uint32_t mode, const float* const* in, float*
 static bool mc_split(const Context& c, uint32_t mode) { return c.copies[mode].shard_split_row; }
 
 void launch_mttkrp(Context& c, uint32_t mode, const float* const* in, float* out, int exec) {
+  NvtxRange nv(exec == MK_EXEC_FAST ? "spMTTKRP fast" :
+               (exec == MK_EXEC_DETERMINISTIC ? "spMTTKRP deterministic" : "spMTTKRP partitioned"),
+               mode);
   if (exec == MK_EXEC_FAST) {
     const int k = choose_fast_kernel(c, mode, in, out);
     if (k == 0 && launch_stream2(c, mode, in, out)) return;
