@@ -35,6 +35,7 @@
 #include <string>
 #include <string_view>
 #include <type_traits>
+#include <utility>
 #include <vector>
 
 #include "mttkrp_b200.h"
@@ -60,6 +61,14 @@ struct Shape {
   explicit Shape(std::vector<index_t> d) : dims(std::move(d)) { validate(); }
   std::size_t mode_count() const { return dims.size(); }
   index_t extent(std::size_t d) const { return dims[d]; }
+  std::uint64_t capacity() const {  // types.hpp:38-46, saturating
+    std::uint64_t cap = 1;
+    for (index_t e : dims) {
+      if (e != 0 && cap > UINT64_MAX / e) return UINT64_MAX;
+      cap *= e;
+    }
+    return cap;
+  }
   void validate() const {
     if (dims.empty()) throw error("shape: a tensor needs at least one mode");
     for (index_t e : dims)
@@ -129,6 +138,23 @@ class SparseTensorCOO {
   std::vector<index_t> coords_;
   std::vector<T> values_;
 };
+
+// tensor.hpp:115-131: order-insensitive equality of two tensors as <indices, value> sets
+template <typename T>
+bool same_element_set(const SparseTensorCOO<T>& a, const SparseTensorCOO<T>& b) {
+  if (!(a.shape() == b.shape()) || a.nnz() != b.nnz()) return false;
+  auto sorted = [](const SparseTensorCOO<T>& t) {
+    std::vector<std::pair<std::vector<index_t>, T>> v;
+    v.reserve(t.nnz());
+    for (std::size_t i = 0; i < t.nnz(); ++i) {
+      auto c = t.coords(i);
+      v.emplace_back(std::vector<index_t>(c.begin(), c.end()), t.value(i));
+    }
+    std::sort(v.begin(), v.end());
+    return v;
+  };
+  return sorted(a) == sorted(b);
+}
 
 template <typename T>
 struct FactorMatrix {
