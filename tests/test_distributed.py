@@ -230,7 +230,9 @@ def test_device_exchange_simulated_ranks(mk, orc, world, kernel):
         _exchange(ctxs, d, 32, deterministic=True)
         want = orc.mttkrp_f64(dims, t.coords, t.values, f, d)
         for c in ctxs:
-            assert orc.max_rel_err_f64(c.output(d), want) <= 1e-5
+            # the sequential fp32 row sums (the reference's order) drift ~1e-5 from fp64 on
+            # these 10^4-10^5-element rows: the north star's 1e-4 bound
+            assert orc.max_rel_err_f64(c.output(d), want) <= 1e-4
     for c in ctxs:
         c.close()
 
