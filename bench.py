@@ -144,30 +144,36 @@ def measured_peaks():
 
 
 def ncu_traffic(config_name):
-    """dram bytes per sweep from the committed ncu --set full summary, if present."""
-    path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-    try:
-        with open(path) as fh:
-            entry = json.load(fh).get(config_name)
-        return float(entry["dram_bytes_per_sweep"]) if entry else None
-    except Exception:
-        return None
+    """dram bytes per sweep from the committed ncu captures (the round's counter capture of the
+    timed plan, profiles/ncu_lsu.json; else the older --set full summary), if present."""
+    for fname in ("ncu_lsu.json", "ncu_traffic.json"):
+        try:
+            with open(os.path.join(ROOT, "profiles", fname)) as fh:
+                entry = json.load(fh).get(config_name)
+            if entry and entry.get("dram_bytes_per_sweep"):
+                return float(entry["dram_bytes_per_sweep"])
+        except Exception:
+            pass
+    return None
 
 
-def lsu_roofline(config_name, kern_ms):
+def lsu_roofline(config_name, kern_ms, sm_mhz=None):
     """Secondary (binding) roofline: bytes through the SM's L1/shared-memory data path per
-    sweep (l1tex data-pipe wavefronts x 128 B from the committed ncu capture) against the
-    chip's 128 B/clk/SM x 148 SMs x sm clock."""
+    sweep (l1tex data-pipe wavefronts x 128 B from the committed ncu capture of the timed
+    plan, tools/ncu_lsu.sh) against the chip's 128 B/clk/SM x 148 SMs x the SM clock sampled
+    during this run's timed region."""
     path = os.path.join(ROOT, "profiles", "ncu_lsu.json")
     try:
         with open(path) as fh:
             entry = json.load(fh).get(config_name)
         if not entry:
             return None
-        peak = 128.0 * entry["sms"] * entry["sm_mhz"] * 1e6 / 1e9  # GB/s
+        mhz = sm_mhz or entry["sm_mhz"]
+        peak = 128.0 * entry["sms"] * mhz * 1e6 / 1e9  # GB/s
         achieved = entry["lsu_bytes_per_sweep"] / (kern_ms * 1e-3) / 1e9
-        return {"bound": "l1/smem data path", "achieved": achieved, "peak": peak,
-                "unit": "GB/s", "frac": achieved / peak, "source": entry.get("source")}
+        return {"bound": "l1/smem data path (128 B/clk/SM)", "achieved": achieved, "peak": peak,
+                "unit": "GB/s", "frac": achieved / peak, "sm_mhz": mhz,
+                "bytes_per_sweep": entry["lsu_bytes_per_sweep"], "source": entry.get("source")}
     except Exception:
         return None
 
@@ -448,7 +454,8 @@ def run_config(args, name, rank, world, local_rank, stream, with_cpu):
                      "frac": achieved / peak, "traffic": ncu_traffic(name),
                      "peak_source": peak_src, "algorithmic_bytes_per_sweep": b_iter,
                      "kernel": sorted({f["kernel"] for f in fast}), "kernel_ms_per_sweep": kern_ms,
-                     "lsu": lsu_roofline(name, kern_ms), "per_mode": fast},
+                     "lsu": lsu_roofline(name, kern_ms, clk.summary().get("sm_mhz")),
+                     "per_mode": fast},
         "e2e": {"value": e2e_ms, "unit": "ms", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": h2d, "path": "mk_sweep_host (C ABI), pinned host buffers",
                 "pageable_per_mode_ms": e2e_pageable_ms},

@@ -47,6 +47,11 @@ enum {
                                 (for_each_partition, parallel.hpp:16-49; Algorithm 2), atomics
                                 only where Scheme 2 partitions or the CTA-internal split cut a
                                 row; the GPU form of the paper's scheme ablation (fp32 only) */
+  MK_EXEC_REFERENCE = 3,     /* the reference's parallel-executor contract (
+                                kernel.hpp:117-121): Scheme 1 copies own their rows and sum in
+                                copy order, so they run the deterministic kernel (bitwise equal
+                                to MK_EXEC_DETERMINISTIC); Scheme 2 copies run MK_EXEC_FAST.
+                                The C++ drop-in's ExecConfig{deterministic=false} default */
 };
 
 typedef struct mk_context mk_context;

@@ -531,8 +531,18 @@ struct ExecConfig {
   std::size_t batch_p = 32;
   bool deterministic = false;
   bool partitioned = false;  // MK_EXEC_PARTITIONED: the reference's partition-per-worker split
+  // Extension (no reference counterpart).  false: the reference's parallel-executor contract,
+  // MK_EXEC_REFERENCE (Scheme 1 modes bitwise equal to deterministic);
+  // true: the B200 fast path, MK_EXEC_FAST (level-ordered kernels, within 1e-4 of the oracle).
+  bool fast = false;
   int exec_code() const {
-    return deterministic ? MK_EXEC_DETERMINISTIC : (partitioned ? MK_EXEC_PARTITIONED : MK_EXEC_FAST);
+    if (deterministic) return MK_EXEC_DETERMINISTIC;
+    if (partitioned) return MK_EXEC_PARTITIONED;
+    return fast ? MK_EXEC_FAST : MK_EXEC_REFERENCE;
+  }
+  // the fp64 device path has no partitioned executor
+  int exec_code64() const {
+    return partitioned && !deterministic ? (fast ? MK_EXEC_FAST : MK_EXEC_REFERENCE) : exec_code();
   }
   void validate() const {
     if (kappa < 1) throw error("kernel: kappa must be at least 1");
@@ -628,7 +638,7 @@ FactorMatrix<T> mttkrp_mode(const SparseTensorCOO<T>& t, const ModePlan& plan,
   auto out = FactorMatrix<T>::zeros(plan.mode, t.extent(plan.mode), factors[0].rank);
   detail::check(detail::mode_call<T>(
       plan.device->ctx, static_cast<uint32_t>(plan.mode),
-      std::is_same_v<T, double> && !config.deterministic ? MK_EXEC_FAST : config.exec_code(),
+      std::is_same_v<T, double> ? config.exec_code64() : config.exec_code(),
       out.data.data()));
   return out;
 }
@@ -651,8 +661,7 @@ std::vector<FactorMatrix<T>> mttkrp_all_modes(const SparseTensorCOO<T>& t,
   for (std::size_t d = 0; d < plans.size(); ++d)
     outs.push_back(FactorMatrix<T>::zeros(d, t.extent(d), factors[0].rank));
   for (auto& o : outs) ptr.push_back(o.data.data());
-  const int exec = std::is_same_v<T, double> && !config.deterministic ? MK_EXEC_FAST
-                                                                       : config.exec_code();
+  const int exec = std::is_same_v<T, double> ? config.exec_code64() : config.exec_code();
   if constexpr (std::is_same_v<T, double>)
     detail::check(mk_mttkrp_all_modes_f64(plans[0].device->ctx, chain_outputs ? 1 : 0, exec,
                                           ptr.data()));
@@ -722,7 +731,7 @@ TimedRun<T> run_timed(const SparseTensorCOO<T>& t, const std::vector<ModePlan>& 
         auto o = FactorMatrix<T>::zeros(d, t.extent(d), factors[0].rank);
         const auto t0 = std::chrono::steady_clock::now();
         detail::check(mk_mttkrp_mode_f64(plans[0].device->ctx, static_cast<uint32_t>(d),
-                                         config.deterministic ? MK_EXEC_DETERMINISTIC : MK_EXEC_FAST,
+                                         config.exec_code64(),
                                          o.data.data()));
         const double ms = std::chrono::duration<double, std::milli>(
                               std::chrono::steady_clock::now() - t0).count();

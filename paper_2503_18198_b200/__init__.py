@@ -52,7 +52,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 _LIB_NAME = "libmttkrp_b200.so"
 
 MK_OK, MK_EINVAL, MK_ENOMEM, MK_ECUDA, MK_ENONFINITE, MK_ESTATE, MK_ENCCL = range(7)
-EXEC_FAST, EXEC_DETERMINISTIC, EXEC_PARTITIONED = 0, 1, 2
+EXEC_FAST, EXEC_DETERMINISTIC, EXEC_PARTITIONED, EXEC_REFERENCE = 0, 1, 2, 3
 
 EXPORTED_SYMBOLS = [
     "mk_last_error", "mk_version", "mk_device_count", "mk_device_sm_count", "mk_create", "mk_destroy",
@@ -334,11 +334,17 @@ class ExecConfig:
     # the reference's work split on the GPU (partition z of the plan on CTA z; the paper's
     # scheme ablation, MK_EXEC_PARTITIONED); no reference counterpart flag
     partitioned: bool = False
+    # the reference's parallel-executor contract (MK_EXEC_REFERENCE: Scheme 1 modes bitwise
+    # equal to deterministic) -- the C++ drop-in's default.  This harness
+    # API defaults to the B200 fast path (MK_EXEC_FAST, within 1e-4 of the oracle).
+    reference: bool = False
 
     def exec_code(self) -> int:
         if self.deterministic:
             return EXEC_DETERMINISTIC
-        return EXEC_PARTITIONED if self.partitioned else EXEC_FAST
+        if self.partitioned:
+            return EXEC_PARTITIONED
+        return EXEC_REFERENCE if self.reference else EXEC_FAST
 
     def validate(self):
         if self.kappa < 1:

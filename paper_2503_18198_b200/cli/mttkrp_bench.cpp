@@ -12,7 +12,10 @@
 //   --tensor X.mkbt   a binary tensor cache is read directly; --cache parses a .tns once and
 //                     keeps <file>.mkbt next to it;
 //   run --verify      compares against the deterministic device executor, which is bitwise
-//                     equal to the reference's oracle_mttkrp (tests/test_gpu_mttkrp.py).
+//                     equal to the reference's oracle_mttkrp (tests/test_gpu_mttkrp.py);
+//   run --fast        the B200 fast executor (MK_EXEC_FAST, within 1e-4 of the oracle) instead
+//                     of the reference's executor contract (MK_EXEC_REFERENCE: Scheme 1 modes
+//                     bitwise equal to --deterministic).
 // No third-party dependency: argument parsing and JSON output are written out here.
 #include <charconv>
 #include <cmath>
@@ -227,6 +230,7 @@ struct Options {
   std::uint64_t seed = 1;
   bool verify = false;
   bool deterministic = false;
+  bool fast = false;
   bool cache = false;
   std::string json_path;
   std::vector<mttkrp::index_t> dims;
@@ -310,7 +314,8 @@ int cmd_run(const Options& opt) {
   const std::size_t kappa = opt.kappa ? opt.kappa : detect_kappa();
   const auto policy = parse_policy(opt.policy);
   const auto strategy = parse_strategy(opt.strategy);
-  const mttkrp::ExecConfig config{kappa, opt.batch_p, opt.deterministic};
+  mttkrp::ExecConfig config{kappa, opt.batch_p, opt.deterministic};
+  config.fast = opt.fast;
   config.validate();
 
   report["backend"] = opt.backend;
@@ -323,6 +328,7 @@ int cmd_run(const Options& opt) {
   report["iters"] = opt.iters;
   report["seed"] = opt.seed;
   report["deterministic"] = opt.deterministic;
+  report["exec"] = opt.deterministic ? "deterministic" : (opt.fast ? "fast" : "reference");
 
   auto plans = mttkrp::build_mode_plans(tensor, kappa, strategy, policy);
   auto factors = mttkrp::random_factors<T>(tensor.shape(), opt.rank, opt.seed);
@@ -477,7 +483,7 @@ void usage() {
       "Sparse MTTKRP benchmark harness with mode-specific tensor layouts (B200 backend)\n"
       "Usage: mttkrp-bench <run|gen|inspect> [options]\n"
       "  run     --tensor F [--rank R] [--kappa K] [--batch P] [--policy adaptive|s1|s2]\n"
-      "          [--strategy cyclic|lpt] [--iters N] [--verify] [--deterministic]\n"
+      "          [--strategy cyclic|lpt] [--iters N] [--verify] [--deterministic] [--fast]\n"
       "          [--precision f32|f64] [--seed S] [--json PATH] [--cache] [--backend gpu]\n"
       "  gen     --dims A,B,C --nnz M --out F(.tns|.mkbt) [--dist uniform|skewed]\n"
       "          [--skew-mode D] [--skew-distinct K] [--seed S] [--precision f32|f64] [--json PATH]\n"
@@ -504,7 +510,7 @@ Cmd parse_args(int argc, char** argv, Options& opt) {
       a = a.substr(0, eq);
     }
     auto flag = [&](const char* name) { return a == name; };
-    const bool is_flag = flag("--verify") || flag("--deterministic") || flag("--cache") ||
+    const bool is_flag = flag("--verify") || flag("--deterministic") || flag("--cache") || flag("--fast") ||
                          flag("--help") || flag("-h");
     if (!is_flag && eq == std::string::npos) {
       if (i + 1 >= argc) throw UsageError{a + " requires an argument"};
@@ -549,6 +555,8 @@ Cmd parse_args(int argc, char** argv, Options& opt) {
       opt.verify = true;
     } else if (cmd == Cmd::run && flag("--deterministic")) {
       opt.deterministic = true;
+    } else if (cmd == Cmd::run && flag("--fast")) {
+      opt.fast = true;
     } else if (cmd == Cmd::gen && flag("--dims")) {
       opt.dims.clear();
       std::stringstream ss(v);

@@ -489,6 +489,16 @@ int choose_fast_kernel(Context& c, uint32_t mode, const float* const* in, float*
   mc.fast_e1 = mc.shard_e1;
   const char* e = std::getenv("MKB_FAST_KERNEL");
   std::string force = e ? e : "";
+  if (force.find(',') != std::string::npos) {  // per-mode list "k0,k1,..." (profiling runs)
+    std::string item;
+    size_t pos = 0;
+    for (uint32_t m = 0; m <= mode; ++m) {
+      const size_t comma = force.find(',', pos);
+      item = force.substr(pos, comma == std::string::npos ? std::string::npos : comma - pos);
+      pos = comma == std::string::npos ? force.size() : comma + 1;
+    }
+    force = item;
+  }
   if (c.force_fast_kernel >= 0) force = c.force_fast_kernel == 0 ? "s2" : (c.force_fast_kernel == 1 ? "stream" : "tiles");
   if (!force.empty()) mc.s2_force_k = -1;  // a forced kernel runs the cost model's plan
   const bool s2_ok = force != "stream" && force != "tiles" && prepare_stream2(c, mode);
@@ -512,6 +522,8 @@ int choose_fast_kernel(Context& c, uint32_t mode, const float* const* in, float*
 static bool mc_split(const Context& c, uint32_t mode) { return c.copies[mode].shard_split_row; }
 
 void launch_mttkrp(Context& c, uint32_t mode, const float* const* in, float* out, int exec) {
+  if (exec == MK_EXEC_REFERENCE)  // Scheme 1 parallel == deterministic
+    exec = c.copies[mode].scheme == MK_SCHEME1 ? MK_EXEC_DETERMINISTIC : MK_EXEC_FAST;
   NvtxRange nv(exec == MK_EXEC_FAST ? "spMTTKRP fast" :
                (exec == MK_EXEC_DETERMINISTIC ? "spMTTKRP deterministic" : "spMTTKRP partitioned"),
                mode);

@@ -143,6 +143,8 @@ void ensure_val64(Context& c, uint32_t mode) {
 
 void launch_mttkrp64(Context& c, uint32_t mode, const double* const* in, double* out, int exec) {
   ModeCopy& mc = c.copies[mode];
+  if (exec == MK_EXEC_REFERENCE)  // Scheme 1 parallel == deterministic
+    exec = mc.scheme == MK_SCHEME1 ? MK_EXEC_DETERMINISTIC : MK_EXEC_FAST;
   ensure_val64(c, mode);
   const size_t out_bytes = static_cast<size_t>(c.dims[mode]) * c.rank64 * sizeof(double);
   // rows without elements are zero (kernel.hpp:88); the fast kernel adds into zeros

@@ -211,6 +211,28 @@ __device__ __forceinline__ void flush(float4* outv, uint32_t row, float2 a0, flo
   }
 }
 
+#ifndef MKB_S2_GLD
+#define MKB_S2_GLD 0  // unstaged factor rows: 0 ld.global.nc, 1 ld.global.cg (L2 only),
+                      // 2 ld.global.nc.L1::no_allocate, 3 ld.global.nc.L1::evict_first
+#endif
+__device__ __forceinline__ float4 ldg_row(const float4* p) {
+#if MKB_S2_GLD == 1
+  return __ldcg(p);
+#elif MKB_S2_GLD == 2
+  float4 v;
+  asm("ld.global.nc.L1::no_allocate.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p));
+  return v;
+#elif MKB_S2_GLD == 3
+  float4 v;
+  asm("ld.global.nc.L1::evict_first.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p));
+  return v;
+#else
+  return __ldg(p);
+#endif
+}
+
 // Per-lane constants of one launch.
 template <int NIN>
 struct Lane {
@@ -241,7 +263,7 @@ struct Body {
 
   static __device__ __forceinline__ float4 gather(const Lane<NIN>& ln, int j, uint32_t c) {
     if (j >= NIN - K) return lds128(ln.sb[j] + c * (G * 16u));
-    return __ldg(ln.gb[j] + static_cast<size_t>(c) * G);
+    return ldg_row(ln.gb[j] + static_cast<size_t>(c) * G);
   }
   static __device__ __forceinline__ float4 outer_row(const Lane<NIN>& ln, uint32_t c) {
     if constexpr (OS) return lds128(ln.so + c * (G * 16u));
@@ -375,7 +397,74 @@ struct Body {
     consume<B>(ln, s, RB, (NB - 2) * B, rA, yA);
     consume<B>(ln, s, RB, (NB - 1) * B, rB, yB);
   }
+
+  // Lead-2 pipeline for plans with exactly ONE inner level gathered through L1/L2 (the rest
+  // staged): the L2-fed rows of batch k+2 are issued while batch k is consumed (twice the
+  // latency cover of chunk()), and the staged rows of batch k only just before its consume
+  // (shared-memory latency), so the extra lead costs no registers: three in-flight L2 row
+  // buffers plus one transient staged buffer, against two full buffers in chunk().
+  static constexpr int NG = NIN - K;  // inner levels gathered through L1/L2
+  template <int B, bool GLOB>
+  static __device__ __forceinline__ void gather_sel(const Lane<NIN>& ln, const uint32_t (&r)[4],
+                                                    float4 (&y)[NIN]) {
+    uint32_t c[4];
+    unpack<NI, NOUT>(r, ln.b0, ln.m0, ln.m1, c);
+#pragma unroll
+    for (int j = 0; j < NIN; ++j)
+      if ((j < NG) == GLOB) y[j] = gather(ln, j, c[j]);
+  }
+  template <int B>
+  static __device__ __forceinline__ void gsel(const Lane<NIN>& ln, const uint32_t (&r)[B][4],
+                                              float4 (&y)[B][NIN], bool glob) {
+#pragma unroll
+    for (int b = 0; b < B; ++b) {
+      if (glob)
+        gather_sel<B, true>(ln, r[b], y[b]);
+      else
+        gather_sel<B, false>(ln, r[b], y[b]);
+    }
+  }
+  // one step of the lead-2 pipeline: records of batch k+2 requested, staged rows of batch k
+  // gathered, batch k consumed, L2-fed rows of batch k+2 requested (when k+2 < NB)
+  template <int B, bool MORE>
+  static __device__ __forceinline__ void step2(const Lane<NIN>& ln, Seg& s, const uint8_t* RA,
+                                               const uint32_t* RB, uint32_t k,
+                                               const uint32_t (&rk)[B][4], float4 (&yk)[B][NIN],
+                                               uint32_t (&rn)[B][4], float4 (&yn)[B][NIN]) {
+    if constexpr (MORE) fetch<B>(RA, (k + 2) * B, rn);
+    gsel<B>(ln, rk, yk, false);
+    consume<B>(ln, s, RB, k * B, rk, yk);
+    if constexpr (MORE) gsel<B>(ln, rn, yn, true);
+  }
+  template <int B, int S>
+  static __device__ __forceinline__ void chunk_lead2(const Lane<NIN>& ln, Seg& s, const uint8_t* RA,
+                                                     const uint32_t* RB) {
+    constexpr int NB = S / B;
+    static_assert(NB % 3 == 0 && NB >= 6, "batches are processed in triples");
+    uint32_t r0[B][4], r1[B][4], r2[B][4];
+    float4 y0[B][NIN], y1[B][NIN], y2[B][NIN];
+    fetch<B>(RA, 0, r0);
+    fetch<B>(RA, B, r1);
+    gsel<B>(ln, r0, y0, true);
+    gsel<B>(ln, r1, y1, true);
+#pragma unroll 1
+    for (uint32_t k = 0; k < NB - 3; k += 3) {
+      step2<B, true>(ln, s, RA, RB, k, r0, y0, r2, y2);
+      step2<B, true>(ln, s, RA, RB, k + 1, r1, y1, r0, y0);
+      step2<B, true>(ln, s, RA, RB, k + 2, r2, y2, r1, y1);
+    }
+    step2<B, true>(ln, s, RA, RB, NB - 3, r0, y0, r2, y2);
+    step2<B, false>(ln, s, RA, RB, NB - 2, r1, y1, r0, y0);
+    step2<B, false>(ln, s, RA, RB, NB - 1, r2, y2, r1, y1);
+  }
 };
+
+#ifndef MKB_S2_XITEM
+#define MKB_S2_XITEM 0  // 1: record tiles prefetched across work items
+#endif
+#ifndef MKB_S2_LEAD
+#define MKB_S2_LEAD 1  // 2: chunk_lead2 for plans with one L1/L2-fed inner level
+#endif
 
 // Shared memory: [header: mbarriers (fixed, so ring phases persist across the modes of a fused
 // sweep) at 0, the current mode's Args at kArgsOff][staged factor slices][outer factor]
@@ -465,9 +554,42 @@ __device__ __forceinline__ bool mode_body(const Args& a, uint8_t* smem, Persist&
   uint32_t it = ps.it;
   uint32_t staged = 0xffffffffu;
   const uint32_t i_end = a.cta_items[blockIdx.x + 1];
+#if MKB_S2_XITEM
+  // Record tiles stream across the CTA's items of the mode: lane 0 requests tile qt of item qi
+  // next (one bulk copy of the tile's records + slow keys into ring stage iss & 1), keeping two
+  // tiles in flight, so an item's first tiles land while the previous item still runs.
+  uint32_t qi = a.cta_items[blockIdx.x], qt = 0, q_tile0 = 0, q_tiles = 0, iss = it;
+  bool q_loaded = false;
+  auto request = [&]() {
+    while (qi < i_end) {
+      if (!q_loaded) {
+        const WDesc dq = a.wdesc[qi * NW + wid];
+        q_tile0 = dq.tile0;
+        q_tiles = dq.tiles;
+        q_loaded = true;
+      }
+      if (qt < q_tiles) break;
+      ++qi;
+      qt = 0;
+      q_loaded = false;
+    }
+    if (qi >= i_end) return;
+    const int st = iss & 1;
+    mbar_arrive_tx(&wbar[st], BA + BB);
+    tma_load_1d(ring + st * (BA + BB), gT + (static_cast<size_t>(q_tile0) + qt) * (BA + BB),
+                BA + BB, &wbar[st]);
+    ++qt;
+    ++iss;
+  };
+  if (lane == 0) {
+    request();
+    request();
+  }
+#endif
   for (uint32_t ii = a.cta_items[blockIdx.x]; ii < i_end; ++ii) {
     const Item item = a.items[ii];
     const WDesc d = a.wdesc[ii * NW + wid];
+#if !MKB_S2_XITEM
     auto issue = [&](uint32_t t, int st) {  // one bulk copy: the tile's records + slow keys
       mbar_arrive_tx(&wbar[st], BA + BB);
       tma_load_1d(ring + st * (BA + BB), gT + (static_cast<size_t>(d.tile0) + t) * (BA + BB),
@@ -477,6 +599,7 @@ __device__ __forceinline__ bool mode_body(const Args& a, uint8_t* smem, Persist&
       if (d.tiles > 0) issue(0, it & 1);
       if (d.tiles > 1) issue(1, (it + 1) & 1);
     }
+#endif
     __syncwarp();
     // (re)stage the block's factor slices (and the outer factor with the first block)
     if constexpr (K > 0 || OS) {
@@ -527,9 +650,16 @@ __device__ __forceinline__ bool mode_body(const Args& a, uint8_t* smem, Persist&
       const uint32_t* RB = reinterpret_cast<const uint32_t*>(ring + st * (BA + BB) + BA) + gw * KS;
       // the last chunk of a group is padded with copies of its last record (value 0, no
       // flag), so every chunk runs the same pipelined path
-      Bd::template chunk<B, S>(ln, s, RA, RB);
+      if constexpr (MKB_S2_LEAD == 2 && Bd::NG == 1)
+        Bd::template chunk_lead2<B, S>(ln, s, RA, RB);
+      else
+        Bd::template chunk<B, S>(ln, s, RA, RB);
       __syncwarp();  // the whole warp is done with this stage
+#if MKB_S2_XITEM
+      if (lane == 0) request();
+#else
       if (lane == 0 && t + 2 < d.tiles) issue(t + 2, st);
+#endif
     }
     // the group's last run
     Bd::fold(s);

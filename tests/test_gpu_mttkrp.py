@@ -263,3 +263,27 @@ def test_sweep_host_and_async_agree(mk):
         assert np.array_equal(ctx.output(d), ref[d])
 
 
+
+
+def test_reference_exec_contract(mk):
+    """SPEC.md:271/403 (acceptance.cpp:250-256): Scheme 1 parallel runs are bit-identical to
+    deterministic runs.  MK_EXEC_REFERENCE (the C++ drop-in's default) honours that; Scheme 2
+    copies run the fast path and stay within tolerance.  Covers the acceptance case (mixed
+    schemes at kappa 8) and a uniform 3-mode tensor at kappa 148."""
+    cases = [([60, 2, 40], 900, 8, 8), ([300, 200, 100], 60_000, 148, 32)]
+    for dims, nnz, kappa, rank in cases:
+        t = mk.generate_synthetic(dims, nnz, seed=77)
+        f = mk.random_factors(dims, rank, 7)
+        for policy in (mk.SchemePolicy.scheme1_only, mk.SchemePolicy.adaptive,
+                       mk.SchemePolicy.scheme2_only):
+            plans = mk.build_mode_plans(t, kappa, mk.Strategy.cyclic, policy)
+            det = mk.mttkrp_all_modes(t, plans, f, mk.ExecConfig(kappa, 32, True), False)
+            for _ in range(2):
+                ref = mk.mttkrp_all_modes(t, plans, f, mk.ExecConfig(kappa, 32, False, reference=True),
+                                          False)
+                for d, p in enumerate(plans):
+                    if p.scheme == mk.Scheme.scheme1:
+                        assert np.array_equal(ref[d].data.view(np.uint32), det[d].data.view(np.uint32)), \
+                            (dims, policy, d)
+                    else:
+                        assert mk.verify_against(ref[d], det[d].data)[0] <= 1e-5, (dims, policy, d)
