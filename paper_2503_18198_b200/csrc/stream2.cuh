@@ -460,10 +460,14 @@ struct Body {
 };
 
 #ifndef MKB_S2_XITEM
-#define MKB_S2_XITEM 0  // 1: record tiles prefetched across work items
+// 1: record tiles prefetched across work items.  Measured on B200 (cfg5): 2.090 -> 2.038 ms
+// alone, but 1.963 -> 2.020 ms on top of the lead-2 pipeline, so off by default.
+#define MKB_S2_XITEM 0
 #endif
 #ifndef MKB_S2_LEAD
-#define MKB_S2_LEAD 1  // 2: chunk_lead2 for plans with one L1/L2-fed inner level
+// 2: chunk_lead2 for plans with exactly one L1/L2-fed inner level (cfg1, cfg5: K = 1).
+// Measured on B200: cfg5 2.090 -> 1.963 ms, cfg1 0.0620 -> 0.0599 ms; 1 = chunk() only.
+#define MKB_S2_LEAD 2
 #endif
 
 // Shared memory: [header: mbarriers (fixed, so ring phases persist across the modes of a fused

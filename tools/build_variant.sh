@@ -8,6 +8,6 @@ R=$(cd "$(dirname "$0")/.." && pwd)
 O=$R/variants/build_$name
 rm -rf $O; mkdir -p $O
 cp -p $R/paper_2503_18198_b200/build/*.o $O/
-rm -f $O/stream2_n*.o
+rm -f $O/stream2_*.o $O/abi.o
 make -s -j16 -C $R/paper_2503_18198_b200 OBJ=$O LIB=$R/variants/lib$name.so EXTRA="$flags" $R/variants/lib$name.so 2>&1 | grep -v 'ptxas warning' || true
 ls -la $R/variants/lib$name.so

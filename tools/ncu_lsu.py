@@ -72,6 +72,10 @@ def fold(tag, cfgs):
             "lsu_wavefronts_per_sweep": wf,
             "lsu_shared_wavefronts_per_sweep": s("l1tex__data_pipe_lsu_wavefronts_mem_shared.sum"),
             "lsu_global_ld_wavefronts_per_sweep": s("l1tex__t_output_wavefronts_pipe_lsu_mem_global_op_ld.sum"),
+            "lsu_lgds_wavefronts_per_sweep": s("l1tex__data_pipe_lsu_wavefronts_mem_lgds.sum"),
+            "data_bank_reads_per_sweep": s("l1tex__data_bank_reads.sum"),
+            "data_bank_writes_per_sweep": s("l1tex__data_bank_writes.sum"),
+            "shared_ld_bank_conflicts_per_sweep": s("l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_ld.sum"),
             "lsu_bytes_per_sweep": wf * 128.0,
             "dram_bytes_per_sweep": s("dram__bytes_read.sum") + s("dram__bytes_write.sum"),
             "l2_to_l1_bytes_per_sweep": s("l1tex__m_xbar2l1tex_read_bytes.sum"),
