@@ -22,6 +22,7 @@
 #include <cstdlib>
 #include <vector>
 
+#include "als_inverse.cuh"
 #include "context.cuh"
 
 namespace mkb {
@@ -132,17 +133,6 @@ __device__ void smem_gemm(const double* Am, uint32_t lda, const double* Bm, uint
 // Block-level V⁻¹ of the symmetric positive definite V = ⊛_{w≠d} G_w by Gauss-Jordan on
 // [V | I] (fp64, SMEM); Jacobi pseudo-inverse when a pivot <= 1e-12 max diag(V).  On return
 // A[:, R:] holds the (pseudo-)inverse.  Returns whether the fallback ran.
-// 1/x to ~1 ulp: the SFU's approximation plus two Newton steps (a division is a long
-// dependent sequence on the pivot chain).
-__device__ __forceinline__ double recip(double x) {
-  double r;
-  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
-  double e = fma(-x, r, 1.0);
-  r = fma(r, e, r);
-  e = fma(-x, r, 1.0);
-  return fma(r, e, r);
-}
-
 // Gauss-Jordan on [V | I] (R x 2R, in A) with every thread holding one fixed segment of one
 // row in registers for all R steps: per step only the pivot row and the pivot column pass
 // through (double-buffered) shared memory, one barrier.  Returns false on a pivot
@@ -186,6 +176,10 @@ __device__ bool gj_registers(double* A, double vmax) {
   return true;
 }
 
+#ifndef ALS_INV
+#define ALS_INV 1  // 1: sweep_inverse (symmetric, R³/2); 0: gj_registers (R³ on [V | I])
+#endif
+
 template <int RT, int NTH>
 __device__ bool block_inverse(const double* __restrict__ grams, uint32_t n, uint32_t d, uint32_t R,
                               double* A, double* T, double* fac, double* scratch) {
@@ -210,7 +204,10 @@ __device__ bool block_inverse(const double* __restrict__ grams, uint32_t n, uint
   }
   __syncthreads();
   if constexpr (RT > 0 && NTH % RT == 0 && (2 * RT) % (NTH / RT) == 0) {
-    if (gj_registers<RT, NTH>(A, vmax)) return false;
+    bool ok;
+    if constexpr (ALS_INV == 1 && RT >= 16) ok = sweep_inverse<RT, NTH>(A, vmax);
+    else ok = gj_registers<RT, NTH>(A, vmax);
+    if (ok) return false;
     __syncthreads();  // singular: the Jacobi pseudo-inverse below
   } else {
     // Gauss-Jordan without pivoting (V is SPD), one barrier per pivot: step j reads X and writes

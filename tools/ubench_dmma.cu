@@ -73,7 +73,9 @@ void run(const char* name, K kern, int threads, double flops_per_thread_iter) {
   cudaFree(buf);
 }
 
+void latencies();
 int main() {
+  latencies();
   run("DFMA 8 chains", k_dfma<8>, 256, 8);
   run("DFMA 8 chains", k_dfma<8>, 1024, 8);
   run("DFMA 16 chains", k_dfma<16>, 1024, 16);
@@ -82,4 +84,39 @@ int main() {
   run("DMMA m8n8k4 4 acc", k_dmma<4>, 1024, 4 * 8);
   run("DMMA m8n8k4 8 acc", k_dmma<8>, 1024, 8 * 8);
   return 0;
+}
+
+// ---- latencies (one thread, dependent chains) -------------------------------------------
+__global__ void k_lat(double* out, double s, long long* cyc) {
+  double a = s;
+  long long t0 = clock64();
+  for (int i = 0; i < 1024; ++i) a = fma(a, 0.999999, 1e-7);
+  long long t1 = clock64();
+  double r = s;
+  for (int i = 0; i < 256; ++i) asm volatile("rcp.approx.ftz.f64 %0, %0;" : "+d"(r));
+  long long t2 = clock64();
+  float f = (float)s;
+  for (int i = 0; i < 1024; ++i) f = fmaf(f, 0.999999f, 1e-7f);
+  long long t3 = clock64();
+  double q = s;
+  for (int i = 0; i < 256; ++i) q = 1.0 / (q + 1.0);
+  long long t4 = clock64();
+  out[0] = a + r + f + q;
+  cyc[0] = t1 - t0;
+  cyc[1] = t2 - t1;
+  cyc[2] = t3 - t2;
+  cyc[3] = t4 - t3;
+}
+
+void latencies() {
+  double* o;
+  long long* c;
+  cudaMalloc(&o, 8);
+  cudaMalloc(&c, 32);
+  k_lat<<<1, 1>>>(o, 1.5, c);
+  k_lat<<<1, 1>>>(o, 1.5, c);
+  long long h[4];
+  cudaMemcpy(h, c, 32, cudaMemcpyDeviceToHost);
+  printf("latency: DFMA %.1f cyc, rcp.approx.f64 %.1f cyc, FFMA %.1f cyc, 1/(q+1) f64 div %.1f cyc\n",
+         h[0] / 1024.0, h[1] / 256.0, h[2] / 1024.0, h[3] / 256.0);
 }
