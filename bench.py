@@ -290,6 +290,8 @@ def run_config(args, name, rank, world, local_rank, stream, with_cpu):
     infos = [ctx.plan_info(d) for d in range(n)]
     distinct = [int(i.distinct_rows) for i in infos]
     ctx.upload_factors(factors)
+    if args.plan == "model":  # reproducible plans: the cost model's choice, no timed autotune
+        ctx.set_plan_mode(mk.PLAN_MODEL)
     b_iter = float(sum(algorithmic_bytes(dims, t.nnz, R, distinct)))
 
     ex = None
@@ -445,7 +447,7 @@ def run_config(args, name, rank, world, local_rank, stream, with_cpu):
     launches_per_sweep = 1 if fused else sum(f["launches"] for f in fast)
     rec = {
         "value": ms, "unit": "ms", "ms_per_step": ms,
-        "config": {"workload": f"{name}: {cfg['desc']}", "kappa": kappa,
+        "config": {"workload": f"{name}: {cfg['desc']}", "kappa": kappa, "plan": args.plan,
                    "policy": "adaptive", "strategy": "cyclic",
                    "schemes": [int(i.scheme) for i in infos],
                    "l2": "flushed between timed steps (memset 2x L2 on the launch stream)",
@@ -542,6 +544,8 @@ def main():
     ap.add_argument("--only", action="store_true",
                     help="only the --config workload (no cfg1-cfg4 sub-records)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--plan", default="timed", choices=["timed", "model"],
+                    help="fast-path plan choice: timed autotune (default) or the cost model only")
     ap.add_argument("--no-cpu", action="store_true",
                     help="skip the cpu_baseline (kernel-tuning runs only)")
     ap.add_argument("--profile", action="store_true",

@@ -120,6 +120,14 @@ int mk_fast_path_info(mk_context* ctx, uint32_t mode, mk_fast_info* info);
  * tiles) or restore the one-time timed choice (-1).  A forced kernel that has no
  * specialisation for the shape falls back along 0 -> 1 -> 2. */
 int mk_set_fast_kernel(mk_context* ctx, int kernel);
+/* How the fast path picks its kernel and shared-memory plan per mode copy (no reference
+ * counterpart: the reference has one executor).  MK_PLAN_TIMED (default): the first fast call
+ * of a mode times the candidates on the actual inputs (L2 flushed) and keeps the fastest.
+ * MK_PLAN_MODEL: the cost model's choice, no timing -- a pure function of the tensor, rank,
+ * kappa and device SM count, so the plan (and mk_fast_path_info) is the same on every run
+ * and box.  Resets the per-mode choices. */
+enum { MK_PLAN_TIMED = 0, MK_PLAN_MODEL = 1 };
+int mk_set_plan_mode(mk_context* ctx, int mode);
 /* ModePlan export (layout.hpp:47-64): order[nnz], partition_offsets[kappa+1],
  * owned_flat[owned_total] (concatenated owned_indices), owned_offsets[kappa+1].
  * Any output pointer may be NULL to skip it. */

@@ -627,6 +627,15 @@ std::vector<T> element_update(const SparseTensorCOO<T>& t, std::size_t element,
   return acc;
 }
 
+// Extension (no reference counterpart): how the fast path picks its plan for the tensor the
+// plans were built from.  timed (default): candidates timed on the first fast call of each
+// mode; model: the cost model's plan, no timing, the same on every run and box.
+enum class PlanMode { timed = MK_PLAN_TIMED, model = MK_PLAN_MODEL };
+inline void set_plan_mode(const std::vector<ModePlan>& plans, PlanMode mode) {
+  if (plans.empty()) throw error("kernel: expected one plan per mode");
+  detail::check(mk_set_plan_mode(plans[0].device->ctx, static_cast<int>(mode)));
+}
+
 // kernel.hpp:161-169 on the device.
 template <typename T>
 FactorMatrix<T> mttkrp_mode(const SparseTensorCOO<T>& t, const ModePlan& plan,

@@ -53,11 +53,12 @@ _LIB_NAME = "libmttkrp_b200.so"
 
 MK_OK, MK_EINVAL, MK_ENOMEM, MK_ECUDA, MK_ENONFINITE, MK_ESTATE, MK_ENCCL = range(7)
 EXEC_FAST, EXEC_DETERMINISTIC, EXEC_PARTITIONED, EXEC_REFERENCE = 0, 1, 2, 3
+PLAN_TIMED, PLAN_MODEL = 0, 1
 
 EXPORTED_SYMBOLS = [
     "mk_last_error", "mk_version", "mk_device_count", "mk_device_sm_count", "mk_create", "mk_destroy",
     "mk_set_stream", "mk_synchronize", "mk_tensor_upload", "mk_tensor_norm2",
-    "mk_build_plans", "mk_get_plan_info", "mk_fast_path_info", "mk_set_fast_kernel", "mk_plan_export", "mk_mode_degrees",
+    "mk_build_plans", "mk_get_plan_info", "mk_fast_path_info", "mk_set_fast_kernel", "mk_set_plan_mode", "mk_plan_export", "mk_mode_degrees",
     "mk_copy_export", "mk_factors_upload", "mk_factor_upload", "mk_factor_download",
     "mk_mttkrp_mode", "mk_mttkrp_all_modes", "mk_sweep_async", "mk_mttkrp_mode_async",
     "mk_output_download",
@@ -158,6 +159,7 @@ def load_library() -> C.CDLL:
             "mk_get_plan_info": (i32, [vp, u32, P(_PlanInfo)]),
             "mk_fast_path_info": (i32, [vp, u32, P(_FastInfo)]),
             "mk_set_fast_kernel": (i32, [vp, i32]),
+            "mk_set_plan_mode": (i32, [vp, i32]),
             "mk_plan_export": (i32, [vp, u32, vp, vp, vp, vp]),
             "mk_mode_degrees": (i32, [vp, u32, vp]),
             "mk_copy_export": (i32, [vp, u32, vp, vp]),
@@ -426,6 +428,11 @@ class Context:
     def set_fast_kernel(self, kernel: int):
         """Force the fast path's kernel (0 level-ordered, 1 fiber-ordered, 2 tiles; -1 = timed choice)."""
         _check(self.lib.mk_set_fast_kernel(self.h, int(kernel)))
+
+    def set_plan_mode(self, mode: int):
+        """PLAN_TIMED (0, default): time the candidate plans on the first fast call of a mode;
+        PLAN_MODEL (1): the cost model's plan, no timing (reproducible across runs and boxes)."""
+        _check(self.lib.mk_set_plan_mode(self.h, int(mode)))
 
     def plan_export(self, mode: int):
         info = self.plan_info(mode)

@@ -308,6 +308,22 @@ int mk_set_fast_kernel(mk_context* ctx, int kernel) {
   });
 }
 
+int mk_set_plan_mode(mk_context* ctx, int mode) {
+  return guarded([&] {
+    need_ctx(ctx);
+    if (mode != MK_PLAN_TIMED && mode != MK_PLAN_MODEL)
+      fail(MK_EINVAL, "kernel: plan mode must be MK_PLAN_TIMED or MK_PLAN_MODEL");
+    Context& c = ctx->c;
+    c.plan_mode = mode;
+    for (uint32_t d = 0; d < kMaxModes; ++d) {
+      c.copies[d].fast_kernel = -1;  // re-choose
+      c.copies[d].s2 = ModeCopy::Stream2();
+      c.copies[d].s2_force_k = -1;
+      c.copies[d].s2_no_os = false;
+    }
+  });
+}
+
 int mk_plan_export(mk_context* ctx, uint32_t mode, uint64_t* order, uint64_t* partition_offsets,
                    uint32_t* owned_flat, uint64_t* owned_offsets) {
   return guarded([&] {

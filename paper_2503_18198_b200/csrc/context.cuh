@@ -152,6 +152,7 @@ struct Context {
   DevBuf<unsigned long long> nonfinite;
   PinnedWord nonfinite_host;
   DevBuf<uint8_t> flush_buf;
+  int plan_mode = MK_PLAN_TIMED;  // mk_set_plan_mode
   int force_fast_kernel = -1;  // mk_set_fast_kernel: -1 timed choice, else 0 / 1 / 2
   DevBuf<uint32_t> s2sync;  // streaming kernel: finished-CTA counter + non-finite flag
   SortScratch scratch;

@@ -501,6 +501,11 @@ int choose_fast_kernel(Context& c, uint32_t mode, const float* const* in, float*
   }
   if (c.force_fast_kernel >= 0) force = c.force_fast_kernel == 0 ? "s2" : (c.force_fast_kernel == 1 ? "stream" : "tiles");
   if (!force.empty()) mc.s2_force_k = -1;  // a forced kernel runs the cost model's plan
+  if (force.empty() && c.plan_mode == MK_PLAN_MODEL) {  // the cost model's choice, no timing
+    if (prepare_stream2(c, mode)) return mc.fast_kernel = 0;
+    if (!mc.shard_split_row && prepare_stream(c, mode)) return mc.fast_kernel = 1;
+    return mc.fast_kernel = 2;
+  }
   const bool s2_ok = force != "stream" && force != "tiles" && prepare_stream2(c, mode);
   // the fiber-ordered records permute elements inside rows: no partial (shard-split) rows
   const bool st_ok = force != "s2" && force != "tiles" && !mc.shard_split_row &&

@@ -464,6 +464,9 @@ struct Body {
 // alone, but 1.963 -> 2.020 ms on top of the lead-2 pipeline, so off by default.
 #define MKB_S2_XITEM 0
 #endif
+#ifndef MKB_S2_LEAD_NG2
+#define MKB_S2_LEAD_NG2 0  // 1: the lead-2 pipeline also for two L1/L2-fed inner levels
+#endif
 #ifndef MKB_S2_LEAD
 // 2: chunk_lead2 for plans with exactly one L1/L2-fed inner level (cfg1, cfg5: K = 1).
 // Measured on B200: cfg5 2.090 -> 1.963 ms, cfg1 0.0620 -> 0.0599 ms; 1 = chunk() only.
@@ -654,7 +657,7 @@ __device__ __forceinline__ bool mode_body(const Args& a, uint8_t* smem, Persist&
       const uint32_t* RB = reinterpret_cast<const uint32_t*>(ring + st * (BA + BB) + BA) + gw * KS;
       // the last chunk of a group is padded with copies of its last record (value 0, no
       // flag), so every chunk runs the same pipelined path
-      if constexpr (MKB_S2_LEAD == 2 && Bd::NG == 1)
+      if constexpr (MKB_S2_LEAD == 2 && (Bd::NG == 1 || (MKB_S2_LEAD_NG2 && Bd::NG == 2)))
         Bd::template chunk_lead2<B, S>(ln, s, RA, RB);
       else
         Bd::template chunk<B, S>(ln, s, RA, RB);

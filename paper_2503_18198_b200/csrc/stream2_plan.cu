@@ -761,7 +761,18 @@ bool launch_sweep2(Context& c, const float* const* in, float* const* outs) {
   // costs at most 6% over the per-mode choices (the fused launch saves more than that).
   bool same_k = true;
   for (uint32_t d = 1; d < c.n; ++d) same_k &= c.copies[d].s2.k == p0.k;
-  if (!same_k) {
+  if (!same_k && c.plan_mode == MK_PLAN_MODEL) {
+    // reproducible plans: the smallest modelled K (always plannable) for every mode
+    uint32_t kc = c.copies[0].s2.k;
+    for (uint32_t d = 1; d < c.n; ++d) kc = std::min(kc, c.copies[d].s2.k);
+    for (uint32_t d = 0; d < c.n; ++d) {
+      ModeCopy& mc = c.copies[d];
+      if (mc.s2.k == kc) continue;
+      mc.s2 = ModeCopy::Stream2();
+      mc.s2_force_k = static_cast<int>(kc);
+      if (!prepare_stream2(c, d)) return false;
+    }
+  } else if (!same_k) {
     float best_sum = 0.f, common = 1e30f;
     int kc = -1;
     for (uint32_t d = 0; d < c.n; ++d) {

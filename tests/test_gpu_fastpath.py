@@ -312,3 +312,28 @@ def test_sharded_ranges_timed_choice(mk, orc):
             if len(own):
                 err = np.abs(got[own] - want[d][own]).max() / max(1.0, np.abs(want[d][own]).max())
                 assert err <= 1e-4, (r, d, err, c.fast_path_info(d).as_dict())
+
+
+def test_model_plan_mode_reproducible(mk, orc):
+    """mk_set_plan_mode(MK_PLAN_MODEL): no timed autotune, so two independent contexts pick
+    the same kernel and plan for every mode (and the fused sweep stays within 1e-4)."""
+    dims = [183, 24, 1140, 1717]
+    t = mk.generate_synthetic(dims, 400_000, seed=3)
+    f = [m.data for m in mk.random_factors(dims, 32, 1)]
+    infos, outs = [], []
+    for _ in range(2):
+        c = mk.Context()
+        c.upload_tensor(t)
+        c.build_plans(148)
+        c.set_plan_mode(mk.PLAN_MODEL)
+        c.upload_factors(f)
+        c.sweep_async(False, False)
+        c.synchronize()
+        infos.append([c.fast_path_info(d).as_dict() for d in range(4)])
+        outs.append([c.output(d) for d in range(4)])
+    assert infos[0] == infos[1]
+    assert all(i["kernel"] in (0, 1, 2) for i in infos[0])
+    for d in range(4):
+        want = orc.mttkrp(dims, t.coords, t.values, f, d)
+        assert mk.verify_against(outs[0][d], want)[0] <= 1e-4
+        assert mk.verify_against(outs[1][d], want)[0] <= 1e-4
