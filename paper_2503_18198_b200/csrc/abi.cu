@@ -168,6 +168,13 @@ int mk_destroy(mk_context* ctx) {
     cudaSetDevice(ctx->c.device);
     cudaStreamSynchronize(ctx->c.stream);
     comm_destroy(ctx->c);
+    if (ctx->c.als_graph_exec) cudaGraphExecDestroy(static_cast<cudaGraphExec_t>(ctx->c.als_graph_exec));
+    if (ctx->c.als_side) {
+      cudaStreamSynchronize(ctx->c.als_side);
+      cudaStreamDestroy(ctx->c.als_side);
+      cudaEventDestroy(ctx->c.als_ev_upd);
+      cudaEventDestroy(ctx->c.als_ev_inv);
+    }
     cudaStream_t own = ctx->c.own_stream;
     delete ctx;
     if (own) cudaStreamDestroy(own);

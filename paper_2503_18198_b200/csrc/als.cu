@@ -82,6 +82,8 @@ struct UpdArgs {
   unsigned int* bar;   // grid barrier counter (monotonic)
   unsigned int target; // barrier target for this launch
   unsigned long long* prof;  // MKB_ALS_PROF: phase timestamps of CTA 0 (ns), else null
+  const double* vinv;        // V⁻¹ precomputed by k_als_inverse (R x R), else null
+  const int* vinv_status;    // its fallback flag
 };
 
 // C (R x R, ldc) = op(A) · B in fp64 shared memory, op(A)(r, k) = A[r*lda + k] or (TA)
@@ -400,7 +402,14 @@ __global__ void __launch_bounds__(NTH) k_als_update(const UpdArgs u) {
   __syncthreads();
   // phase 2
   stamp(2);
-  const bool fell_back = block_inverse<RT, NTH>(u.grams, u.n, u.d, R, A, T, fac, scratch);
+  bool fell_back;
+  if (u.vinv) {  // computed on the side stream during this mode's spMTTKRP
+    for (uint32_t p = threadIdx.x; p < RR; p += blockDim.x) A[(p / R) * W2 + R + p % R] = __ldcg(&u.vinv[p]);
+    fell_back = __ldcg(u.vinv_status) != 0;
+    __syncthreads();
+  } else {
+    fell_back = block_inverse<RT, NTH>(u.grams, u.n, u.d, R, A, T, fac, scratch);
+  }
   stamp(3);
   // (Pm shares the inverse's ping-pong buffer: loaded after it)
   for (uint32_t p = threadIdx.x; p < RR; p += blockDim.x) Pm[p] = __ldcg(&u.P[p]);
@@ -477,6 +486,23 @@ __global__ void __launch_bounds__(NTH) k_als_update(const UpdArgs u) {
   stamp(5);
 }
 
+// V_d⁻¹ alone, on one CTA (the side stream of an overlapped CPD-ALS iteration): it depends
+// only on the Grams G_w (w != d), so it runs while mode d's spMTTKRP occupies the other SMs.
+template <int RT, int NTH>
+__global__ void __launch_bounds__(NTH) k_als_inverse(const double* __restrict__ grams, uint32_t n,
+                                                     uint32_t d, uint32_t Rr, double* vinv,
+                                                     int* status) {
+  extern __shared__ double dsm[];
+  const uint32_t R = RT ? RT : Rr, RR = R * R, W2 = 2 * R;
+  double* A = dsm;
+  double* T = A + 2 * RR;
+  double* scratch = T + 2 * RR;
+  double* fac = scratch + RR;
+  const bool fell_back = block_inverse<RT, NTH>(grams, n, d, R, A, T, fac, scratch);
+  for (uint32_t p = threadIdx.x; p < RR; p += blockDim.x) vinv[p] = A[(p / R) * W2 + R + p % R];
+  if (threadIdx.x == 0) *status = fell_back ? 1 : 0;
+}
+
 size_t upd_smem(uint32_t R) {
   return sizeof(double) * (5 * R * R + 2 * R) + sizeof(float) * (R * R + kGramRows * R);
 }
@@ -527,7 +553,7 @@ void als_prepare(Context& c) {
 
 // Y_d = M_d V⁻¹ diag(1/λ) with V = ⊛_{w≠d} G_w; G_d, λ and (last mode) the fit terms.
 // M_d is the (possibly all-gathered) MTTKRP output in c.outputs[d].
-void als_update_mode(Context& c, uint32_t d) {
+void als_update_mode(Context& c, uint32_t d, bool pre_inverse) {
   NvtxRange nv("CPD-ALS update", d);
   als_prepare(c);
   const uint32_t R = c.rank, n = c.n;
@@ -550,6 +576,8 @@ void als_update_mode(Context& c, uint32_t d) {
   const bool do_prof = std::getenv("MKB_ALS_PROF") != nullptr;  // per-phase times to stderr
   if (do_prof) c.als_prof.resize(8);
   u.prof = do_prof ? c.als_prof.get() : nullptr;
+  u.vinv = pre_inverse ? c.als_vinv.get() : nullptr;
+  u.vinv_status = pre_inverse ? c.als_vinv_status.get() : nullptr;
   const unsigned grid = static_cast<unsigned>(std::min<uint64_t>(
       c.num_sms, std::max<uint64_t>(1, (u.rows + kGramRows - 1) / kGramRows)));
   u.target = (c.als_bar_count += grid);
@@ -589,15 +617,102 @@ void als_fit(Context& c, double* fit, float* lambda_host) {
   *fit = 1.0 - std::sqrt(resid2) / std::sqrt(c.norm2);
 }
 
+// V_d⁻¹ on the side stream (one CTA).
+static void launch_inverse(Context& c, uint32_t d) {
+  const uint32_t R = c.rank;
+  const size_t smem = upd_smem(R);
+  auto go = [&](auto kern, unsigned nth) {
+    MKB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(smem)));
+    kern<<<1, nth, smem, c.als_side>>>(c.gram.get(), c.n, d, R, c.als_vinv.get(),
+                                       c.als_vinv_status.get());
+    MKB_LAUNCH();
+  };
+  if (R == 16) go(k_als_inverse<16, 256>, 256);
+  else if (R == 32) go(k_als_inverse<32, ALS_NTH32>, ALS_NTH32);
+  else if (R == 64) go(k_als_inverse<64, ALS_NTH64>, ALS_NTH64);
+  else go(k_als_inverse<0, 256>, 256);
+}
+
+// One CPD-ALS iteration.  V_d = ⊛_{w≠d} G_w depends only on the Grams, which are final once
+// mode d-1's update ran, so V_d⁻¹ (latency-bound, one SM: 6 us at R = 32, 37 us at R = 64) is
+// computed on a side stream WHILE mode d's spMTTKRP runs on the other SMs: the level-ordered
+// kernel is planned for SM count - 1 CTAs during ALS (plans cached per grid), and update(d)
+// reads V_d⁻¹ instead of computing it (R >= 64; MKB_ALS_OVERLAP=1/0 forces it on/off).
 void als_iteration(Context& c, double* fit, float* lambda_host) {
   als_prepare(c);
+  const uint32_t R = c.rank;
   const float* in[kMaxModes];
   for (uint32_t w = 0; w < c.n; ++w) in[w] = c.factors[w].get();
-  reset_nonfinite(c);
-  for (uint32_t d = 0; d < c.n; ++d) {
-    launch_mttkrp(c, d, in, c.outputs[d].get(), MK_EXEC_FAST);
-    als_update_mode(c, d);
+  // worth one SM only when the inverse is long: at R = 64 (cfg3: 0.758 -> 0.637 ms per
+  // iteration); at R = 32 the ~6 us inverse does not pay for the 148th CTA (cfg5 +0.7 %)
+  const char* ov = std::getenv("MKB_ALS_OVERLAP");
+  const bool overlap = c.n >= 2 && c.num_sms > 1 &&
+                       (ov && *ov ? ov[0] == '1' : R >= 64);
+  if (overlap) {
+    if (!c.als_side) {
+      MKB_CUDA(cudaStreamCreateWithFlags(&c.als_side, cudaStreamNonBlocking));
+      MKB_CUDA(cudaEventCreateWithFlags(&c.als_ev_upd, cudaEventDisableTiming));
+      MKB_CUDA(cudaEventCreateWithFlags(&c.als_ev_inv, cudaEventDisableTiming));
+    }
+    c.als_vinv.resize(static_cast<size_t>(R) * R);
+    c.als_vinv_status.resize(1);
   }
+  c.s2_grid = overlap ? c.num_sms - 1 : 0;
+  auto side_inverse = [&](uint32_t d) {  // after everything queued on the main stream so far
+    MKB_CUDA(cudaEventRecord(c.als_ev_upd, c.stream));
+    MKB_CUDA(cudaStreamWaitEvent(c.als_side, c.als_ev_upd, 0));
+    launch_inverse(c, d);
+    MKB_CUDA(cudaEventRecord(c.als_ev_inv, c.als_side));
+  };
+  // One iteration, replay-safe: the update kernels' grid-barrier targets and the MᵀM
+  // accumulators restart from zero every iteration.
+  auto body = [&] {
+    MKB_CUDA(cudaMemsetAsync(c.als_bar.get(), 0, sizeof(unsigned int), c.stream));
+    c.als_bar_count = 0;
+    MKB_CUDA(cudaMemsetAsync(c.mtm.get(), 0, 2 * sizeof(double) * R * R, c.stream));
+    c.als_epoch = 0;
+    reset_nonfinite(c);
+    if (overlap) side_inverse(0);
+    for (uint32_t d = 0; d < c.n; ++d) {
+      launch_mttkrp(c, d, in, c.outputs[d].get(), MK_EXEC_FAST);
+      if (overlap) MKB_CUDA(cudaStreamWaitEvent(c.stream, c.als_ev_inv, 0));
+      als_update_mode(c, d, overlap);
+      if (overlap && d + 1 < c.n) side_inverse(d + 1);
+    }
+  };
+  // CUDA graph: the first iteration with a given state runs eagerly (one-time kernel choices
+  // and plans synchronise and allocate), the second is captured, later ones replay it while
+  // nothing was re-planned or re-allocated since (g_devmem_epoch).  MKB_GRAPH=0 / MKB_ALS_PROF
+  // run every iteration eagerly.
+  const char* ge = std::getenv("MKB_GRAPH");
+  const bool use_graph = !(ge && ge[0] == '0') && std::getenv("MKB_ALS_PROF") == nullptr;
+  const uint64_t key = (static_cast<uint64_t>(R) << 32) | (static_cast<uint64_t>(c.n) << 8) |
+                       (overlap ? 1u : 0u);
+  const unsigned long long ep = g_devmem_epoch.load();
+  if (use_graph && c.als_graph_exec && c.als_graph_key == key && c.als_graph_epoch == ep) {
+    MKB_CUDA(cudaGraphLaunch(static_cast<cudaGraphExec_t>(c.als_graph_exec), c.stream));
+  } else if (use_graph && c.als_graph_key == key && c.als_eager_epoch == ep) {
+    if (c.als_graph_exec) {
+      cudaGraphExecDestroy(static_cast<cudaGraphExec_t>(c.als_graph_exec));
+      c.als_graph_exec = nullptr;
+    }
+    cudaGraph_t g = nullptr;
+    MKB_CUDA(cudaStreamBeginCapture(c.stream, cudaStreamCaptureModeRelaxed));
+    body();
+    MKB_CUDA(cudaStreamEndCapture(c.stream, &g));
+    cudaGraphExec_t ex = nullptr;
+    MKB_CUDA(cudaGraphInstantiate(&ex, g, 0));
+    cudaGraphDestroy(g);
+    c.als_graph_exec = ex;
+    c.als_graph_epoch = g_devmem_epoch.load();
+    MKB_CUDA(cudaGraphLaunch(ex, c.stream));
+  } else {
+    body();
+    c.als_graph_key = key;
+    c.als_eager_epoch = g_devmem_epoch.load();
+  }
+  c.s2_grid = 0;  // sweeps keep every SM (the ALS plans stay cached for the next iteration)
   als_fit(c, fit, lambda_host);
 }
 

@@ -3,6 +3,7 @@
 
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cstdint>
 #include <cstdio>
 #include <stdexcept>
@@ -68,6 +69,11 @@ struct PinnedWord {
 
 // Owning device allocation (cudaMalloc; 256-byte aligned, so float4 rows are aligned
 // whenever the row stride is a multiple of 4 floats).
+// Bumped whenever device memory a kernel may have captured is freed or re-pointed (DevBuf
+// release / view) or a fast-path kernel choice changes: a captured CUDA graph is replayed only
+// while this is unchanged since its capture (als.cu).
+inline std::atomic<unsigned long long> g_devmem_epoch{0};
+
 template <typename T>
 class DevBuf {
  public:
@@ -103,12 +109,16 @@ class DevBuf {
   // A non-owning window into another buffer (the factor / output arenas, context.cuh).
   void view(T* p, size_t n) {
     release();
+    ++g_devmem_epoch;
     p_ = p;
     n_ = n;
     owned_ = false;
   }
   void release() {
-    if (p_ && owned_) cudaFree(p_);
+    if (p_ && owned_) {
+      cudaFree(p_);
+      ++g_devmem_epoch;
+    }
     p_ = nullptr;
     n_ = 0;
     owned_ = true;

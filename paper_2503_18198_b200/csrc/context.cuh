@@ -80,6 +80,7 @@ struct ModeCopy {
     bool no_os = false;                        // planned with the outer factor unstaged
     uint32_t rank = 0;
     uint64_t key_e0 = ~0ull, key_e1 = ~0ull;  // shard range the plan was built for
+    unsigned key_grid = 0;                     // CTAs the work split was built for
     uint32_t ni = 0, nout = 0, k = 0, aw = 2;  // input levels, outer levels, staged levels
     uint32_t nt = 512;                         // threads per CTA
     bool os = false;                           // outer factor staged in shared memory
@@ -153,6 +154,7 @@ struct Context {
   PinnedWord nonfinite_host;
   DevBuf<uint8_t> flush_buf;
   int plan_mode = MK_PLAN_TIMED;  // mk_set_plan_mode
+  int s2_grid = 0;  // level-ordered CTAs (0: SM count; CPD-ALS leaves one SM to its inverse)
   int force_fast_kernel = -1;  // mk_set_fast_kernel: -1 timed choice, else 0 / 1 / 2
   DevBuf<uint32_t> s2sync;  // streaming kernel: finished-CTA counter + non-finite flag
   SortScratch scratch;
@@ -169,6 +171,17 @@ struct Context {
   DevBuf<double> als_scalars;
   DevBuf<int> als_status;
   DevBuf<unsigned long long> als_prof;  // MKB_ALS_PROF: phase timestamps of the update
+  // overlapped inverse: V_d⁻¹ computed on a side stream (one CTA) while mode d's spMTTKRP runs
+  // on the other SMs (als.cu als_iteration)
+  cudaStream_t als_side = nullptr;
+  cudaEvent_t als_ev_upd = nullptr, als_ev_inv = nullptr;
+  DevBuf<double> als_vinv;  // R x R
+  DevBuf<int> als_vinv_status;  // 1: the Jacobi pseudo-inverse ran
+  // the iteration captured as a CUDA graph (als.cu): replayed while the key and the device
+  // memory epoch match the capture; the eager iteration before it records its own epoch
+  void* als_graph_exec = nullptr;  // cudaGraphExec_t
+  uint64_t als_graph_key = ~0ull;
+  unsigned long long als_graph_epoch = ~0ull, als_eager_epoch = ~0ull;
   bool grams_valid = false;
   bool last_sweep_fused = false;  // the last sweep() ran as one k_sweep2 launch
 
@@ -211,7 +224,7 @@ void sweep_sharded(Context& c);
 void als_iteration_sharded(Context& c, double* fit, float* lambda_host);
 // ALS pieces (als.cu), used by the single-GPU iteration and the sharded driver.
 void als_prepare(Context& c);
-void als_update_mode(Context& c, uint32_t d);
+void als_update_mode(Context& c, uint32_t d, bool pre_inverse = false);
 void als_fit(Context& c, double* fit, float* lambda_host);
 // Streaming TMA kernel (stream.cu); false when the shape has no specialisation.
 bool launch_stream(Context& c, uint32_t mode, const float* const* in, float* out);

@@ -484,6 +484,7 @@ int choose_fast_kernel(Context& c, uint32_t mode, const float* const* in, float*
   if (mc.fast_kernel >= 0 && mc.fast_rank == c.rank && mc.fast_e0 == mc.shard_e0 &&
       mc.fast_e1 == mc.shard_e1)
     return mc.fast_kernel;
+  ++g_devmem_epoch;  // a (re)choice: captured graphs of the old choice are stale
   mc.fast_rank = c.rank;
   mc.fast_e0 = mc.shard_e0;
   mc.fast_e1 = mc.shard_e1;

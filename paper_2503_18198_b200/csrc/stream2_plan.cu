@@ -221,8 +221,9 @@ void rank_of_row_build(Context& c, uint32_t mode, DevBuf<uint32_t>& rank) {
 bool prepare_stream2(Context& c, uint32_t mode) {
   ModeCopy& mc = c.copies[mode];
   ModeCopy::Stream2& p = mc.s2;
+  const unsigned want_grid = static_cast<unsigned>(c.s2_grid ? c.s2_grid : c.num_sms);
   if (p.tried && p.rank == c.rank && p.key_e0 == mc.shard_e0 && p.key_e1 == mc.shard_e1 &&
-      p.k_req == mc.s2_force_k && p.no_os == mc.s2_no_os)
+      p.k_req == mc.s2_force_k && p.no_os == mc.s2_no_os && p.key_grid == want_grid)
     return p.ok;
   p = ModeCopy::Stream2();
   p.tried = true;
@@ -231,6 +232,7 @@ bool prepare_stream2(Context& c, uint32_t mode) {
   p.rank = c.rank;
   p.key_e0 = mc.shard_e0;
   p.key_e1 = mc.shard_e1;
+  p.key_grid = want_grid;
   if (env_int("MKB_STREAM2", 1) == 0) return false;
   if (c.n < 3 || c.n > 5 || c.nnz == 0 || (c.rank != 32 && c.rank != 64)) return false;
   if (c.nnz >= 0x7fffff00ull) return false;
@@ -496,7 +498,7 @@ bool prepare_stream2(Context& c, uint32_t mode) {
   //    a warp's groups stream chunk-interleaved records.
   const uint32_t S = s2::seg_len(p.aw), RS = s2::rec_stride(p.aw), KS = s2::key_stride(p.aw);
   const uint32_t NW = p.nt / 32, GPW = 32 / G, NG = NW * GPW;
-  const unsigned grid = static_cast<unsigned>(c.num_sms);
+  const unsigned grid = want_grid;  // CTAs (SM count, or one fewer while CPD-ALS overlaps)
   const uint64_t E0 = E0s, E1 = E1s;
   std::vector<WDesc> wd;
   std::vector<uint32_t> gstart, dblk, items, cta(grid + 1, 0);

@@ -111,3 +111,53 @@ def test_rank_deficient_uses_pinv(mk):
     fit, lam = ctx.cpd_als_iter()
     Y, lam64, fit64, _ = als_oracle.als_iteration(dims, t.coords, t.values, f0)
     assert np.isfinite(fit) and abs(fit - fit64) < 5e-3
+
+
+@pytest.mark.parametrize("overlap", ["0", "1"])
+def test_overlapped_inverse_matches_serial(mk, monkeypatch, overlap):
+    """The side-stream V_d⁻¹ (k_als_inverse during mode d's spMTTKRP on SM count - 1 CTAs)
+    gives the same iteration as the serial update: factors, lambda and fit to the fast
+    spMTTKRP's own run-to-run spread (its atomics are not bit-reproducible, 1e-4)."""
+    dims = [300, 200, 150, 40]
+    t = mk.generate_powerlaw(dims, 80_000, 1.0, 5)
+    f0 = [m.data for m in mk.random_factors(dims, 64, 2)]
+    res = []
+    for ov in ("0", overlap):
+        monkeypatch.setenv("MKB_ALS_OVERLAP", ov)
+        ctx = mk.Context()
+        ctx.upload_tensor(t)
+        ctx.build_plans(148)
+        ctx.upload_factors(f0)
+        fit, lam = ctx.cpd_als_iter()
+        res.append((fit, lam, [ctx.download_factor(d) for d in range(4)]))
+    (f_a, l_a, y_a), (f_b, l_b, y_b) = res
+    assert abs(f_a - f_b) <= 1e-5
+    assert np.allclose(l_a, l_b, rtol=1e-4)
+    for d in range(4):
+        assert mk.verify_against(y_b[d], y_a[d])[0] <= 1e-4
+
+
+@pytest.mark.parametrize("rank", [32, 64])
+def test_graph_replay_matches_eager(mk, monkeypatch, rank):
+    """The captured CPD-ALS iteration (eager, capture, then replays) follows the eager
+    iteration, also across a re-plan in between (an unchained sweep re-plans the level-ordered
+    kernel for every SM; the stale graph must not be replayed)."""
+    dims = [400, 300, 200]
+    t = mk.generate_synthetic(dims, 120_000, seed=4)
+    f0 = [m.data for m in mk.random_factors(dims, rank, 3)]
+    fits = {}
+    for g in ("0", "1"):
+        monkeypatch.setenv("MKB_GRAPH", g)
+        ctx = mk.Context()
+        ctx.upload_tensor(t)
+        ctx.build_plans(148)
+        ctx.upload_factors(f0)
+        seq = []
+        for it in range(6):
+            if it == 3:
+                ctx.sweep_async(False, False)
+            seq.append(ctx.cpd_als_iter()[0])
+        fits[g] = (seq, [ctx.download_factor(d) for d in range(3)])
+    assert np.allclose(fits["0"][0], fits["1"][0], rtol=0, atol=1e-6), fits
+    for d in range(3):
+        assert mk.verify_against(fits["1"][1][d], fits["0"][1][d])[0] <= 1e-4
