@@ -332,7 +332,7 @@ def test_model_plan_mode_reproducible(mk, orc):
         infos.append([c.fast_path_info(d).as_dict() for d in range(4)])
         outs.append([c.output(d) for d in range(4)])
     assert infos[0] == infos[1]
-    assert all(i["kernel"] in (0, 1, 2) for i in infos[0])
+    assert all(i["kernel"] != "undecided" for i in infos[0])
     for d in range(4):
         want = orc.mttkrp(dims, t.coords, t.values, f, d)
         assert mk.verify_against(outs[0][d], want)[0] <= 1e-4
