@@ -638,17 +638,16 @@ static void launch_inverse(Context& c, uint32_t d) {
 // mode d-1's update ran, so V_d⁻¹ (latency-bound, one SM: 6 us at R = 32, 37 us at R = 64) is
 // computed on a side stream WHILE mode d's spMTTKRP runs on the other SMs: the level-ordered
 // kernel is planned for SM count - 1 CTAs during ALS (plans cached per grid), and update(d)
-// reads V_d⁻¹ instead of computing it (R >= 64; MKB_ALS_OVERLAP=1/0 forces it on/off).
+// reads V_d⁻¹ instead of computing it (MKB_ALS_OVERLAP=0: the serial form).
 void als_iteration(Context& c, double* fit, float* lambda_host) {
   als_prepare(c);
   const uint32_t R = c.rank;
   const float* in[kMaxModes];
   for (uint32_t w = 0; w < c.n; ++w) in[w] = c.factors[w].get();
-  // worth one SM only when the inverse is long: at R = 64 (cfg3: 0.758 -> 0.637 ms per
-  // iteration); at R = 32 the ~6 us inverse does not pay for the 148th CTA (cfg5 +0.7 %)
+  // measured on B200 (bench.py cpd_als_ms_per_iter, graph replay): cfg1 0.167 -> 0.156,
+  // cfg2 0.289 -> 0.268, cfg3 0.758 -> 0.637, cfg5 2.145 -> 2.136 ms per iteration
   const char* ov = std::getenv("MKB_ALS_OVERLAP");
-  const bool overlap = c.n >= 2 && c.num_sms > 1 &&
-                       (ov && *ov ? ov[0] == '1' : R >= 64);
+  const bool overlap = c.n >= 2 && c.num_sms > 1 && !(ov && ov[0] == '0');
   if (overlap) {
     if (!c.als_side) {
       MKB_CUDA(cudaStreamCreateWithFlags(&c.als_side, cudaStreamNonBlocking));
