@@ -1,7 +1,8 @@
 #!/usr/bin/env python3
 """Small workload for compute-sanitizer (tools/sanitize.sh): every device code path of the
 library once — format build, the fused level-ordered sweep, each fast kernel forced per mode,
-the deterministic / partitioned / fp64 executors, a CPD-ALS iteration, a simulated 2-rank
+the deterministic / partitioned / fp64 executors, CPD-ALS iterations (eager, captured and
+replayed, side-stream inverse and serial), the cost-model plans, a simulated 2-rank
 shard exchange and the one-rank NCCL sweep — on tensors small enough for the tools' overhead."""
 import os
 import sys
@@ -34,7 +35,14 @@ def run(dims, nnz, R, gen="uniform"):
     c.mttkrp_all_modes_f64(False, False)
     c.upload_factors(f)
     if R <= 64:
-        c.cpd_als_iter()
+        for _ in range(3):             # eager, graph capture, graph replay (side-stream inverse)
+            c.cpd_als_iter()
+        os.environ["MKB_ALS_OVERLAP"] = "0"
+        c.cpd_als_iter()               # the serial update (inverse inside k_als_update)
+        os.environ.pop("MKB_ALS_OVERLAP")
+    c.set_plan_mode(mk.PLAN_MODEL)     # the cost model's plans (lead-2 pipeline where K = 1)
+    c.sweep_async(False, False)
+    c.set_plan_mode(mk.PLAN_TIMED)
     c.synchronize()
     # 2-rank exchange simulated with two contexts
     import torch
@@ -67,6 +75,7 @@ def run(dims, nnz, R, gen="uniform"):
 
 if __name__ == "__main__":
     run([60, 50, 40], 20_000, 32)
+    run([300, 300, 300], 60_000, 32)
     run([50, 7, 40, 9], 20_000, 32)
     run([40, 30, 20, 17], 15_000, 64, "powerlaw")
     run([30, 20, 25, 15, 300], 10_000, 32)
