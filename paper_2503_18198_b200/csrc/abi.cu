@@ -1,6 +1,7 @@
 // C-ABI entry points (include/mttkrp_b200.h).  Each converts internal exceptions into an
 // mk_status plus a thread-local message, mirroring how the reference surfaces
 // mttkrp::error (types.hpp:18-21).
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -168,6 +169,15 @@ int mk_destroy(mk_context* ctx) {
     cudaSetDevice(ctx->c.device);
     cudaStreamSynchronize(ctx->c.stream);
     comm_destroy(ctx->c);
+    if (ctx->c.io_h2d) {
+      cudaStreamSynchronize(ctx->c.io_h2d);
+      cudaStreamSynchronize(ctx->c.io_d2h);
+      cudaStreamDestroy(ctx->c.io_h2d);
+      cudaStreamDestroy(ctx->c.io_d2h);
+      cudaEventDestroy(ctx->c.io_ev_main);
+      cudaEventDestroy(ctx->c.io_ev_h2d);
+      cudaEventDestroy(ctx->c.io_ev_d2h);
+    }
     if (ctx->c.als_graph_exec) cudaGraphExecDestroy(static_cast<cudaGraphExec_t>(ctx->c.als_graph_exec));
     if (ctx->c.als_side) {
       cudaStreamSynchronize(ctx->c.als_side);
@@ -616,6 +626,123 @@ int mk_output_download(mk_context* ctx, uint32_t mode, float* out) {
   });
 }
 
+// ---- host-buffer pipeline (mk_sweep_host) ------------------------------------------------
+// cuStreamWaitValue32 / cuStreamWriteValue32 through the runtime's driver entry points (the
+// library links the static runtime only).  Null when the driver does not offer them.
+namespace {
+using PfnValue32 = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+struct MemOps {
+  PfnValue32 wait = nullptr, write = nullptr;
+};
+const MemOps& memops() {
+  static const MemOps m = [] {
+    MemOps r;
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuStreamWaitValue32", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      r.wait = reinterpret_cast<PfnValue32>(p);
+    p = nullptr;
+    if (cudaGetDriverEntryPoint("cuStreamWriteValue32", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      r.write = reinterpret_cast<PfnValue32>(p);
+    if (!r.wait || !r.write) r = MemOps();
+    cudaGetLastError();
+    return r;
+  }();
+  return m;
+}
+
+// One unchained fused sweep with host buffers, copies overlapped with the kernel: factor
+// H2D copies on one stream (each followed by a flag write), the fused kernel on the context
+// stream (each mode waits in-kernel for the flags of the factors it reads), and per-mode D2H
+// copies on a third stream (each waits for its mode's done flag).  The modes run in the order
+// that exposes the fewest bytes: first the mode whose own factor is largest (it needs only
+// the others), last the one with the smallest output.  Returns false (nothing issued) when
+// the fused sweep is not already the fast path's choice, or stream memory ops are missing.
+bool sweep_host_pipelined(Context& c, const float* const* factors, float* const* outs) {
+  const MemOps& mo = memops();
+  const char* e = std::getenv("MKB_PIPE");
+  if (!mo.wait || (e && e[0] == '0') || !c.last_sweep_fused) return false;
+  for (uint32_t d = 0; d < c.n; ++d) {
+    const ModeCopy& mc = c.copies[d];
+    if (mc.fast_kernel != 0 || mc.fast_rank != c.rank) return false;
+  }
+  if (!c.io_h2d) {
+    MKB_CUDA(cudaStreamCreateWithFlags(&c.io_h2d, cudaStreamNonBlocking));
+    MKB_CUDA(cudaStreamCreateWithFlags(&c.io_d2h, cudaStreamNonBlocking));
+    MKB_CUDA(cudaEventCreateWithFlags(&c.io_ev_main, cudaEventDisableTiming));
+    MKB_CUDA(cudaEventCreateWithFlags(&c.io_ev_h2d, cudaEventDisableTiming));
+    MKB_CUDA(cudaEventCreateWithFlags(&c.io_ev_d2h, cudaEventDisableTiming));
+  }
+  if (!c.io_flags.get()) {
+    c.io_flags.resize(2 * kMaxModes);
+    MKB_CUDA(cudaMemsetAsync(c.io_flags.get(), 0, 2 * kMaxModes * sizeof(uint32_t), c.stream));
+    c.io_epoch = 0;
+  }
+  SweepIO io{};
+  io.fin = c.io_flags.get();
+  io.fdone = c.io_flags.get() + kMaxModes;
+  io.epoch = ++c.io_epoch;
+  uint32_t first = 0, last = ~0u;
+  for (uint32_t d = 1; d < c.n; ++d)
+    if (c.dims[d] > c.dims[first]) first = d;
+  for (uint32_t d = 0; d < c.n; ++d)
+    if (d != first && (last == ~0u || c.dims[d] < c.dims[last])) last = d;
+  uint32_t m = 0;
+  io.order[m++] = first;
+  for (uint32_t d = 0; d < c.n; ++d)
+    if (d != first && d != last) io.order[m++] = d;
+  io.order[m++] = last;
+  // both copy streams start after everything already queued (earlier kernels read the factors)
+  MKB_CUDA(cudaEventRecord(c.io_ev_main, c.stream));
+  MKB_CUDA(cudaStreamWaitEvent(c.io_h2d, c.io_ev_main, 0));
+  MKB_CUDA(cudaStreamWaitEvent(c.io_d2h, c.io_ev_main, 0));
+  auto h2d = [&](uint32_t w) {
+    MKB_CUDA(cudaMemcpyAsync(c.factors[w].get(), factors[w],
+                             static_cast<size_t>(c.dims[w]) * c.rank * sizeof(float),
+                             cudaMemcpyHostToDevice, c.io_h2d));
+    if (mo.write(reinterpret_cast<CUstream>(c.io_h2d),
+                 reinterpret_cast<CUdeviceptr>(io.fin + w), io.epoch, 0) != CUDA_SUCCESS)
+      fail(MK_ECUDA, "cuStreamWriteValue32 failed");
+  };
+  for (uint32_t w = 0; w < c.n; ++w)
+    if (w != first) h2d(w);
+  h2d(first);
+  const float* in[kMaxModes];
+  float* dev_out[kMaxModes];
+  for (uint32_t w = 0; w < c.n; ++w) {
+    in[w] = c.factors[w].get();
+    dev_out[w] = c.outputs[w].get();
+  }
+  if (!launch_sweep2(c, in, dev_out, &io)) {  // cannot happen after a fused sweep; be safe
+    MKB_CUDA(cudaEventRecord(c.io_ev_h2d, c.io_h2d));
+    MKB_CUDA(cudaStreamWaitEvent(c.stream, c.io_ev_h2d, 0));
+    c.last_sweep_fused = false;
+    sweep(c, 0, MK_EXEC_FAST);
+    for (uint32_t d = 0; d < c.n; ++d)
+      MKB_CUDA(cudaMemcpyAsync(outs[d], c.outputs[d].get(),
+                               static_cast<size_t>(c.dims[d]) * c.rank * sizeof(float),
+                               cudaMemcpyDeviceToHost, c.stream));
+    return true;
+  }
+  for (uint32_t k = 0; k < c.n; ++k) {
+    const uint32_t d = io.order[k];
+    if (mo.wait(reinterpret_cast<CUstream>(c.io_d2h), reinterpret_cast<CUdeviceptr>(io.fdone + d),
+                io.epoch, CU_STREAM_WAIT_VALUE_GEQ) != CUDA_SUCCESS)
+      fail(MK_ECUDA, "cuStreamWaitValue32 failed");
+    MKB_CUDA(cudaMemcpyAsync(outs[d], c.outputs[d].get(),
+                             static_cast<size_t>(c.dims[d]) * c.rank * sizeof(float),
+                             cudaMemcpyDeviceToHost, c.io_d2h));
+  }
+  MKB_CUDA(cudaEventRecord(c.io_ev_h2d, c.io_h2d));
+  MKB_CUDA(cudaEventRecord(c.io_ev_d2h, c.io_d2h));
+  MKB_CUDA(cudaStreamWaitEvent(c.stream, c.io_ev_h2d, 0));
+  MKB_CUDA(cudaStreamWaitEvent(c.stream, c.io_ev_d2h, 0));
+  return true;
+}
+}  // namespace
+
 int mk_sweep_host(mk_context* ctx, const float* const* factors, float* const* outs, int chain,
                   int exec) {
   return guarded([&] {
@@ -623,6 +750,10 @@ int mk_sweep_host(mk_context* ctx, const float* const* factors, float* const* ou
     Context& c = ctx->c;
     need_plans(c);
     need_factors(c);
+    if (!chain && exec == MK_EXEC_FAST && sweep_host_pipelined(c, factors, outs)) {
+      check_nonfinite(c);
+      return;
+    }
     copy_factors_in(c, factors);
     sweep(c, chain, exec);
     if (host_packed(c, reinterpret_cast<const void* const*>(outs))) {  // one copy: every copy pays ~6 us of PCIe latency

@@ -177,6 +177,11 @@ struct Context {
   cudaEvent_t als_ev_upd = nullptr, als_ev_inv = nullptr;
   DevBuf<double> als_vinv;  // R x R
   DevBuf<int> als_vinv_status;  // 1: the Jacobi pseudo-inverse ran
+  // host-buffer pipeline of mk_sweep_host (abi.cu): H2D and D2H copy streams, flags
+  cudaStream_t io_h2d = nullptr, io_d2h = nullptr;
+  cudaEvent_t io_ev_main = nullptr, io_ev_h2d = nullptr, io_ev_d2h = nullptr;
+  DevBuf<uint32_t> io_flags;  // [0, kMaxModes): factor H2D epochs; [kMaxModes, 2k): mode done
+  uint32_t io_epoch = 0;
   // the iteration captured as a CUDA graph (als.cu): replayed while the key and the device
   // memory epoch match the capture; the eager iteration before it records its own epoch
   void* als_graph_exec = nullptr;  // cudaGraphExec_t
@@ -239,7 +244,17 @@ bool prepare_stream2(Context& c, uint32_t mode);
 bool launch_stream2(Context& c, uint32_t mode, const float* const* in, float* out);
 // One fused launch for an unchained all-mode sweep (when every mode shares the level-ordered
 // kernel's specialisation); false if not applicable (nothing launched).
-bool launch_sweep2(Context& c, const float* const* in, float* const* outs);
+// Host-buffer pipeline of an unchained fused sweep (abi.cu mk_sweep_host): the modes run in
+// `order`; slot m waits for the H2D flags of the factors it reads, and each finished mode
+// raises its done flag for the D2H copy stream.
+struct SweepIO {
+  const uint32_t* fin;   // per factor: epoch of its last H2D copy
+  uint32_t* fdone;       // per mode: epoch of its last completed output
+  uint32_t epoch;
+  uint32_t order[kMaxModes];
+};
+bool launch_sweep2(Context& c, const float* const* in, float* const* outs,
+                   const SweepIO* io = nullptr);
 // rank_of_row[row_seq[k]] = k for the copy's non-empty rows
 void rank_of_row_build(Context& c, uint32_t mode, DevBuf<uint32_t>& rank);
 void check_nonfinite(Context& c);  // synchronises; throws MK_ENONFINITE

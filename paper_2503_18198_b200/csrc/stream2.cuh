@@ -705,7 +705,8 @@ __device__ __forceinline__ bool mode_body(const Args& a, uint8_t* smem, Persist&
 // non-finite; the last CTA to finish the mode rescans its elements in the reference's order
 // and resets the mode's counters (and, after the launch's last mode, the zeroing counter).
 template <int NI, int NOUT, int G, int NT>
-__device__ __forceinline__ void mode_epilogue(const Args& a, bool bad, bool last_mode) {
+__device__ __forceinline__ void mode_epilogue(const Args& a, bool bad, bool last_mode,
+                                              uint32_t* done = nullptr, uint32_t epoch = 0) {
   const int tid = threadIdx.x, lane = tid & 31;
   if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(&a.sync[1], 1u);
   __shared__ uint32_t last;
@@ -723,6 +724,10 @@ __device__ __forceinline__ void mode_epilogue(const Args& a, bool bad, bool last
       a.sync[0] = 0;
       a.sync[1] = 0;
       if (last_mode) *a.zcnt = 0;
+      if (done) {  // the mode's output is complete: a copy stream may read it now
+        __threadfence_system();
+        asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(done), "r"(epoch) : "memory");
+      }
     }
   }
   __syncthreads();  // the next mode may reuse this mode's shared memory
@@ -765,7 +770,28 @@ __global__ void __launch_bounds__(NT, MINB) k_stream2(const Args a) {
 struct SweepArgs {
   Args m[kMaxModes];
   uint32_t nmodes;
+  // host-buffer pipeline (mk_sweep_host): slot m waits until fin[w] >= epoch for every factor
+  // w in need[m] (written by cuStreamWriteValue32 after each H2D copy) and, when done, sets
+  // fdone[mode[m]] = epoch (a copy stream waits on it before the D2H copy); fin == null: off
+  const uint32_t* fin;
+  uint32_t* fdone;
+  uint32_t epoch;
+  uint32_t need[kMaxModes];
+  uint32_t mode[kMaxModes];
 };
+
+// thread 0: spin until every flag in `need` has reached `epoch`
+__device__ __forceinline__ void wait_inputs(const uint32_t* fin, uint32_t need, uint32_t epoch) {
+  for (uint32_t w = 0; need; ++w, need >>= 1) {
+    if (!(need & 1u)) continue;
+    uint32_t v;
+    do {
+      asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(fin + w) : "memory");
+      if (static_cast<int>(v - epoch) >= 0) break;
+      __nanosleep(256);
+    } while (true);
+  }
+}
 
 template <int NI, int NOUT, int K, bool OS, int G, int B, int NT, int MINB>
 __global__ void __launch_bounds__(NT, MINB) k_sweep2(const SweepArgs sa) {
@@ -785,18 +811,21 @@ __global__ void __launch_bounds__(NT, MINB) k_sweep2(const SweepArgs sa) {
   Args* as = reinterpret_cast<Args*>(smem + kArgsOff);
   static_assert(kArgsOff + sizeof(Args) <= kHeader, "header too small");
   for (uint32_t m = 0; m < sa.nmodes; ++m) {
+    uint32_t need = 0, mode = 0;
     if (threadIdx.x == 0) {
       switch (m) {
-        case 0: *as = sa.m[0]; break;
-        case 1: *as = sa.m[1]; break;
-        case 2: *as = sa.m[2]; break;
-        case 3: *as = sa.m[3]; break;
-        default: *as = sa.m[4]; break;
+        case 0: *as = sa.m[0]; need = sa.need[0]; mode = sa.mode[0]; break;
+        case 1: *as = sa.m[1]; need = sa.need[1]; mode = sa.mode[1]; break;
+        case 2: *as = sa.m[2]; need = sa.need[2]; mode = sa.mode[2]; break;
+        case 3: *as = sa.m[3]; need = sa.need[3]; mode = sa.mode[3]; break;
+        default: *as = sa.m[4]; need = sa.need[4]; mode = sa.mode[4]; break;
       }
+      if (sa.fin) wait_inputs(sa.fin, need, sa.epoch);
     }
     __syncthreads();
     const bool bad = mode_body<NI, NOUT, K, OS, G, B, NT>(*as, smem, ps);
-    mode_epilogue<NI, NOUT, G, NT>(*as, bad, m + 1 == sa.nmodes);
+    mode_epilogue<NI, NOUT, G, NT>(*as, bad, m + 1 == sa.nmodes,
+                                   sa.fdone ? sa.fdone + mode : nullptr, sa.epoch);
   }
 }
 

@@ -751,7 +751,7 @@ bool launch_stream2(Context& c, uint32_t mode, const float* const* in, float* ou
 
 // One launch for an unchained all-mode sweep when every mode runs the level-ordered kernel
 // with the same specialisation; false (nothing launched) otherwise.
-bool launch_sweep2(Context& c, const float* const* in, float* const* outs) {
+bool launch_sweep2(Context& c, const float* const* in, float* const* outs, const SweepIO* io) {
   if (std::getenv("MKB_FUSE") && std::getenv("MKB_FUSE")[0] == '0') return false;
   const uint32_t G = c.rank / 4;
   size_t smem = 0;
@@ -834,7 +834,17 @@ bool launch_sweep2(Context& c, const float* const* in, float* const* outs) {
   static_assert(sizeof(s2::SweepArgs) <= 32000, "kernel parameter space");
   s2::SweepArgs sa{};
   sa.nmodes = c.n;
-  for (uint32_t d = 0; d < c.n; ++d) fill_args(c, d, in, outs[d], sa.m[d], sw + 4 + 2 * d, sw + 2);
+  for (uint32_t m = 0; m < c.n; ++m) {  // slot m runs mode order[m] (identity without io)
+    const uint32_t d = io ? io->order[m] : m;
+    fill_args(c, d, in, outs[d], sa.m[m], sw + 4 + 2 * m, sw + 2);
+    sa.mode[m] = d;
+    sa.need[m] = ((1u << c.n) - 1u) & ~(1u << d);
+  }
+  if (io) {
+    sa.fin = io->fin;
+    sa.fdone = io->fdone;
+    sa.epoch = io->epoch;
+  }
   cudaStream_t st = c.stream;
   const unsigned grid = p0.grid;
   switch (c.n * 100 + G) {

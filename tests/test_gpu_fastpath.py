@@ -337,3 +337,30 @@ def test_model_plan_mode_reproducible(mk, orc):
         want = orc.mttkrp(dims, t.coords, t.values, f, d)
         assert mk.verify_against(outs[0][d], want)[0] <= 1e-4
         assert mk.verify_against(outs[1][d], want)[0] <= 1e-4
+
+
+@pytest.mark.parametrize("pipe", ["1", "0"])
+def test_sweep_host_pipelined(mk, orc, monkeypatch, pipe):
+    """mk_sweep_host after a fused sweep overlaps the copies with the kernel (factor H2D on one
+    stream with flag writes, in-kernel waits per mode, per-mode D2H behind the done flags, modes
+    reordered): over several steps with new factors each time, every output matches the oracle
+    (MKB_PIPE=0: the serial path, same check)."""
+    monkeypatch.setenv("MKB_PIPE", pipe)
+    dims = [300, 500, 800]
+    R = 32
+    t = mk.generate_synthetic(dims, 200_000, seed=8)
+    c = mk.Context()
+    c.upload_tensor(t)
+    c.build_plans(148)
+    c.set_plan_mode(mk.PLAN_MODEL)  # the fused level-ordered sweep, independent of timing noise
+    c.upload_factors([m.data for m in mk.random_factors(dims, R, 1)])
+    c.sweep_async(False, False)
+    c.synchronize()
+    assert c.last_sweep_fused()
+    for step in range(4):
+        f = [m.data for m in mk.random_factors(dims, R, 10 + step)]
+        outs = [np.full((d, R), np.nan, np.float32) for d in dims]
+        c.sweep_host(f, outs)
+        for d in range(3):
+            want = orc.mttkrp(dims, t.coords, t.values, f, d)
+            assert mk.verify_against(outs[d], want)[0] <= 1e-4, (step, d)
