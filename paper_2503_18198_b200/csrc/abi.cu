@@ -177,6 +177,11 @@ int mk_destroy(mk_context* ctx) {
       cudaEventDestroy(ctx->c.io_ev_main);
       cudaEventDestroy(ctx->c.io_ev_h2d);
       cudaEventDestroy(ctx->c.io_ev_d2h);
+      for (uint32_t w = 0; w < kMaxModes; ++w)
+        if (ctx->c.io_ev_f[w]) {
+          cudaEventDestroy(ctx->c.io_ev_f[w]);
+          cudaEventDestroy(ctx->c.io_ev_done[w]);
+        }
     }
     if (ctx->c.als_graph_exec) cudaGraphExecDestroy(static_cast<cudaGraphExec_t>(ctx->c.als_graph_exec));
     if (ctx->c.als_side) {
@@ -660,20 +665,87 @@ const MemOps& memops() {
 // that exposes the fewest bytes: first the mode whose own factor is largest (it needs only
 // the others), last the one with the smallest output.  Returns false (nothing issued) when
 // the fused sweep is not already the fast path's choice, or stream memory ops are missing.
+// The same overlap when the modes run as separate launches (a per-mode kernel mix, cfg4):
+// stream events instead of in-kernel flags -- each mode's launch waits for the H2D events of
+// the factors it reads, and each output's D2H waits for its mode's event.  cfg4 moves a 111 MB
+// factor each way per step; ordered first, its mode computes while that factor's H2D (for
+// the other modes) and its own output's D2H run on the two copy engines.
+static void sweep_host_events(Context& c, const float* const* factors, float* const* outs,
+                              const uint32_t* order) {
+  for (uint32_t w = 0; w < c.n; ++w)
+    if (!c.io_ev_f[w]) {
+      MKB_CUDA(cudaEventCreateWithFlags(&c.io_ev_f[w], cudaEventDisableTiming));
+      MKB_CUDA(cudaEventCreateWithFlags(&c.io_ev_done[w], cudaEventDisableTiming));
+    }
+  auto h2d = [&](uint32_t w) {
+    MKB_CUDA(cudaMemcpyAsync(c.factors[w].get(), factors[w],
+                             static_cast<size_t>(c.dims[w]) * c.rank * sizeof(float),
+                             cudaMemcpyHostToDevice, c.io_h2d));
+    MKB_CUDA(cudaEventRecord(c.io_ev_f[w], c.io_h2d));
+  };
+  for (uint32_t w = 0; w < c.n; ++w)
+    if (w != order[0]) h2d(w);
+  h2d(order[0]);
+  const float* in[kMaxModes];
+  for (uint32_t w = 0; w < c.n; ++w) in[w] = c.factors[w].get();
+  for (uint32_t k = 0; k < c.n; ++k) {
+    const uint32_t d = order[k];
+    for (uint32_t w = 0; w < c.n; ++w)
+      if (w != d) MKB_CUDA(cudaStreamWaitEvent(c.stream, c.io_ev_f[w], 0));
+    launch_mttkrp(c, d, in, c.outputs[d].get(), MK_EXEC_FAST);
+    MKB_CUDA(cudaEventRecord(c.io_ev_done[d], c.stream));
+    MKB_CUDA(cudaStreamWaitEvent(c.io_d2h, c.io_ev_done[d], 0));
+    MKB_CUDA(cudaMemcpyAsync(outs[d], c.outputs[d].get(),
+                             static_cast<size_t>(c.dims[d]) * c.rank * sizeof(float),
+                             cudaMemcpyDeviceToHost, c.io_d2h));
+  }
+  // the factor every mode but the first reads arrived before those modes ran; the last H2D
+  // (order[0]'s own factor) is joined here, with the D2H copies
+  MKB_CUDA(cudaEventRecord(c.io_ev_h2d, c.io_h2d));
+  MKB_CUDA(cudaEventRecord(c.io_ev_d2h, c.io_d2h));
+  MKB_CUDA(cudaStreamWaitEvent(c.stream, c.io_ev_h2d, 0));
+  MKB_CUDA(cudaStreamWaitEvent(c.stream, c.io_ev_d2h, 0));
+}
+
 bool sweep_host_pipelined(Context& c, const float* const* factors, float* const* outs) {
   const MemOps& mo = memops();
   const char* e = std::getenv("MKB_PIPE");
-  if (!mo.wait || (e && e[0] == '0') || !c.last_sweep_fused) return false;
+  if (e && e[0] == '0') return false;
+  bool chosen = true, all_s2 = true;
   for (uint32_t d = 0; d < c.n; ++d) {
     const ModeCopy& mc = c.copies[d];
-    if (mc.fast_kernel != 0 || mc.fast_rank != c.rank) return false;
+    chosen &= mc.fast_kernel >= 0 && mc.fast_rank == c.rank && mc.fast_e0 == mc.shard_e0 &&
+              mc.fast_e1 == mc.shard_e1;
+    all_s2 &= mc.fast_kernel == 0;
   }
+  if (!chosen) return false;  // the first fast call (kernel choice, timing) runs unpipelined
+  const bool fused = c.last_sweep_fused && all_s2 && mo.wait;
   if (!c.io_h2d) {
     MKB_CUDA(cudaStreamCreateWithFlags(&c.io_h2d, cudaStreamNonBlocking));
     MKB_CUDA(cudaStreamCreateWithFlags(&c.io_d2h, cudaStreamNonBlocking));
     MKB_CUDA(cudaEventCreateWithFlags(&c.io_ev_main, cudaEventDisableTiming));
     MKB_CUDA(cudaEventCreateWithFlags(&c.io_ev_h2d, cudaEventDisableTiming));
     MKB_CUDA(cudaEventCreateWithFlags(&c.io_ev_d2h, cudaEventDisableTiming));
+  }
+  uint32_t order[kMaxModes];
+  {
+    uint32_t first = 0, last = ~0u, m = 0;
+    for (uint32_t d = 1; d < c.n; ++d)
+      if (c.dims[d] > c.dims[first]) first = d;
+    for (uint32_t d = 0; d < c.n; ++d)
+      if (d != first && (last == ~0u || c.dims[d] < c.dims[last])) last = d;
+    order[m++] = first;
+    for (uint32_t d = 0; d < c.n; ++d)
+      if (d != first && d != last) order[m++] = d;
+    order[m++] = last;
+  }
+  if (!fused) {
+    MKB_CUDA(cudaEventRecord(c.io_ev_main, c.stream));
+    MKB_CUDA(cudaStreamWaitEvent(c.io_h2d, c.io_ev_main, 0));
+    MKB_CUDA(cudaStreamWaitEvent(c.io_d2h, c.io_ev_main, 0));
+    sweep_host_events(c, factors, outs, order);
+    c.last_sweep_fused = false;
+    return true;
   }
   if (!c.io_flags.get()) {
     c.io_flags.resize(2 * kMaxModes);
@@ -684,16 +756,8 @@ bool sweep_host_pipelined(Context& c, const float* const* factors, float* const*
   io.fin = c.io_flags.get();
   io.fdone = c.io_flags.get() + kMaxModes;
   io.epoch = ++c.io_epoch;
-  uint32_t first = 0, last = ~0u;
-  for (uint32_t d = 1; d < c.n; ++d)
-    if (c.dims[d] > c.dims[first]) first = d;
-  for (uint32_t d = 0; d < c.n; ++d)
-    if (d != first && (last == ~0u || c.dims[d] < c.dims[last])) last = d;
-  uint32_t m = 0;
-  io.order[m++] = first;
-  for (uint32_t d = 0; d < c.n; ++d)
-    if (d != first && d != last) io.order[m++] = d;
-  io.order[m++] = last;
+  for (uint32_t d = 0; d < c.n; ++d) io.order[d] = order[d];
+  const uint32_t first = order[0];
   // both copy streams start after everything already queued (earlier kernels read the factors)
   MKB_CUDA(cudaEventRecord(c.io_ev_main, c.stream));
   MKB_CUDA(cudaStreamWaitEvent(c.io_h2d, c.io_ev_main, 0));

@@ -180,6 +180,7 @@ struct Context {
   // host-buffer pipeline of mk_sweep_host (abi.cu): H2D and D2H copy streams, flags
   cudaStream_t io_h2d = nullptr, io_d2h = nullptr;
   cudaEvent_t io_ev_main = nullptr, io_ev_h2d = nullptr, io_ev_d2h = nullptr;
+  cudaEvent_t io_ev_f[kMaxModes] = {}, io_ev_done[kMaxModes] = {};  // per-mode pipeline
   DevBuf<uint32_t> io_flags;  // [0, kMaxModes): factor H2D epochs; [kMaxModes, 2k): mode done
   uint32_t io_epoch = 0;
   // the iteration captured as a CUDA graph (als.cu): replayed while the key and the device

@@ -339,12 +339,12 @@ def test_model_plan_mode_reproducible(mk, orc):
         assert mk.verify_against(outs[1][d], want)[0] <= 1e-4
 
 
-@pytest.mark.parametrize("pipe", ["1", "0"])
-def test_sweep_host_pipelined(mk, orc, monkeypatch, pipe):
+@pytest.mark.parametrize("pipe,kernel", [("1", -1), ("0", -1), ("1", 1)])
+def test_sweep_host_pipelined(mk, orc, monkeypatch, pipe, kernel):
     """mk_sweep_host after a fused sweep overlaps the copies with the kernel (factor H2D on one
     stream with flag writes, in-kernel waits per mode, per-mode D2H behind the done flags, modes
     reordered): over several steps with new factors each time, every output matches the oracle
-    (MKB_PIPE=0: the serial path, same check)."""
+    (MKB_PIPE=0: the serial path; kernel 1: per-mode launches, the stream-event pipeline)."""
     monkeypatch.setenv("MKB_PIPE", pipe)
     dims = [300, 500, 800]
     R = 32
@@ -354,9 +354,11 @@ def test_sweep_host_pipelined(mk, orc, monkeypatch, pipe):
     c.build_plans(148)
     c.set_plan_mode(mk.PLAN_MODEL)  # the fused level-ordered sweep, independent of timing noise
     c.upload_factors([m.data for m in mk.random_factors(dims, R, 1)])
+    if kernel >= 0:
+        c.set_fast_kernel(kernel)
     c.sweep_async(False, False)
     c.synchronize()
-    assert c.last_sweep_fused()
+    assert c.last_sweep_fused() == (kernel < 0)
     for step in range(4):
         f = [m.data for m in mk.random_factors(dims, R, 10 + step)]
         outs = [np.full((d, R), np.nan, np.float32) for d in dims]
