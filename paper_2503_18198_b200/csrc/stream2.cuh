@@ -143,7 +143,7 @@ __device__ __forceinline__ void read_rec(const uint8_t* ringA, uint32_t i, uint3
 // inputs by ascending mode, __fmul_rn) and report each offending element's reference copy
 // position; the atomic minimum is the reference's first failing position.
 template <int NI, int NOUT, int G, int NW>
-__device__ __noinline__ void rescan_all(const Args& a) {
+__device__ __noinline__ void rescan_all(const Args& a, uint32_t t0, uint32_t tstride) {
   using L = Lay<NI, NOUT>;
   constexpr int S = seg_len(L::AW), RS = rec_stride(L::AW), KS = key_stride(L::AW);
   constexpr int GPW = 32 / G;
@@ -154,7 +154,7 @@ __device__ __noinline__ void rescan_all(const Args& a) {
     for (uint32_t w = 0; w < static_cast<uint32_t>(NW); ++w) {
       const WDesc d = a.wdesc[ii * NW + w];
       const uint32_t total = d.tiles * GPW * S;
-      for (uint32_t q = threadIdx.x; q < total; q += blockDim.x) {
+      for (uint32_t q = t0; q < total; q += tstride) {
         const uint32_t s = q % S, g = (q / S) % GPW, t = q / (S * GPW);
         const size_t tile = static_cast<size_t>(d.tile0) + t;
         const size_t slot = (tile * GPW + g) * RS + s;
@@ -459,6 +459,9 @@ struct Body {
   }
 };
 
+#ifndef MKB_S2_WARPEPI
+#define MKB_S2_WARPEPI 1  // fused sweep of unstaged plans: per-warp mode ends, no CTA barrier
+#endif
 #ifndef MKB_S2_XITEM
 // 1: record tiles prefetched across work items.  Measured on B200 (cfg5): 2.090 -> 2.038 ms
 // alone, but 1.963 -> 2.020 ms on top of the lead-2 pipeline, so off by default.
@@ -474,9 +477,9 @@ struct Body {
 #endif
 
 // Shared memory: [header: mbarriers (fixed, so ring phases persist across the modes of a fused
-// sweep) at 0, the current mode's Args at kArgsOff][staged factor slices][outer factor]
+// sweep) at 0, the modes' Args at kArgsOff][staged factor slices][outer factor]
 // [per-warp record rings].
-constexpr uint32_t kHeader = 1024, kArgsOff = 512;
+constexpr uint32_t kHeader = 2048, kArgsOff = 512;  // Args of up to kMaxModes modes at kArgsOff
 #ifndef MKB_S2_B
 #define MKB_S2_B 3  // elements per gather batch (8-B records)
 #endif
@@ -718,7 +721,8 @@ __device__ __forceinline__ void mode_epilogue(const Args& a, bool bad, bool last
   __syncthreads();
   if (last) {
     __threadfence();
-    if (*reinterpret_cast<volatile uint32_t*>(&a.sync[1])) rescan_all<NI, NOUT, G, NT / 32>(a);
+    if (*reinterpret_cast<volatile uint32_t*>(&a.sync[1]))
+      rescan_all<NI, NOUT, G, NT / 32>(a, threadIdx.x, blockDim.x);
     __syncthreads();
     if (tid == 0) {
       a.sync[0] = 0;
@@ -731,6 +735,40 @@ __device__ __forceinline__ void mode_epilogue(const Args& a, bool bad, bool last
     }
   }
   __syncthreads();  // the next mode may reuse this mode's shared memory
+}
+
+// The same end of a mode counted per WARP, with no CTA barrier: for plans with no shared-memory
+// staging (K = 0, outer factor unstaged) nothing in shared memory is shared between a CTA's
+// warps across modes (record rings and their barriers are per warp), so a warp that finishes
+// mode m starts its share of mode m + 1 at once instead of idling until the CTA's slowest
+// warp is done (power-law cfg3: ~10 % of stall samples sat in those barriers).  The last warp
+// of the grid to finish the mode does the rescan and resets.
+template <int NI, int NOUT, int G, int NT>
+__device__ __forceinline__ void mode_epilogue_warp(const Args& a, bool bad, bool last_mode,
+                                                   uint32_t* done, uint32_t epoch) {
+  const int lane = threadIdx.x & 31;
+  const bool any_bad = __any_sync(0xffffffffu, bad);
+  uint32_t last = 0;
+  if (lane == 0) {
+    if (any_bad) atomicOr(&a.sync[1], 1u);
+    __threadfence();
+    last = atomicAdd(&a.sync[0], 1u) == gridDim.x * (NT / 32) - 1;
+  }
+  last = __shfl_sync(0xffffffffu, last, 0);
+  if (last) {
+    __threadfence();
+    if (*reinterpret_cast<volatile uint32_t*>(&a.sync[1])) rescan_all<NI, NOUT, G, NT / 32>(a, lane, 32);
+    __syncwarp();
+    if (lane == 0) {
+      a.sync[0] = 0;
+      a.sync[1] = 0;
+      if (last_mode) *a.zcnt = 0;
+      if (done) {
+        __threadfence_system();
+        asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(done), "r"(epoch) : "memory");
+      }
+    }
+  }
 }
 
 template <int NT>
@@ -806,26 +844,55 @@ __global__ void __launch_bounds__(NT, MINB) k_sweep2(const SweepArgs sa) {
     atomicAdd(sa.m[0].zcnt, 1u);
   }
   Persist ps{0u, 0u, false};
-  // The mode's Args go to shared memory (static-index copies): indexing the kernel-parameter
-  // array with a runtime mode would put all of it on the local-memory stack.
+  // Every mode's Args go to shared memory once (static-index copies, thread m copies mode m):
+  // indexing the kernel-parameter array with a runtime mode would put all of it on the
+  // local-memory stack.
   Args* as = reinterpret_cast<Args*>(smem + kArgsOff);
-  static_assert(kArgsOff + sizeof(Args) <= kHeader, "header too small");
-  for (uint32_t m = 0; m < sa.nmodes; ++m) {
-    uint32_t need = 0, mode = 0;
-    if (threadIdx.x == 0) {
-      switch (m) {
-        case 0: *as = sa.m[0]; need = sa.need[0]; mode = sa.mode[0]; break;
-        case 1: *as = sa.m[1]; need = sa.need[1]; mode = sa.mode[1]; break;
-        case 2: *as = sa.m[2]; need = sa.need[2]; mode = sa.mode[2]; break;
-        case 3: *as = sa.m[3]; need = sa.need[3]; mode = sa.mode[3]; break;
-        default: *as = sa.m[4]; need = sa.need[4]; mode = sa.mode[4]; break;
-      }
-      if (sa.fin) wait_inputs(sa.fin, need, sa.epoch);
+  static_assert(kArgsOff + 5 * sizeof(Args) <= kHeader, "header too small");  // N <= 5
+  switch (threadIdx.x) {
+    case 0: as[0] = sa.m[0]; break;
+    case 1: if (sa.nmodes > 1) as[1] = sa.m[1]; break;
+    case 2: if (sa.nmodes > 2) as[2] = sa.m[2]; break;
+    case 3: if (sa.nmodes > 3) as[3] = sa.m[3]; break;
+    case 4: if (sa.nmodes > 4) as[4] = sa.m[4]; break;
+    default: break;
+  }
+  __syncthreads();
+  constexpr bool kWarpEpi = MKB_S2_WARPEPI && K == 0 && !OS;  // nothing shared across warps
+  const int lane = threadIdx.x & 31;
+  // static-index reads of the pipeline words of slot m (values of the kernel parameters)
+  auto slot_need = [&](uint32_t m) {
+    switch (m) {
+      case 0: return sa.need[0];
+      case 1: return sa.need[1];
+      case 2: return sa.need[2];
+      case 3: return sa.need[3];
+      default: return sa.need[4];
     }
-    __syncthreads();
-    const bool bad = mode_body<NI, NOUT, K, OS, G, B, NT>(*as, smem, ps);
-    mode_epilogue<NI, NOUT, G, NT>(*as, bad, m + 1 == sa.nmodes,
-                                   sa.fdone ? sa.fdone + mode : nullptr, sa.epoch);
+  };
+  auto slot_done = [&](uint32_t m) -> uint32_t* {
+    if (!sa.fdone) return nullptr;
+    switch (m) {
+      case 0: return sa.fdone + sa.mode[0];
+      case 1: return sa.fdone + sa.mode[1];
+      case 2: return sa.fdone + sa.mode[2];
+      case 3: return sa.fdone + sa.mode[3];
+      default: return sa.fdone + sa.mode[4];
+    }
+  };
+  for (uint32_t m = 0; m < sa.nmodes; ++m) {
+    if constexpr (kWarpEpi) {
+      if (sa.fin && lane == 0) wait_inputs(sa.fin, slot_need(m), sa.epoch);
+      __syncwarp();
+    } else {
+      if (sa.fin && threadIdx.x == 0) wait_inputs(sa.fin, slot_need(m), sa.epoch);
+      __syncthreads();
+    }
+    const bool bad = mode_body<NI, NOUT, K, OS, G, B, NT>(as[m], smem, ps);
+    if constexpr (kWarpEpi)
+      mode_epilogue_warp<NI, NOUT, G, NT>(as[m], bad, m + 1 == sa.nmodes, slot_done(m), sa.epoch);
+    else
+      mode_epilogue<NI, NOUT, G, NT>(as[m], bad, m + 1 == sa.nmodes, slot_done(m), sa.epoch);
   }
 }
 
