@@ -109,6 +109,7 @@ void sweep(Context& c, int chain, int exec) {
   if (!chain && exec == MK_EXEC_FAST) {
     float* outs[kMaxModes];
     for (uint32_t d = 0; d < c.n; ++d) outs[d] = c.outputs[d].get();
+    tune_sweep(c, in, outs);  // once per set of choices: fused level-ordered vs the timed mix
     c.last_sweep_fused = launch_sweep2(c, in, outs);  // one launch (stream2.cuh k_sweep2)
     if (c.last_sweep_fused) return;
   }

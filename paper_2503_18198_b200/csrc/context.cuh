@@ -190,6 +190,7 @@ struct Context {
   unsigned long long als_graph_epoch = ~0ull, als_eager_epoch = ~0ull;
   bool grams_valid = false;
   bool last_sweep_fused = false;  // the last sweep() ran as one k_sweep2 launch
+  bool sweep_tuned = false;       // tune_sweep decided fused-vs-mix for the current choices
 
   // NCCL communicator and the sharded sweep's exchange buffers / CUDA graph (comm.cu)
   void* nccl_comm = nullptr;
@@ -237,6 +238,9 @@ bool launch_stream(Context& c, uint32_t mode, const float* const* in, float* out
 bool prepare_stream(Context& c, uint32_t mode);  // builds its records; false: no specialisation
 // Fast-path kernel selection (mttkrp.cu): 0 level-ordered, 1 fiber-ordered, 2 tiles.
 int choose_fast_kernel(Context& c, uint32_t mode, const float* const* in, float* out);
+// Unchained fast sweep whose per-mode timed choices mix kernels: time that mix against every
+// mode on the level-ordered kernel as ONE fused launch, keep the faster (mttkrp.cu).
+void tune_sweep(Context& c, const float* const* in, float* const* outs);
 void flush_l2(Context& c);  // write 2x the L2 size on the context's stream
 void pack_records(Context& c, uint32_t mode, const uint32_t* rank_of_row);
 // v2 level-ordered streaming kernel (stream2_plan.cu): records built per factor rank on first

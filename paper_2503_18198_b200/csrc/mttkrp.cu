@@ -485,6 +485,7 @@ int choose_fast_kernel(Context& c, uint32_t mode, const float* const* in, float*
       mc.fast_e1 == mc.shard_e1)
     return mc.fast_kernel;
   ++g_devmem_epoch;  // a (re)choice: captured graphs of the old choice are stale
+  c.sweep_tuned = false;
   mc.fast_rank = c.rank;
   mc.fast_e0 = mc.shard_e0;
   mc.fast_e1 = mc.shard_e1;
@@ -526,6 +527,42 @@ int choose_fast_kernel(Context& c, uint32_t mode, const float* const* in, float*
 }
 
 static bool mc_split(const Context& c, uint32_t mode) { return c.copies[mode].shard_split_row; }
+
+// The per-mode choices are timed one launch at a time; a fused sweep also saves the launch
+// gaps, mode tails and per-mode pre-zeroing, so a mode whose standalone winner is another
+// kernel can still be better off level-ordered inside the fused sweep (cfg4: the timed mix
+// 0.391 ms vs the all-level-ordered fused sweep 0.349 ms).  Both are timed once (L2 flushed,
+// min of two) and the faster stays until a choice changes.
+void tune_sweep(Context& c, const float* const* in, float* const* outs) {
+  if (c.sweep_tuned) return;
+  c.sweep_tuned = true;
+  if (c.plan_mode == MK_PLAN_MODEL || c.force_fast_kernel >= 0 || std::getenv("MKB_FAST_KERNEL"))
+    return;
+  int keep[kMaxModes];
+  bool mixed = false;
+  for (uint32_t d = 0; d < c.n; ++d) {
+    keep[d] = choose_fast_kernel(c, d, in, outs[d]);
+    mixed |= keep[d] != 0;
+  }
+  if (!mixed) return;
+  for (uint32_t d = 0; d < c.n; ++d)
+    if (keep[d] != 0 && !prepare_stream2(c, d)) return;
+  const float mix_ms = time_launch(c, [&] {
+    for (uint32_t d = 0; d < c.n; ++d) launch_mttkrp(c, d, in, outs[d], MK_EXEC_FAST);
+  });
+  for (uint32_t d = 0; d < c.n; ++d) c.copies[d].fast_kernel = 0;
+  bool fused = true;
+  const float fused_ms = time_launch(c, [&] { fused = fused && launch_sweep2(c, in, outs); });
+  const bool win = fused && fused_ms < mix_ms;
+  if (!win)
+    for (uint32_t d = 0; d < c.n; ++d) c.copies[d].fast_kernel = keep[d];
+  ++g_devmem_epoch;
+  c.sweep_tuned = true;  // (launch_sweep2 above may have re-planned; the decision stands)
+  if (std::getenv("MKB_DEBUG"))
+    std::fprintf(stderr, "[mkb] sweep: per-mode mix %.1f us, fused level-ordered %.1f us%s -> %s\n",
+                 mix_ms * 1e3, fused_ms * 1e3, fused ? "" : " (not fusable)",
+                 win ? "fused" : "mix");
+}
 
 void launch_mttkrp(Context& c, uint32_t mode, const float* const* in, float* out, int exec) {
   if (exec == MK_EXEC_REFERENCE)  // Scheme 1 parallel == deterministic

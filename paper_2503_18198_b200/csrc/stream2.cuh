@@ -483,6 +483,9 @@ constexpr uint32_t kHeader = 2048, kArgsOff = 512;  // Args of up to kMaxModes m
 #ifndef MKB_S2_B
 #define MKB_S2_B 3  // elements per gather batch (8-B records)
 #endif
+#ifndef MKB_S2_B4
+#define MKB_S2_B4 1  // elements per gather batch with four inner levels (16-B records; 3 spills)
+#endif
 #ifndef MKB_S2_NT
 #define MKB_S2_NT 512  // threads per CTA (one CTA per SM)
 #endif
@@ -907,7 +910,7 @@ constexpr uint32_t ring_bytes(int G, int NT) {
 
 template <int NI, int NOUT, int K, bool OS, int G, int NT, int MINB>
 void launch_one(const Args& a, unsigned grid, size_t smem, cudaStream_t st) {
-  constexpr int B = Lay<NI, NOUT>::AW == 2 ? MKB_S2_B : 3;
+  constexpr int B = Lay<NI, NOUT>::AW == 2 ? MKB_S2_B : (Lay<NI, NOUT>::NIN == 4 ? MKB_S2_B4 : 3);
   auto kern = k_stream2<NI, NOUT, K, OS, G, B, NT, MINB>;
   static bool attr_set = false;  // the attribute is per function, set before first launch
   if (!attr_set) {
@@ -923,7 +926,7 @@ void launch_one(const Args& a, unsigned grid, size_t smem, cudaStream_t st) {
 
 template <int NI, int NOUT, int K, bool OS, int G, int NT, int MINB>
 void launch_sweep_one(const SweepArgs& a, unsigned grid, size_t smem, cudaStream_t st) {
-  constexpr int B = Lay<NI, NOUT>::AW == 2 ? MKB_S2_B : 3;
+  constexpr int B = Lay<NI, NOUT>::AW == 2 ? MKB_S2_B : (Lay<NI, NOUT>::NIN == 4 ? MKB_S2_B4 : 3);
   auto kern = k_sweep2<NI, NOUT, K, OS, G, B, NT, MINB>;
   static bool attr_set = false;
   if (!attr_set) {
