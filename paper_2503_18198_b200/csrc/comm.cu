@@ -165,9 +165,12 @@ void sweep_sharded(Context& c) {
   ensure_exchange(c);
   reset_nonfinite(c);
   const bool use_graph = std::getenv("MKB_GRAPH") == nullptr || std::getenv("MKB_GRAPH")[0] != '0';
+  // a re-plan, re-allocation or new kernel choice since the capture makes the graph stale
+  if (c.graph_warm && g_devmem_epoch.load() != c.graph_epoch) invalidate_graph(c);
   if (!use_graph || !c.graph_warm) {
     enqueue_sweep(c);  // eager: the fast path's one-time plan choice happens here
     c.graph_warm = true;
+    c.graph_epoch = g_devmem_epoch.load();
     return;
   }
   if (!c.graph_exec) {
@@ -186,6 +189,7 @@ void sweep_sharded(Context& c) {
     cudaGraphDestroy(g);
     if (e != cudaSuccess) fail(MK_ECUDA, std::string("graph: ") + cudaGetErrorString(e));
     c.graph_exec = ge;
+    c.graph_epoch = g_devmem_epoch.load();
   }
   MKB_CUDA(cudaGraphLaunch(static_cast<cudaGraphExec_t>(c.graph_exec), c.stream));
 }

@@ -199,6 +199,7 @@ struct Context {
   uint64_t xstride[kMaxModes] = {};
   void* graph_exec = nullptr;  // cudaGraphExec_t of the captured sharded sweep
   bool graph_warm = false;     // one eager sweep ran (the fast path's kernel choice is made)
+  unsigned long long graph_epoch = 0;  // g_devmem_epoch when the eager sweep / capture ran
 };
 
 // One CPD-ALS iteration over all modes (als.cu); fit and optional lambda[R] to host.
