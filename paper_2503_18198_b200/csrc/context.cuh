@@ -61,6 +61,10 @@ struct ModeCopy {
     uint64_t key_seg = 0, key_tile = 0, key_e0 = ~0ull, key_e1 = ~0ull;
   };
   ZeroList zl_stream, zl_tiles;
+  // deterministic kernel: copy rows long enough for the one-CTA-per-row path (mttkrp.cu
+  // k_mttkrp_rows_long), cached per (threshold, shard range)
+  DevBuf<uint32_t> det_long;
+  uint64_t det_long_n = 0, det_long_key_min = 0, det_long_key_e0 = ~0ull, det_long_key_e1 = ~0ull;
   // fast-path kernel chosen for this copy by a one-time timing of the candidates
   // (mttkrp.cu): -1 undecided, 0 level-ordered streaming kernel, 1 fiber-ordered streaming
   // kernel, 2 generic tile kernel; keyed by factor rank and shard range

@@ -27,6 +27,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <string>
+#include <vector>
 
 #include "context.cuh"
 
@@ -52,6 +53,8 @@ struct MttkrpArgs {
   uint32_t ntiles;
   uint32_t nrows;
   uint32_t n_in;
+  uint32_t long_min;             // deterministic: rows this long run in k_mttkrp_rows_long
+  const uint32_t* long_rows;     // (their copy-row indices; 0 / null: none)
 };
 
 template <int VEC>
@@ -239,6 +242,121 @@ __global__ void __launch_bounds__(256) k_mttkrp_tiles(const MttkrpArgs a) {
   }
 }
 
+// Deterministic path for LONG rows (power-law head rows, Scheme 2-sized runs): the reference
+// order is a sequential fp32 sum over the row's elements, so one chain of additions per rank
+// is unavoidable, but the terms are not: one CTA per long row, warps 1..15 compute the terms
+// (gathers + __fmul_rn products, as k_mttkrp_rows) chunk by chunk into a shared-memory ring,
+// and warp 0 adds them in element order (__fadd_rn, lane = rank), ~4 cycles per element.
+// Bitwise the same as k_mttkrp_rows (and the reference's oracle_mttkrp); a 137 K-element row
+// costs ~0.3 ms instead of the one-group loop's ~30 ms.
+constexpr int kLongCh = 32, kLongSlots = 16;  // elements per chunk, ring slots
+constexpr int kLongThreads = 512;  // warp 0 adds, warps 1..15 produce
+template <int NI, int VEC, int G, int KREP>
+__global__ void __launch_bounds__(kLongThreads) k_mttkrp_rows_long(const MttkrpArgs a) {
+  constexpr int F = KREP * VEC, R = G * F, EPW = 32 / G;  // elements per producer warp step
+  static_assert(R % 32 == 0 && R <= 64, "long-row path: R = 32 or 64");
+  extern __shared__ float ring[];  // kLongSlots x kLongCh x R
+  __shared__ volatile int ready[kLongSlots], freed[kLongSlots];
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  if (tid < kLongSlots) {
+    ready[tid] = 0;
+    freed[tid] = 0;
+  }
+  __syncthreads();
+  const uint32_t k = __ldg(a.long_rows + blockIdx.x);
+  const uint32_t row = __ldg(a.row_seq + k);
+  const uint64_t s = max(static_cast<uint64_t>(__ldg(a.row_ptr + k)), a.e0),
+                 e = min(static_cast<uint64_t>(__ldg(a.row_ptr + k + 1)), a.e1);
+  const int nchunks = static_cast<int>((e - s + kLongCh - 1) / kLongCh);
+  constexpr int NP = kLongThreads / 32 - 1;  // producer warps
+  if (wid > 0) {  // producers: chunk c on warp 1 + c % NP
+    const int lane_g = lane % G, gw = lane / G;
+    for (int c = wid - 1; c < nchunks; c += NP) {
+      const int slot = c % kLongSlots;
+      while (freed[slot] < c - kLongSlots + 1) __nanosleep(32);
+      float* dst = ring + static_cast<size_t>(slot) * kLongCh * R;
+      const uint64_t c0 = s + static_cast<uint64_t>(c) * kLongCh;
+#pragma unroll 4
+      for (int e0 = 0; e0 < kLongCh; e0 += EPW) {
+        const uint64_t j = c0 + e0 + gw;
+        if (j >= e) break;
+        float t[F];
+        const float v = __ldg(a.val + j);
+#pragma unroll
+        for (int q = 0; q < F; ++q) t[q] = v;
+#pragma unroll
+        for (int i = 0; i < NI; ++i) {
+          float y[F];
+          load_row<VEC, G, KREP>(a.in_Y[i], __ldg(a.in_idx[i] + j), a.rank, lane_g, y);
+#pragma unroll
+          for (int q = 0; q < F; ++q) t[q] = __fmul_rn(t[q], y[q]);
+        }
+        float* te = dst + (e0 + gw) * R;
+#pragma unroll
+        for (int kr = 0; kr < KREP; ++kr)
+          *reinterpret_cast<float4*>(te + rank_of<VEC, G>(lane_g, kr, 0)) =
+              make_float4(t[kr * 4 + 0], t[kr * 4 + 1], t[kr * 4 + 2], t[kr * 4 + 3]);
+      }
+      __syncwarp();
+      __threadfence_block();
+      if (lane == 0) ready[slot] = c + 1;
+    }
+  } else {  // the adder: element order, lane = rank (R / 32 ranks per lane)
+    constexpr int RPL = R / 32;
+    float acc[RPL];
+#pragma unroll
+    for (int q = 0; q < RPL; ++q) acc[q] = 0.0f;
+    unsigned long long first_bad = ~0ull;
+    for (int c = 0; c < nchunks; ++c) {
+      const int slot = c % kLongSlots;
+      while (ready[slot] != c + 1) __nanosleep(32);
+      __threadfence_block();
+      const float* src = ring + static_cast<size_t>(slot) * kLongCh * R;
+      const uint64_t left = e - s - static_cast<uint64_t>(c) * kLongCh;
+      const int ne = left < static_cast<uint64_t>(kLongCh) ? static_cast<int>(left) : kLongCh;
+      bool bad = false;
+      int bad_at = 0;
+      int i = 0;
+      for (; i + 8 <= ne; i += 8) {  // eight terms loaded ahead of their in-order additions
+        float t[8][RPL];
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+#pragma unroll
+          for (int q = 0; q < RPL; ++q) t[u][q] = src[(i + u) * R + q * 32 + lane];
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+#pragma unroll
+          for (int q = 0; q < RPL; ++q) {
+            if (!isfinite(t[u][q]) && !bad) bad = true, bad_at = i + u;
+            acc[q] = __fadd_rn(acc[q], t[u][q]);
+          }
+      }
+      for (; i < ne; ++i) {
+#pragma unroll
+        for (int q = 0; q < RPL; ++q) {
+          const float t = src[i * R + q * 32 + lane];
+          if (!isfinite(t) && !bad) bad = true, bad_at = i;
+          acc[q] = __fadd_rn(acc[q], t);
+        }
+      }
+      // the first element whose term is non-finite in ANY rank (kernel.hpp:109-114)
+      const unsigned bm = __ballot_sync(0xffffffffu, bad);
+      if (bm && first_bad == ~0ull) {
+        int at = bad ? bad_at : kLongCh;
+        for (int o = 16; o; o >>= 1) at = min(at, __shfl_xor_sync(0xffffffffu, at, o));
+        first_bad = s + static_cast<uint64_t>(c) * kLongCh + at;
+      }
+      __syncwarp();
+      __threadfence_block();
+      if (lane == 0) freed[slot] = c + 1;
+    }
+    if (first_bad != ~0ull && lane == 0) atomicMin(a.nonfinite, a.tag | first_bad);
+    float* o = a.out + static_cast<size_t>(row) * R;
+#pragma unroll
+    for (int q = 0; q < RPL; ++q) o[q * 32 + lane] = acc[q];
+  }
+}
+
 template <int NI, int VEC, int G, int KREP>
 __global__ void __launch_bounds__(256) k_mttkrp_rows(const MttkrpArgs a) {
   constexpr int F = KREP * VEC;
@@ -251,9 +369,11 @@ __global__ void __launch_bounds__(256) k_mttkrp_rows(const MttkrpArgs a) {
 
   for (uint32_t k = a.k0 + gid; k < a.k0 + a.nrows; k += groups) {
     const uint32_t row = __ldg(a.row_seq + k);
+    const uint32_t p0 = __ldg(a.row_ptr + k), p1 = __ldg(a.row_ptr + k + 1);
+    if (a.long_min && p1 - p0 >= a.long_min) continue;  // k_mttkrp_rows_long's row
     // clamped to the launch's range: the end rows of a shard may be partial
-    const uint64_t s = max(static_cast<uint64_t>(__ldg(a.row_ptr + k)), a.e0),
-                   e = min(static_cast<uint64_t>(__ldg(a.row_ptr + k + 1)), a.e1);
+    const uint64_t s = max(static_cast<uint64_t>(p0), a.e0),
+                   e = min(static_cast<uint64_t>(p1), a.e1);
     float acc[F];
 #pragma unroll
     for (int q = 0; q < F; ++q) acc[q] = 0.0f;
@@ -374,9 +494,44 @@ void launch_cfg(Context& c, const MttkrpArgs& a, ModeCopy& mc, uint32_t mode, in
   }
   if (a.e1 <= a.e0) return;
   if (exec == MK_EXEC_DETERMINISTIC) {
+    MttkrpArgs ad = a;
+    if constexpr (VEC == 4 && (G * KREP * VEC == 32 || G * KREP * VEC == 64)) {
+      // rows of at least MKB_DET_LONG (default 512) elements: one CTA each (k_mttkrp_rows_long)
+      const char* ev = std::getenv("MKB_DET_LONG");
+      const uint32_t lmin = ev && *ev ? static_cast<uint32_t>(std::atoi(ev)) : 512u;
+      if (lmin > 0) {
+        if (mc.det_long_key_min != lmin || mc.det_long_key_e0 != a.e0 || mc.det_long_key_e1 != a.e1) {
+          std::vector<uint32_t> rp(mc.distinct + 1);
+          MKB_CUDA(cudaMemcpyAsync(rp.data(), mc.row_ptr.get(), rp.size() * sizeof(uint32_t),
+                                   cudaMemcpyDeviceToHost, st));
+          MKB_CUDA(cudaStreamSynchronize(st));
+          std::vector<uint32_t> ks;
+          for (uint64_t k = a.k0; k < a.k0 + a.nrows; ++k)
+            if (rp[k + 1] - rp[k] >= lmin) ks.push_back(static_cast<uint32_t>(k));
+          mc.det_long.resize(std::max<size_t>(ks.size(), 1));
+          if (!ks.empty())
+            MKB_CUDA(cudaMemcpyAsync(mc.det_long.get(), ks.data(), ks.size() * 4,
+                                     cudaMemcpyHostToDevice, st));
+          mc.det_long_n = ks.size();
+          mc.det_long_key_min = lmin;
+          mc.det_long_key_e0 = a.e0;
+          mc.det_long_key_e1 = a.e1;
+        }
+        if (mc.det_long_n) {
+          ad.long_min = lmin;
+          ad.long_rows = mc.det_long.get();
+          const size_t smem = static_cast<size_t>(kLongSlots) * kLongCh * (G * KREP * VEC) * 4;
+          auto kern = k_mttkrp_rows_long<NI, VEC, G, KREP>;
+          MKB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        static_cast<int>(smem)));
+          kern<<<static_cast<unsigned>(mc.det_long_n), kLongThreads, smem, st>>>(ad);
+          MKB_LAUNCH();
+        }
+      }
+    }
     const unsigned blocks = static_cast<unsigned>(
         std::min<uint64_t>(ceil_div(a.nrows, per_block), c.num_sms * 16ull));
-    k_mttkrp_rows<NI, VEC, G, KREP><<<std::max(1u, blocks), 256, 0, st>>>(a);
+    k_mttkrp_rows<NI, VEC, G, KREP><<<std::max(1u, blocks), 256, 0, st>>>(ad);
   } else {
     const unsigned blocks = static_cast<unsigned>(
         std::min<uint64_t>(ceil_div(a.ntiles, per_block), c.num_sms * 8ull));
