@@ -244,36 +244,38 @@ __global__ void __launch_bounds__(256) k_mttkrp_tiles(const MttkrpArgs a) {
 
 // Deterministic path for LONG rows (power-law head rows, Scheme 2-sized runs): the reference
 // order is a sequential fp32 sum over the row's elements, so one chain of additions per rank
-// is unavoidable, but the terms are not: one CTA per long row, warps 1..15 compute the terms
+// is unavoidable, but the terms are not: one CTA per long row, warps 1..7 compute the terms
 // (gathers + __fmul_rn products, as k_mttkrp_rows) chunk by chunk into a shared-memory ring,
 // and warp 0 adds them in element order (__fadd_rn, lane = rank), ~4 cycles per element.
 // Bitwise the same as k_mttkrp_rows (and the reference's oracle_mttkrp); a 137 K-element row
 // costs ~0.3 ms instead of the one-group loop's ~30 ms.
-constexpr int kLongCh = 32, kLongSlots = 16;  // elements per chunk, ring slots
-constexpr int kLongThreads = 512;  // warp 0 adds, warps 1..15 produce
+constexpr int kLongCh = 32, kLongSlots = 7;  // elements per chunk, ring slots (named barriers 1-14)
+constexpr int kLongThreads = 256;  // warp 0 adds, warps 1..7 produce (warp w fills slot w - 1)
 template <int NI, int VEC, int G, int KREP>
 __global__ void __launch_bounds__(kLongThreads) k_mttkrp_rows_long(const MttkrpArgs a) {
   constexpr int F = KREP * VEC, R = G * F, EPW = 32 / G;  // elements per producer warp step
   static_assert(R % 32 == 0 && R <= 64, "long-row path: R = 32 or 64");
   extern __shared__ float ring[];  // kLongSlots x kLongCh x R
-  __shared__ volatile int ready[kLongSlots], freed[kLongSlots];
+  // Hand-off per slot through named barriers of 64 threads: slot s belongs to producer warp
+  // 1 + s alone (chunks c = s, s + 7, ...), so each barrier only ever pairs that warp with the
+  // adder, in chunk order.  FULL(s) = 1 + s: the producer bar.arrive's after writing chunk c,
+  // the adder bar.sync's before reading it; EMPTY(s) = 1 + kLongSlots + s: the adder arrives
+  // after reading chunk c when chunk c + kLongSlots exists, whose producer syncs before
+  // writing it.  (Unlike an mbarrier hand-off, compute-sanitizer's racecheck models these.)
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  if (tid < kLongSlots) {
-    ready[tid] = 0;
-    freed[tid] = 0;
-  }
-  __syncthreads();
+  auto bar_sync = [](int id) { asm volatile("bar.sync %0, 64;" ::"r"(id) : "memory"); };
+  auto bar_arrive = [](int id) { asm volatile("bar.arrive %0, 64;" ::"r"(id) : "memory"); };
   const uint32_t k = __ldg(a.long_rows + blockIdx.x);
   const uint32_t row = __ldg(a.row_seq + k);
   const uint64_t s = max(static_cast<uint64_t>(__ldg(a.row_ptr + k)), a.e0),
                  e = min(static_cast<uint64_t>(__ldg(a.row_ptr + k + 1)), a.e1);
   const int nchunks = static_cast<int>((e - s + kLongCh - 1) / kLongCh);
-  constexpr int NP = kLongThreads / 32 - 1;  // producer warps
-  if (wid > 0) {  // producers: chunk c on warp 1 + c % NP
+  static_assert(kLongThreads / 32 - 1 == kLongSlots, "one producer warp per slot");
+  if (wid > 0) {  // producers: chunk c on warp 1 + c % kLongSlots
     const int lane_g = lane % G, gw = lane / G;
-    for (int c = wid - 1; c < nchunks; c += NP) {
+    for (int c = wid - 1; c < nchunks; c += kLongSlots) {
       const int slot = c % kLongSlots;
-      while (freed[slot] < c - kLongSlots + 1) __nanosleep(32);
+      if (c >= kLongSlots) bar_sync(1 + kLongSlots + slot);  // chunk c - kLongSlots was read
       float* dst = ring + static_cast<size_t>(slot) * kLongCh * R;
       const uint64_t c0 = s + static_cast<uint64_t>(c) * kLongCh;
 #pragma unroll 4
@@ -297,9 +299,8 @@ __global__ void __launch_bounds__(kLongThreads) k_mttkrp_rows_long(const MttkrpA
           *reinterpret_cast<float4*>(te + rank_of<VEC, G>(lane_g, kr, 0)) =
               make_float4(t[kr * 4 + 0], t[kr * 4 + 1], t[kr * 4 + 2], t[kr * 4 + 3]);
       }
-      __syncwarp();
-      __threadfence_block();
-      if (lane == 0) ready[slot] = c + 1;
+      __syncwarp();  // bar.* is warp-aligned: the element loop's early exits reconverge first
+      bar_arrive(1 + slot);
     }
   } else {  // the adder: element order, lane = rank (R / 32 ranks per lane)
     constexpr int RPL = R / 32;
@@ -309,8 +310,7 @@ __global__ void __launch_bounds__(kLongThreads) k_mttkrp_rows_long(const MttkrpA
     unsigned long long first_bad = ~0ull;
     for (int c = 0; c < nchunks; ++c) {
       const int slot = c % kLongSlots;
-      while (ready[slot] != c + 1) __nanosleep(32);
-      __threadfence_block();
+      bar_sync(1 + slot);
       const float* src = ring + static_cast<size_t>(slot) * kLongCh * R;
       const uint64_t left = e - s - static_cast<uint64_t>(c) * kLongCh;
       const int ne = left < static_cast<uint64_t>(kLongCh) ? static_cast<int>(left) : kLongCh;
@@ -346,9 +346,7 @@ __global__ void __launch_bounds__(kLongThreads) k_mttkrp_rows_long(const MttkrpA
         for (int o = 16; o; o >>= 1) at = min(at, __shfl_xor_sync(0xffffffffu, at, o));
         first_bad = s + static_cast<uint64_t>(c) * kLongCh + at;
       }
-      __syncwarp();
-      __threadfence_block();
-      if (lane == 0) freed[slot] = c + 1;
+      if (c + kLongSlots < nchunks) bar_arrive(1 + kLongSlots + slot);
     }
     if (first_bad != ~0ull && lane == 0) atomicMin(a.nonfinite, a.tag | first_bad);
     float* o = a.out + static_cast<size_t>(row) * R;
