@@ -287,3 +287,37 @@ def test_reference_exec_contract(mk):
                             (dims, policy, d)
                     else:
                         assert mk.verify_against(ref[d], det[d].data)[0] <= 1e-5, (dims, policy, d)
+
+
+@pytest.mark.parametrize("rank", [32, 64])
+def test_deterministic_long_rows(mk, orc, monkeypatch, rank):
+    """k_mttkrp_rows_long (rows of >= 512 elements, one CTA each, producer warps + an in-order
+    adder): bitwise equal to the one-group kernel (MKB_DET_LONG=0) and to the C oracle on a
+    tensor with heavy rows in every mode, and a non-finite term inside a heavy row is reported
+    at the reference's first failing copy position (kernel.hpp:109-114)."""
+    dims = [7, 40, 600]
+    t = mk.generate_synthetic(dims, 60_000, seed=9)
+    f = [m.data for m in mk.random_factors(dims, rank, 4)]
+    outs = {}
+    for lm in ("512", "0"):
+        monkeypatch.setenv("MKB_DET_LONG", lm)
+        c = mk.Context()
+        c.upload_tensor(t)
+        c.build_plans(148)
+        c.upload_factors(f)
+        outs[lm] = c.mttkrp_all_modes(False, True)
+    for d in range(3):
+        want = orc.mttkrp(dims, t.coords, t.values, f, d)
+        assert np.array_equal(outs["512"][d].view(np.uint32), outs["0"][d].view(np.uint32)), d
+        assert np.array_equal(outs["512"][d].view(np.uint32), want.view(np.uint32)), d
+    # an infinite factor entry read by elements of mode 0's heavy rows
+    monkeypatch.setenv("MKB_DET_LONG", "512")
+    bad = [x.copy() for x in f]
+    bad[2][123, 5] = np.inf
+    plans = mk.build_mode_plans(t, 148)
+    order = np.asarray(plans[0].order, dtype=np.int64)
+    hits = np.nonzero(np.asarray(t.coords)[order, 2] == 123)[0]
+    assert len(hits)
+    pos = int(hits[0])
+    with pytest.raises(mk.MttkrpError, match=rf"tensor element {int(order[pos])} \(mode 0, copy position {pos}\)"):
+        mk.mttkrp_mode(t, plans[0], bad, mk.ExecConfig(148, 32, True))
