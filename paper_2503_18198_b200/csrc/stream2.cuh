@@ -256,6 +256,9 @@ struct Seg {
   bool zeroed;                                // the launch's pre-zeroing is complete
 };
 
+#ifndef MKB_S2_LEAD_STAGED
+#define MKB_S2_LEAD_STAGED 1  // lead-2 for fully staged plans too (cfg2 0.1555 -> 0.1541 ms)
+#endif
 template <int NI, int NOUT, int K, bool OS, int G>
 struct Body {
   using L = Lay<NI, NOUT>;
@@ -404,6 +407,9 @@ struct Body {
   // (shared-memory latency), so the extra lead costs no registers: three in-flight L2 row
   // buffers plus one transient staged buffer, against two full buffers in chunk().
   static constexpr int NG = NIN - K;  // inner levels gathered through L1/L2
+  // levels gathered two batches ahead: the L1/L2-fed ones, or (MKB_S2_LEAD_STAGED, fully
+  // staged plans) every level
+  static constexpr int NGE = (MKB_S2_LEAD_STAGED && NG == 0) ? NIN : NG;
   template <int B, bool GLOB>
   static __device__ __forceinline__ void gather_sel(const Lane<NIN>& ln, const uint32_t (&r)[4],
                                                     float4 (&y)[NIN]) {
@@ -411,7 +417,7 @@ struct Body {
     unpack<NI, NOUT>(r, ln.b0, ln.m0, ln.m1, c);
 #pragma unroll
     for (int j = 0; j < NIN; ++j)
-      if ((j < NG) == GLOB) y[j] = gather(ln, j, c[j]);
+      if ((j < NGE) == GLOB) y[j] = gather(ln, j, c[j]);
   }
   template <int B>
   static __device__ __forceinline__ void gsel(const Lane<NIN>& ln, const uint32_t (&r)[B][4],
@@ -663,7 +669,8 @@ __device__ __forceinline__ bool mode_body(const Args& a, uint8_t* smem, Persist&
       const uint32_t* RB = reinterpret_cast<const uint32_t*>(ring + st * (BA + BB) + BA) + gw * KS;
       // the last chunk of a group is padded with copies of its last record (value 0, no
       // flag), so every chunk runs the same pipelined path
-      if constexpr (MKB_S2_LEAD == 2 && (Bd::NG == 1 || (MKB_S2_LEAD_NG2 && Bd::NG == 2)))
+      if constexpr (MKB_S2_LEAD == 2 && (Bd::NG == 1 || (MKB_S2_LEAD_NG2 && Bd::NG == 2) ||
+                                         (MKB_S2_LEAD_STAGED && Bd::NG == 0 && NT <= 384)))
         Bd::template chunk_lead2<B, S>(ln, s, RA, RB);
       else
         Bd::template chunk<B, S>(ln, s, RA, RB);
