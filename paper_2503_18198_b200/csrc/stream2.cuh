@@ -468,11 +468,6 @@ struct Body {
 #ifndef MKB_S2_WARPEPI
 #define MKB_S2_WARPEPI 1  // fused sweep of unstaged plans: per-warp mode ends, no CTA barrier
 #endif
-#ifndef MKB_S2_XITEM
-// 1: record tiles prefetched across work items.  Measured on B200 (cfg5): 2.090 -> 2.038 ms
-// alone, but 1.963 -> 2.020 ms on top of the lead-2 pipeline, so off by default.
-#define MKB_S2_XITEM 0
-#endif
 #ifndef MKB_S2_LEAD_NG2
 #define MKB_S2_LEAD_NG2 0  // 1: the lead-2 pipeline also for two L1/L2-fed inner levels
 #endif
@@ -573,42 +568,9 @@ __device__ __forceinline__ bool mode_body(const Args& a, uint8_t* smem, Persist&
   uint32_t it = ps.it;
   uint32_t staged = 0xffffffffu;
   const uint32_t i_end = a.cta_items[blockIdx.x + 1];
-#if MKB_S2_XITEM
-  // Record tiles stream across the CTA's items of the mode: lane 0 requests tile qt of item qi
-  // next (one bulk copy of the tile's records + slow keys into ring stage iss & 1), keeping two
-  // tiles in flight, so an item's first tiles land while the previous item still runs.
-  uint32_t qi = a.cta_items[blockIdx.x], qt = 0, q_tile0 = 0, q_tiles = 0, iss = it;
-  bool q_loaded = false;
-  auto request = [&]() {
-    while (qi < i_end) {
-      if (!q_loaded) {
-        const WDesc dq = a.wdesc[qi * NW + wid];
-        q_tile0 = dq.tile0;
-        q_tiles = dq.tiles;
-        q_loaded = true;
-      }
-      if (qt < q_tiles) break;
-      ++qi;
-      qt = 0;
-      q_loaded = false;
-    }
-    if (qi >= i_end) return;
-    const int st = iss & 1;
-    mbar_arrive_tx(&wbar[st], BA + BB);
-    tma_load_1d(ring + st * (BA + BB), gT + (static_cast<size_t>(q_tile0) + qt) * (BA + BB),
-                BA + BB, &wbar[st]);
-    ++qt;
-    ++iss;
-  };
-  if (lane == 0) {
-    request();
-    request();
-  }
-#endif
   for (uint32_t ii = a.cta_items[blockIdx.x]; ii < i_end; ++ii) {
     const Item item = a.items[ii];
     const WDesc d = a.wdesc[ii * NW + wid];
-#if !MKB_S2_XITEM
     auto issue = [&](uint32_t t, int st) {  // one bulk copy: the tile's records + slow keys
       mbar_arrive_tx(&wbar[st], BA + BB);
       tma_load_1d(ring + st * (BA + BB), gT + (static_cast<size_t>(d.tile0) + t) * (BA + BB),
@@ -618,7 +580,6 @@ __device__ __forceinline__ bool mode_body(const Args& a, uint8_t* smem, Persist&
       if (d.tiles > 0) issue(0, it & 1);
       if (d.tiles > 1) issue(1, (it + 1) & 1);
     }
-#endif
     __syncwarp();
     // (re)stage the block's factor slices (and the outer factor with the first block)
     if constexpr (K > 0 || OS) {
@@ -675,11 +636,7 @@ __device__ __forceinline__ bool mode_body(const Args& a, uint8_t* smem, Persist&
       else
         Bd::template chunk<B, S>(ln, s, RA, RB);
       __syncwarp();  // the whole warp is done with this stage
-#if MKB_S2_XITEM
-      if (lane == 0) request();
-#else
       if (lane == 0 && t + 2 < d.tiles) issue(t + 2, st);
-#endif
     }
     // the group's last run
     Bd::fold(s);
