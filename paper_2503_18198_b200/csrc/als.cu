@@ -4,7 +4,8 @@
 // (oracle/als.py) — parity for this subsystem is "unpinned" against the reference.
 //
 // Per mode d of an iteration: the spMTTKRP, then ONE cooperative launch (k_als_update):
-//   P      = Mᵀ M                               (phase 1: per-CTA partials, fp64 atomics)
+//   P      = Mᵀ M                               (phase 1: per-CTA partials; grid barrier; phase
+//                                                 1b: reduced in CTA order, deterministic)
 //   -- grid barrier --
 //   V      = ⊛_{w≠d} G_w,  G_w = Y_wᵀ Y_w      (R×R, fp64, Grams kept resident)
 //   V⁻¹                                         (phase 2, every CTA redundantly: Gauss-Jordan
@@ -36,7 +37,7 @@ namespace {
 #endif
 constexpr int kGramRows = 64;  // rows staged per block iteration
 
-// G += Yᵀ Y over a row range; one thread per (r, s) pair (s >= r mirrored at the end).
+// Partial Yᵀ Y of this CTA's row range; one thread per (r, s) pair.
 __global__ void __launch_bounds__(256) k_gram(const float* __restrict__ Y, uint32_t rows,
                                               uint32_t R, double* __restrict__ G) {
   extern __shared__ float tile[];  // kGramRows x R
@@ -61,9 +62,20 @@ __global__ void __launch_bounds__(256) k_gram(const float* __restrict__ Y, uint3
       }
     }
   }
+  // this CTA's partial; k_gram_reduce sums the partials in CTA order (deterministic Grams:
+  // every rank of a sharded CPD-ALS starts from the same bits)
   for (int k = 0; k < per; ++k) {
     const uint32_t p = threadIdx.x + k * blockDim.x;
-    if (p < pairs) atomicAdd(&G[p], acc[k]);
+    if (p < pairs) G[static_cast<size_t>(blockIdx.x) * pairs + p] = acc[k];
+  }
+}
+
+__global__ void k_gram_reduce(const double* __restrict__ part, uint32_t nparts, uint32_t pairs,
+                              double* __restrict__ G) {
+  for (uint32_t p = blockIdx.x * blockDim.x + threadIdx.x; p < pairs; p += gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (uint32_t b = 0; b < nparts; ++b) s += part[static_cast<size_t>(b) * pairs + p];
+    G[p] = s;
   }
 }
 
@@ -73,14 +85,14 @@ struct UpdArgs {
   float* Y;            // updated factor, rows x R
   uint32_t rows, R, n, d;
   double* grams;       // N x R x R
-  double* P;           // this mode's MᵀM accumulator (zero on entry)
-  double* P_next;      // the next mode's accumulator (zeroed here)
+  double* P;           // this mode's MᵀM (written by the reduction, phase 1b)
+  double* Ppart;       // per-CTA partial MᵀM (grid x R x R)
   float* lambda;
   double* scalars;     // [⟨X,X̂⟩, ||X̂||²] (last mode)
   int last;
   int* status;
   unsigned int* bar;   // grid barrier counter (monotonic)
-  unsigned int target; // barrier target for this launch
+  unsigned int target; // first grid barrier's target (the second's is target + gridDim.x)
   unsigned long long* prof;  // MKB_ALS_PROF: phase timestamps of CTA 0 (ns), else null
   const double* vinv;        // V⁻¹ precomputed by k_als_inverse (R x R), else null
   const int* vinv_status;    // its fallback flag
@@ -374,32 +386,47 @@ __global__ void __launch_bounds__(NTH) k_als_update(const UpdArgs u) {
         }
       }
     }
-    if (r1 > r0) {
+    // this CTA's partial (zeros when it has no rows), reduced in CTA order below: a fixed
+    // summation order, so every rank of a sharded ALS (and every run) gets the same P
+    double* part = u.Ppart + static_cast<size_t>(blockIdx.x) * RR;
 #pragma unroll
-      for (int q = 0; q < TPT; ++q) {
-        const uint32_t t = threadIdx.x + q * NTH;
-        if (t >= ntile) continue;
-        const uint32_t ra = (t / tc) * 2, c0 = (t % tc) * 4;
+    for (int q = 0; q < TPT; ++q) {
+      const uint32_t t = threadIdx.x + q * NTH;
+      if (t >= ntile) continue;
+      const uint32_t ra = (t / tc) * 2, c0 = (t % tc) * 4;
 #pragma unroll
-        for (int i = 0; i < 2; ++i)
+      for (int i = 0; i < 2; ++i)
 #pragma unroll
-          for (int j = 0; j < 4; ++j)
-            if (ra + i < R && c0 + j < R) atomicAdd(&u.P[(ra + i) * R + c0 + j], acc[q][i][j]);
-      }
+        for (int j = 0; j < 4; ++j)
+          if (ra + i < R && c0 + j < R) part[(ra + i) * R + c0 + j] = acc[q][i][j];
     }
   }
-  // grid barrier (cooperative launch: every CTA is resident)
-  __syncthreads();
+  // grid barriers (cooperative launch: every CTA is resident)
+  auto grid_barrier = [&](unsigned int target) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence();
+      atomicAdd(u.bar, 1u);
+      unsigned int v;
+      do {
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(u.bar) : "memory");
+      } while (static_cast<int>(v - target) < 0);
+    }
+    __syncthreads();
+  };
   stamp(1);
-  if (threadIdx.x == 0) {
-    __threadfence();
-    atomicAdd(u.bar, 1u);
-    unsigned int v;
-    do {
-      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(u.bar) : "memory");
-    } while (static_cast<int>(v - u.target) < 0);
+  grid_barrier(u.target);
+  // phase 1b: P = sum of the partials in CTA order, CTA c reducing its slice of the entries
+  {
+    const uint32_t p0 = static_cast<uint32_t>(static_cast<uint64_t>(RR) * blockIdx.x / gridDim.x);
+    const uint32_t p1 = static_cast<uint32_t>(static_cast<uint64_t>(RR) * (blockIdx.x + 1) / gridDim.x);
+    for (uint32_t p = p0 + threadIdx.x; p < p1; p += blockDim.x) {
+      double sum = 0.0;
+      for (uint32_t b = 0; b < gridDim.x; ++b) sum += __ldcg(&u.Ppart[static_cast<size_t>(b) * RR + p]);
+      u.P[p] = sum;
+    }
   }
-  __syncthreads();
+  grid_barrier(u.target + gridDim.x);
   // phase 2
   stamp(2);
   bool fell_back;
@@ -434,7 +461,6 @@ __global__ void __launch_bounds__(NTH) k_als_update(const UpdArgs u) {
     for (uint32_t p = threadIdx.x; p < RR; p += blockDim.x) {
       const uint32_t r = p / R, c = p % R;
       G[p] = Gs[p] / (lam[r] * lam[c]);
-      u.P_next[p] = 0.0;
     }
     for (uint32_t r = threadIdx.x; r < R; r += blockDim.x) u.lambda[r] = static_cast<float>(lam[r]);
     __syncthreads();
@@ -515,9 +541,12 @@ int blocks_for(uint64_t rows, int sms) {
 void gram_of(Context& c, uint32_t w) {
   const uint32_t R = c.rank;
   double* G = c.gram.get() + static_cast<size_t>(w) * R * R;
-  MKB_CUDA(cudaMemsetAsync(G, 0, sizeof(double) * R * R, c.stream));
-  k_gram<<<blocks_for(c.dims[w], c.num_sms), 256, kGramRows * R * sizeof(float), c.stream>>>(
-      c.factors[w].get(), c.dims[w], R, G);
+  const unsigned blocks = blocks_for(c.dims[w], c.num_sms);
+  c.als_ppart.resize(std::max<size_t>(static_cast<size_t>(blocks), c.num_sms) * R * R);
+  k_gram<<<blocks, 256, kGramRows * R * sizeof(float), c.stream>>>(c.factors[w].get(), c.dims[w],
+                                                                   R, c.als_ppart.get());
+  MKB_LAUNCH();
+  k_gram_reduce<<<(R * R + 255) / 256, 256, 0, c.stream>>>(c.als_ppart.get(), blocks, R * R, G);
   MKB_LAUNCH();
 }
 
@@ -536,8 +565,7 @@ void als_prepare(Context& c) {
   c.lambda.resize(R);
   c.als_scalars.resize(2);
   c.als_status.resize(1);
-  // two MᵀM accumulators (ping-pong, each left zeroed by the update that consumed it); a new
-  // rank re-lays them out, so both are re-zeroed and the ping-pong restarts at slot 0
+  // the MᵀM buffer (overwritten by every update's ordered reduction); a new rank re-lays it out
   if (c.mtm.size() < 2 * static_cast<size_t>(R) * R || c.mtm_rank != R) {
     c.mtm.resize(2 * static_cast<size_t>(R) * R);
     MKB_CUDA(cudaMemsetAsync(c.mtm.get(), 0, 2 * sizeof(double) * R * R, c.stream));
@@ -566,8 +594,9 @@ void als_update_mode(Context& c, uint32_t d, bool pre_inverse) {
   u.n = n;
   u.d = d;
   u.grams = c.gram.get();
-  u.P = c.mtm.get() + static_cast<size_t>(c.als_epoch & 1) * R * R;
-  u.P_next = c.mtm.get() + static_cast<size_t>((c.als_epoch + 1) & 1) * R * R;
+  u.P = c.mtm.get();
+  c.als_ppart.resize(static_cast<size_t>(c.num_sms) * R * R);
+  u.Ppart = c.als_ppart.get();
   u.lambda = c.lambda.get();
   u.scalars = c.als_scalars.get();
   u.last = d + 1 == n ? 1 : 0;
@@ -580,7 +609,8 @@ void als_update_mode(Context& c, uint32_t d, bool pre_inverse) {
   u.vinv_status = pre_inverse ? c.als_vinv_status.get() : nullptr;
   const unsigned grid = static_cast<unsigned>(std::min<uint64_t>(
       c.num_sms, std::max<uint64_t>(1, (u.rows + kGramRows - 1) / kGramRows)));
-  u.target = (c.als_bar_count += grid);
+  u.target = c.als_bar_count + grid;  // two grid barriers per launch
+  c.als_bar_count += 2 * grid;
   ++c.als_epoch;
   auto go = [&](auto kern, unsigned nth, size_t smem) {
     MKB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -165,7 +165,8 @@ struct Context {
 
   // CPD-ALS state
   DevBuf<double> gram;    // N x R x R (fp64)
-  DevBuf<double> mtm;     // 2 x R x R: MᵀM accumulators (fp64, ping-pong, zero between uses)
+  DevBuf<double> mtm;     // MᵀM of the current update (fp64; 2 x R x R allocated)
+  DevBuf<double> als_ppart;  // per-CTA partial MᵀM (SM count x R x R), reduced in CTA order
   uint32_t mtm_rank = 0;  // rank the accumulators were laid out (and zeroed) for
   DevBuf<unsigned int> als_bar;  // grid barrier counter of the fused update (monotonic)
   unsigned int als_bar_count = 0;
