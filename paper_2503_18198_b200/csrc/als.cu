@@ -417,13 +417,26 @@ __global__ void __launch_bounds__(NTH) k_als_update(const UpdArgs u) {
   stamp(1);
   grid_barrier(u.target);
   // phase 1b: P = sum of the partials in CTA order, CTA c reducing its slice of the entries
+  // (one warp per entry: lane l sums partials l, l + 32, ... in order, then a fixed butterfly)
   {
     const uint32_t p0 = static_cast<uint32_t>(static_cast<uint64_t>(RR) * blockIdx.x / gridDim.x);
     const uint32_t p1 = static_cast<uint32_t>(static_cast<uint64_t>(RR) * (blockIdx.x + 1) / gridDim.x);
-    for (uint32_t p = p0 + threadIdx.x; p < p1; p += blockDim.x) {
-      double sum = 0.0;
-      for (uint32_t b = 0; b < gridDim.x; ++b) sum += __ldcg(&u.Ppart[static_cast<size_t>(b) * RR + p]);
-      u.P[p] = sum;
+    if (gridDim.x <= 32) {  // few partials (and many entries per CTA): a thread per entry
+      for (uint32_t p = p0 + threadIdx.x; p < p1; p += blockDim.x) {
+        double sum = 0.0;
+        for (uint32_t b = 0; b < gridDim.x; ++b) sum += __ldcg(&u.Ppart[static_cast<size_t>(b) * RR + p]);
+        u.P[p] = sum;
+      }
+    } else {
+      const uint32_t lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+      for (uint32_t p = p0 + w; p < p1; p += nw) {
+        double sum = 0.0;
+        for (uint32_t b = lane; b < gridDim.x; b += 32)
+          sum += __ldcg(&u.Ppart[static_cast<size_t>(b) * RR + p]);
+#pragma unroll
+        for (int o = 16; o; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+        if (lane == 0) u.P[p] = sum;
+      }
     }
   }
   grid_barrier(u.target + gridDim.x);
