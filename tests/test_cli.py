@@ -216,3 +216,22 @@ def test_cached_tensor_run(cli, tmp_path):
     assert os.path.exists(str(tns) + ".mkbt")
     r = run_cli(cli, ["run", "--tensor", str(tns) + ".mkbt", "--verify", "--json", str(rep)])
     assert r.returncode == 0 and json.loads(rep.read_text())["nnz"] == 3000
+
+
+@pytest.mark.gpu
+def test_run_exec_reference_and_fast(cli, tmp_path):
+    """`run` keeps the reference's executor contract by default (exec "reference": Scheme 1
+    modes bitwise equal to --deterministic, SPEC.md:271); `--fast` selects the B200 fast path;
+    both verify against the deterministic executor."""
+    tns, rep = tmp_path / "t.tns", tmp_path / "report.json"
+    assert run_cli(cli, ["gen", "--dims", "300,200,160", "--nnz", "50000", "--seed", "4", "--out",
+                         str(tns)]).returncode == 0
+    for flags, want in (([], "reference"), (["--fast"], "fast"), (["--deterministic"], "deterministic")):
+        r = run_cli(cli, ["run", "--tensor", str(tns), "--rank", "32", "--verify", "--iters", "2",
+                          "--json", str(rep)] + flags)
+        assert r.returncode == 0, r.stderr
+        j = json.loads(rep.read_text())
+        assert j["exec"] == want and j["verify"]["passed"] is True
+        if want != "fast":  # every extent >= kappa (SM count): all modes Scheme 1, bitwise
+            assert j["timing"]["outputs_bit_identical"] is True
+            assert j["verify"]["max_rel_err"] == 0.0
