@@ -460,7 +460,7 @@ def run_config(args, name, rank, world, local_rank, stream, with_cpu):
                      "lsu": lsu_roofline(name, kern_ms, clk.summary().get("sm_mhz")),
                      "per_mode": fast},
         "e2e": {"value": e2e_ms, "unit": "ms", "h2d_bytes_per_step": h2d,
-                "d2h_bytes_per_step": h2d, "path": "mk_sweep_host (C ABI), pinned host buffers",
+                "d2h_bytes_per_step": h2d, "path": "mk_sweep_host (C ABI), pinned host buffers; H2D / kernel / D2H pipelined above 2 MB of copies",
                 "pageable_per_mode_ms": e2e_pageable_ms},
         "gpu_launches": (launches_per_sweep + (2 * n if ex is not None else 0)) * args.steps,
         "allgather_bytes_per_sweep": ex.bytes_per_sweep(R, n) if ex is not None else 0,
