@@ -24,6 +24,7 @@
 #include <vector>
 
 #include "als_inverse.cuh"
+#include "tma.cuh"
 #include "context.cuh"
 
 namespace mkb {
@@ -35,7 +36,10 @@ namespace {
 #ifndef ALS_NTH64
 #define ALS_NTH64 1024
 #endif
-constexpr int kGramRows = 64;  // rows staged per block iteration
+constexpr int kGramRows = 64;  // rows staged per block iteration (k_gram; update grid sizing)
+// rows of M staged per iteration of the update's phases 1 and 3 (a CTA's share of a big mode
+// in few rounds: cfg4 mode 4 has ~5900 rows per CTA)
+constexpr uint32_t upd_tile_rows(uint32_t R) { return R == 32 || R == 16 ? 256u : 64u; }
 
 // Partial Yᵀ Y of this CTA's row range; one thread per (r, s) pair.
 __global__ void __launch_bounds__(256) k_gram(const float* __restrict__ Y, uint32_t rows,
@@ -329,7 +333,7 @@ __device__ bool block_inverse(const double* __restrict__ grams, uint32_t n, uint
 // per-pivot Gauss-Jordan step is R·(R+1) independent updates, so larger ranks get more threads.
 template <int RT, int NTH>
 __global__ void __launch_bounds__(NTH) k_als_update(const UpdArgs u) {
-  extern __shared__ double dsm[];
+  extern __shared__ __align__(128) double dsm[];
   constexpr int RMAX = RT ? RT : 64;
   const uint32_t R = RT ? RT : u.R, RR = R * R, W2 = 2 * R;
   double* A = dsm;             // R x 2R
@@ -339,7 +343,8 @@ __global__ void __launch_bounds__(NTH) k_als_update(const UpdArgs u) {
   double* lam = scratch + RR;  // R
   double* fac = lam + R;       // R
   float* S = reinterpret_cast<float*>(fac + R);  // R x R
-  float* tile = S + RR;                          // kGramRows x R
+  float* tile = S + RR;                          // upd_tile_rows(R) x R
+  constexpr uint32_t TROWS = upd_tile_rows(RT);
   auto stamp = [&](int k) {
     if (u.prof && blockIdx.x == 0 && threadIdx.x == 0) {
       unsigned long long t;
@@ -350,25 +355,74 @@ __global__ void __launch_bounds__(NTH) k_als_update(const UpdArgs u) {
   stamp(0);
   const uint32_t r0 = static_cast<uint32_t>(static_cast<uint64_t>(u.rows) * blockIdx.x / gridDim.x);
   const uint32_t r1 = static_cast<uint32_t>(static_cast<uint64_t>(u.rows) * (blockIdx.x + 1) / gridDim.x);
+  // Passes over this CTA's rows [r0, r1) of M in tiles of TROWS rows, double-buffered: one
+  // TMA bulk copy per tile (the rows are contiguous) issued one tile ahead, when the rank is
+  // a compile-time multiple of 4; else a synchronous strided loop.  body(tile, b, nr).
+  __shared__ __align__(8) uint64_t tbar[2];
+  uint32_t tphase[2] = {0u, 0u};
+  constexpr bool kTma = RT > 0 && RT % 4 == 0;
+  if constexpr (kTma) {
+    if (threadIdx.x == 0) {
+      mbar_init(&tbar[0], 1);
+      mbar_init(&tbar[1], 1);
+      mbar_fence_init();
+    }
+  }
+  auto tile_pass = [&](auto&& body) {
+    float* buf[2] = {tile, tile + TROWS * R};
+    auto issue = [&](uint32_t b, int k) {
+      if (threadIdx.x == 0) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        const uint32_t bytes = min(r1 - b, TROWS) * R * 4u;
+        mbar_arrive_tx(&tbar[k], bytes);
+        const uint8_t* src = reinterpret_cast<const uint8_t*>(u.M + static_cast<size_t>(b) * R);
+        for (uint32_t off = 0; off < bytes; off += 65536u)
+          tma_load_1d(reinterpret_cast<uint8_t*>(buf[k]) + off, src + off, min(bytes - off, 65536u),
+                      &tbar[k]);
+      }
+    };
+    __syncthreads();  // both buffers free
+    if constexpr (kTma)
+      if (r0 < r1) issue(r0, 0);
+    int cur = 0;
+    for (uint32_t b = r0; b < r1; b += TROWS) {
+      const uint32_t nr = min(r1 - b, TROWS);
+      if constexpr (kTma) {
+        if (b + TROWS < r1) issue(b + TROWS, cur ^ 1);  // freed by the previous iteration's barrier
+        mbar_wait(&tbar[cur], tphase[cur]);
+        tphase[cur] ^= 1u;
+      } else {
+        for (uint32_t i = threadIdx.x; i < nr * R; i += blockDim.x)
+          buf[cur][i] = u.M[static_cast<size_t>(b) * R + i];
+        __syncthreads();
+      }
+      body(buf[cur], b, nr);
+      __syncthreads();  // every thread is done with this buffer
+      cur ^= 1;
+    }
+  };
+
   // phase 1: P += MᵀM over this CTA's rows, 2 x 4 register tiles of P per thread
   {
     constexpr bool VEC1 = RT > 0 && RT % 4 == 0;
     constexpr int TPT = ((RMAX + 1) / 2 * ((RMAX + 3) / 4) + NTH - 1) / NTH;
     const uint32_t tc = (R + 3) / 4, ntile = (R + 1) / 2 * tc;
+    // fewer 2x4 tiles than threads (compile-time rank): NSUB thread sets split the rows (row
+    // i to set i % NSUB), each writing its own partial, so every thread works
+    constexpr uint32_t NT_C = RT ? (RT + 1) / 2 * ((RT + 3) / 4) : 0;
+    constexpr uint32_t NSUB = (RT && NT_C <= static_cast<uint32_t>(NTH)) ? NTH / NT_C : 1;
+    const uint32_t sub = NSUB > 1 ? threadIdx.x / NT_C : 0;
+    // the row split pays on big modes only (more partials to reduce): uniform over the grid
+    const uint32_t nsub = u.rows / gridDim.x >= 512u ? NSUB : 1u;
     double acc[TPT][2][4] = {};
-    for (uint32_t b = r0; b < r1; b += kGramRows) {
-      const uint32_t nr = min(r1 - b, static_cast<uint32_t>(kGramRows));
-      __syncthreads();
-      for (uint32_t i = threadIdx.x; i < nr * R; i += blockDim.x)
-        tile[i] = u.M[static_cast<size_t>(b) * R + i];
-      __syncthreads();
+    tile_pass([&](const float* tl, uint32_t, uint32_t nr) {
 #pragma unroll
       for (int q = 0; q < TPT; ++q) {
-        const uint32_t t = threadIdx.x + q * NTH;
-        if (t >= ntile) continue;
+        const uint32_t t = NSUB > 1 ? threadIdx.x % NT_C : threadIdx.x + q * NTH;
+        if (t >= ntile || sub >= nsub) continue;
         const uint32_t ra = (t / tc) * 2, rb = min(ra + 1, R - 1), c0 = (t % tc) * 4;
-        for (uint32_t i = 0; i < nr; ++i) {
-          const float* row = tile + i * R;
+        for (uint32_t i = sub; i < nr; i += nsub) {
+          const float* row = tl + i * R;
           const double a0 = row[ra], a1 = row[rb];
           double bv[4];
           if constexpr (VEC1) {
@@ -385,14 +439,14 @@ __global__ void __launch_bounds__(NTH) k_als_update(const UpdArgs u) {
           }
         }
       }
-    }
+    });
     // this CTA's partial (zeros when it has no rows), reduced in CTA order below: a fixed
     // summation order, so every rank of a sharded ALS (and every run) gets the same P
-    double* part = u.Ppart + static_cast<size_t>(blockIdx.x) * RR;
+    double* part = u.Ppart + (static_cast<size_t>(blockIdx.x) * nsub + sub) * RR;
 #pragma unroll
     for (int q = 0; q < TPT; ++q) {
-      const uint32_t t = threadIdx.x + q * NTH;
-      if (t >= ntile) continue;
+      const uint32_t t = NSUB > 1 ? threadIdx.x % NT_C : threadIdx.x + q * NTH;
+      if (t >= ntile || sub >= nsub) continue;
       const uint32_t ra = (t / tc) * 2, c0 = (t % tc) * 4;
 #pragma unroll
       for (int i = 0; i < 2; ++i)
@@ -421,17 +475,20 @@ __global__ void __launch_bounds__(NTH) k_als_update(const UpdArgs u) {
   {
     const uint32_t p0 = static_cast<uint32_t>(static_cast<uint64_t>(RR) * blockIdx.x / gridDim.x);
     const uint32_t p1 = static_cast<uint32_t>(static_cast<uint64_t>(RR) * (blockIdx.x + 1) / gridDim.x);
-    if (gridDim.x <= 32) {  // few partials (and many entries per CTA): a thread per entry
+    constexpr uint32_t NSUB_R = (RT && (RT + 1) / 2 * ((RT + 3) / 4) <= static_cast<uint32_t>(NTH))
+                                    ? NTH / ((RT + 1) / 2 * ((RT + 3) / 4)) : 1;
+    const uint32_t nparts = gridDim.x * (u.rows / gridDim.x >= 512u ? NSUB_R : 1u);
+    if (nparts <= 32) {  // few partials (and many entries per CTA): a thread per entry
       for (uint32_t p = p0 + threadIdx.x; p < p1; p += blockDim.x) {
         double sum = 0.0;
-        for (uint32_t b = 0; b < gridDim.x; ++b) sum += __ldcg(&u.Ppart[static_cast<size_t>(b) * RR + p]);
+        for (uint32_t b = 0; b < nparts; ++b) sum += __ldcg(&u.Ppart[static_cast<size_t>(b) * RR + p]);
         u.P[p] = sum;
       }
     } else {
       const uint32_t lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
       for (uint32_t p = p0 + w; p < p1; p += nw) {
         double sum = 0.0;
-        for (uint32_t b = lane; b < gridDim.x; b += 32)
+        for (uint32_t b = lane; b < nparts; b += 32)
           sum += __ldcg(&u.Ppart[static_cast<size_t>(b) * RR + p]);
 #pragma unroll
         for (int o = 16; o; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
@@ -507,21 +564,41 @@ __global__ void __launch_bounds__(NTH) k_als_update(const UpdArgs u) {
   }
   __syncthreads();
   stamp(4);
-  // phase 3: Y = M S
-  for (uint32_t b = r0; b < r1; b += kGramRows) {
-    const uint32_t nr = min(r1 - b, static_cast<uint32_t>(kGramRows));
+  // phase 3: Y = M S (at R = 32: lane = rank with its column of S in registers, a warp per
+  // row, the row read as eight broadcast 16-B loads -- FMA-bound instead of two shared-memory
+  // reads per FMA; the same fmaf order over s, so the same bits)
+  float scol[RT == 32 ? 32 : 1];
+  if constexpr (RT == 32) {
     __syncthreads();
-    for (uint32_t i = threadIdx.x; i < nr * R; i += blockDim.x)
-      tile[i] = u.M[static_cast<size_t>(b) * R + i];
-    __syncthreads();
-    for (uint32_t p = threadIdx.x; p < nr * R; p += blockDim.x) {
-      const uint32_t i = p / R, r = p % R;
-      float a = 0.f;
-#pragma unroll 8
-      for (uint32_t s2 = 0; s2 < R; ++s2) a = fmaf(tile[i * R + s2], S[s2 * R + r], a);
-      u.Y[static_cast<size_t>(b) * R + p] = a;
-    }
+#pragma unroll
+    for (int s2 = 0; s2 < 32; ++s2) scol[s2] = S[s2 * 32 + (threadIdx.x & 31)];
   }
+  tile_pass([&](const float* tl, uint32_t b, uint32_t nr) {
+    if constexpr (RT == 32) {
+      const uint32_t lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+      for (uint32_t i = w; i < nr; i += nw) {
+        const float4* row = reinterpret_cast<const float4*>(tl + i * 32);
+        float a = 0.f;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const float4 v = row[q];
+          a = fmaf(v.x, scol[4 * q + 0], a);
+          a = fmaf(v.y, scol[4 * q + 1], a);
+          a = fmaf(v.z, scol[4 * q + 2], a);
+          a = fmaf(v.w, scol[4 * q + 3], a);
+        }
+        u.Y[(static_cast<size_t>(b) + i) * 32 + lane] = a;
+      }
+    } else {
+      for (uint32_t p = threadIdx.x; p < nr * R; p += blockDim.x) {
+        const uint32_t i = p / R, r = p % R;
+        float a = 0.f;
+#pragma unroll 8
+        for (uint32_t s2 = 0; s2 < R; ++s2) a = fmaf(tl[i * R + s2], S[s2 * R + r], a);
+        u.Y[static_cast<size_t>(b) * R + p] = a;
+      }
+    }
+  });
   stamp(5);
 }
 
@@ -531,7 +608,7 @@ template <int RT, int NTH>
 __global__ void __launch_bounds__(NTH) k_als_inverse(const double* __restrict__ grams, uint32_t n,
                                                      uint32_t d, uint32_t Rr, double* vinv,
                                                      int* status) {
-  extern __shared__ double dsm[];
+  extern __shared__ __align__(128) double dsm[];
   const uint32_t R = RT ? RT : Rr, RR = R * R, W2 = 2 * R;
   double* A = dsm;
   double* T = A + 2 * RR;
@@ -543,7 +620,7 @@ __global__ void __launch_bounds__(NTH) k_als_inverse(const double* __restrict__ 
 }
 
 size_t upd_smem(uint32_t R) {
-  return sizeof(double) * (5 * R * R + 2 * R) + sizeof(float) * (R * R + kGramRows * R);
+  return sizeof(double) * (5 * R * R + 2 * R) + sizeof(float) * (R * R + 2 * upd_tile_rows(R) * R);
 }
 
 int blocks_for(uint64_t rows, int sms) {
@@ -608,7 +685,7 @@ void als_update_mode(Context& c, uint32_t d, bool pre_inverse) {
   u.d = d;
   u.grams = c.gram.get();
   u.P = c.mtm.get();
-  c.als_ppart.resize(static_cast<size_t>(c.num_sms) * R * R);
+  c.als_ppart.resize(static_cast<size_t>(c.num_sms) * 8 * R * R);  // grid x NSUB (<= 8) partials
   u.Ppart = c.als_ppart.get();
   u.lambda = c.lambda.get();
   u.scalars = c.als_scalars.get();
