@@ -353,8 +353,13 @@ __global__ void __launch_bounds__(NTH) k_als_update(const UpdArgs u) {
     }
   };
   stamp(0);
-  const uint32_t r0 = static_cast<uint32_t>(static_cast<uint64_t>(u.rows) * blockIdx.x / gridDim.x);
-  const uint32_t r1 = static_cast<uint32_t>(static_cast<uint64_t>(u.rows) * (blockIdx.x + 1) / gridDim.x);
+  // CTA 0 also writes G_d, λ and the fit terms after the redundant R x R work, which would
+  // put that on the launch's critical path: with 8+ CTAs it gets no rows (phases 1 and 3)
+  const bool rowless0 = gridDim.x >= 8;
+  const uint32_t nrc = rowless0 ? gridDim.x - 1 : gridDim.x;  // CTAs with rows
+  const uint32_t bi = rowless0 ? (blockIdx.x == 0 ? nrc : blockIdx.x - 1) : blockIdx.x;
+  const uint32_t r0 = bi >= nrc ? u.rows : static_cast<uint32_t>(static_cast<uint64_t>(u.rows) * bi / nrc);
+  const uint32_t r1 = bi >= nrc ? u.rows : static_cast<uint32_t>(static_cast<uint64_t>(u.rows) * (bi + 1) / nrc);
   // Passes over this CTA's rows [r0, r1) of M in tiles of TROWS rows, double-buffered: one
   // TMA bulk copy per tile (the rows are contiguous) issued one tile ahead, when the rank is
   // a compile-time multiple of 4; else a synchronous strided loop.  body(tile, b, nr).
