@@ -485,16 +485,33 @@ __global__ void __launch_bounds__(NTH) k_als_update(const UpdArgs u) {
     const uint32_t nparts = gridDim.x * (u.rows / gridDim.x >= 512u ? NSUB_R : 1u);
     if (nparts <= 32) {  // few partials (and many entries per CTA): a thread per entry
       for (uint32_t p = p0 + threadIdx.x; p < p1; p += blockDim.x) {
+        // eight partials' loads in flight at a time (an L2 round trip per eight, not per
+        // partial), summed in the same order
         double sum = 0.0;
-        for (uint32_t b = 0; b < nparts; ++b) sum += __ldcg(&u.Ppart[static_cast<size_t>(b) * RR + p]);
+        for (uint32_t b0 = 0; b0 < nparts; b0 += 8) {
+          double v[8];
+#pragma unroll
+          for (uint32_t j = 0; j < 8; ++j)
+            v[j] = b0 + j < nparts ? __ldcg(&u.Ppart[static_cast<size_t>(b0 + j) * RR + p]) : 0.0;
+#pragma unroll
+          for (uint32_t j = 0; j < 8; ++j)
+            if (b0 + j < nparts) sum += v[j];
+        }
         u.P[p] = sum;
       }
     } else {
       const uint32_t lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
       for (uint32_t p = p0 + w; p < p1; p += nw) {
         double sum = 0.0;
-        for (uint32_t b = lane; b < nparts; b += 32)
-          sum += __ldcg(&u.Ppart[static_cast<size_t>(b) * RR + p]);
+        for (uint32_t b0 = lane; b0 < nparts; b0 += 4 * 32) {  // four loads in flight per lane
+          double v[4];
+#pragma unroll
+          for (uint32_t j = 0; j < 4; ++j)
+            v[j] = b0 + 32 * j < nparts ? __ldcg(&u.Ppart[static_cast<size_t>(b0 + 32 * j) * RR + p]) : 0.0;
+#pragma unroll
+          for (uint32_t j = 0; j < 4; ++j)
+            if (b0 + 32 * j < nparts) sum += v[j];
+        }
 #pragma unroll
         for (int o = 16; o; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
         if (lane == 0) u.P[p] = sum;
